@@ -1,0 +1,461 @@
+#!/usr/bin/env python3
+"""Benchmark: batched bicluster-fitness evaluation on B200 (EBIC hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c2|c4|c5] [--shard rows|pop]
+
+A STEP is one pass of the hot path over one batch: evaluate_population of P
+candidates against all R rows (trend.cpp:56-72), i.e. P fitness evals and P*R
+row-checks.  Metric (BASELINE.json): candidate fitness evals/s (row-checks/s
+reported alongside), % of the HBM roofline.
+
+Default workload = BASELINE configs[2] ("c3"): 20k x 1000 planted-trend float32
+matrix, P = 16384 (L uniform in [3,5]), approx 0.03.  BASELINE's metric and both
+of its numeric targets (>= 60% HBM roofline at 20k x 1000; >= 6x at 8 GPUs
+row-sharded) are quoted on this configuration; configs[1] is the bit-exact
+parity case (tests/test_gpu_parity.py::test_config2_bit_exact).
+
+N > 1 (torchrun, one process per GPU): rows are sharded across ranks and the
+per-candidate partial counts are summed with one NCCL all_reduce per step
+(strong scaling: the total work is fixed).
+
+value    : device-resident inputs (population CSR already in HBM), per-step CUDA
+           events on the launching stream around kernel + all_reduce; L2 is
+           flushed (512 MiB write, untimed) before every timed step.
+e2e      : the same metric through the public host API (ebic_eval_counts via
+           Evaluator.evaluate_population / ShardedEvaluator): host CSR copied to
+           pinned staging and H2D, counts D2H, every step inside the timed region.
+roofline : algorithmic bytes 4*L*R per eval / average fitness-kernel
+           time (CUDA events), vs the measured HBM copy bandwidth.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "candidate fitness evals/s & row-checks/s at 1/2/4/8 B200; % of HBM roofline"
+
+CONFIGS = {
+    # name: rows, cols, population, len range, approx, negative, planted (rows, cols)
+    "c2": dict(rows=10_000, cols=500, pop=4096, len_min=3, len_max=5, approx=0.03, negative=False, bic=(500, 20),
+               label="c2: 10k x 500 planted-trend f32 matrix, P=4096 (L in [3,5]), approx 0.03"),
+    "c3": dict(rows=20_000, cols=1000, pop=16384, len_min=3, len_max=5, approx=0.03, negative=False, bic=(500, 20),
+               label="c3: 20k x 1000 planted-trend f32 matrix, P=16384 (L in [3,5]), approx 0.03"),
+    "c4": dict(rows=200_000, cols=2000, pop=32768, len_min=3, len_max=5, approx=0.03, negative=False,
+               bic=(5000, 20),
+               label="c4: 200k x 2000 planted-trend f32 matrix (1.6 GB), P=32768 (L in [3,5]), approx 0.03"),
+    "c5": dict(rows=1_000_000, cols=64, pop=1024, len_min=16, len_max=16, approx=0.03, negative=False,
+               bic=(10_000, 16),
+               label="c5 microbench point: 1M x 64 f32, P=1024, L=16, approx 0.03"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config: str, world: int):
+    """dram read+write bytes per launch of the fitness kernel from the committed ncu capture."""
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        rec = d.get(config)
+        if rec and world == 1:
+            return rec["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(f[1]), smax=float(f[2]), hw=f[5], hwt=f[6], swt=f[7], pcap=f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = []
+        for key, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
+                          ("pcap", "sw_power_cap")):
+            if any(r[key].lower() == "active" for r in rows):
+                reasons.append(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows), "sm_max_mhz": max(r["smax"] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_inputs(cfg, n_pops: int):
+    from paper_2105_01196_b200 import synth
+
+    m, _ = synth.planted_trend_matrix(cfg["rows"], cfg["cols"], 3, cfg["bic"][0], cfg["bic"][1], seed=1)
+    if cfg["len_min"] == cfg["len_max"]:
+        pops = [synth.exact_len_population(cfg["pop"], cfg["cols"], cfg["len_min"], seed=42 + i) for i in range(n_pops)]
+    else:
+        pops = [synth.random_population(cfg["pop"], cfg["cols"], cfg["len_min"], cfg["len_max"], seed=42 + i)
+                for i in range(n_pops)]
+    return m, pops
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own evaluate_population on a WorkerPool
+# (oracle/_ref, "reference") or the C restatement ("port"), all host threads.
+# ---------------------------------------------------------------------------
+def cpu_eval_setup(m: np.ndarray):
+    import oracle
+
+    if oracle.reference_available():
+        mat = oracle.RefMatrix(m.astype(np.float64))
+        pool = oracle.RefPool(0)
+
+        def run(pop):
+            rp = oracle.RefPopulation(pop.cols, pop.offsets)
+            return oracle.ref_evaluate(mat, rp, CUR_APPROX[0], CUR_NEG[0], pool)
+
+        return run, "reference", pool.size
+    threads = oracle.port().oracle_threads()
+
+    def run(pop):
+        return oracle.evaluate_population(m, pop.cols, pop.offsets, CUR_APPROX[0], CUR_NEG[0], threads=threads)
+
+    return run, "port", threads
+
+
+CUR_APPROX = [0.03]
+CUR_NEG = [False]
+
+
+def cpu_sample(run, pop, budget_s: float):
+    """Evaluate a prefix of `pop` sized to ~budget_s seconds; returns (n, seconds, counts)."""
+    from paper_2105_01196_b200.shard import slice_population
+
+    n = min(len(pop), 32)
+    t0 = time.perf_counter()
+    run(slice_population(pop, 0, n))
+    probe = time.perf_counter() - t0
+    n = int(max(1, min(len(pop), n * budget_s / max(probe, 1e-6))))
+    sub = slice_population(pop, 0, n)
+    t0 = time.perf_counter()
+    counts = run(sub)
+    return n, time.perf_counter() - t0, counts
+
+
+def bench_reference(args, cfg, rank):
+    if rank != 0:
+        return 0
+    CUR_APPROX[0], CUR_NEG[0] = cfg["approx"], cfg["negative"]
+    m, pops = make_inputs(cfg, 1)
+    run, kind, cores = cpu_eval_setup(m)
+    pop = pops[0]
+    per_step = float(os.environ.get("EBIC_REF_STEP_S", "3.0"))
+    for _ in range(args.warmup):
+        cpu_sample(run, pop, min(per_step, 1.0))
+    tot_n, tot_t = 0, 0.0
+    n_step = None
+    for _ in range(args.steps):
+        if n_step is None:
+            n_step, t, _ = cpu_sample(run, pop, per_step)
+        else:
+            from paper_2105_01196_b200.shard import slice_population
+
+            sub = slice_population(pop, 0, n_step)
+            t0 = time.perf_counter()
+            run(sub)
+            t = time.perf_counter() - t0
+        tot_n += n_step
+        tot_t += t
+    value = tot_n / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "row_checks_per_s": value * cfg["rows"],
+        "config": {"workload": cfg["label"], "rows": cfg["rows"], "cols": cfg["cols"], "population": cfg["pop"],
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": kind,
+                         "sample": f"{n_step} of {cfg['pop']} candidates x all {cfg['rows']} rows per step "
+                                   f"(reference evaluate_population on WorkerPool({cores}))" if kind == "reference"
+                         else f"{n_step} of {cfg['pop']} candidates per step (C restatement, {cores} threads)"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def bench_ours(args, cfg, rank, world, local_rank, dist):
+    import torch
+
+    from paper_2105_01196_b200 import Evaluator, TrendParams
+    from paper_2105_01196_b200.shard import ShardedEvaluator, row_range
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tp = TrendParams(approx=cfg["approx"], negative_trends=cfg["negative"])
+    n_pops = 4
+    m, pops = make_inputs(cfg, n_pops)
+    R, Ccols, P = cfg["rows"], cfg["cols"], cfg["pop"]
+    b, e = row_range(R, rank, world) if args.shard == "rows" else (0, R)
+
+    ev = Evaluator(local_rank)
+    ev.upload(np.ascontiguousarray(m[b:e]), row_base=b)
+    stream = torch.cuda.current_stream(dev)
+    ev.set_stream(stream.cuda_stream)
+
+    # device-resident populations
+    d_pops = []
+    for pop in pops:
+        if args.shard == "pop":
+            from paper_2105_01196_b200.shard import pop_range, slice_population
+
+            pb, pe = pop_range(len(pop), rank, world)
+            pop = slice_population(pop, pb, pe)
+        d_pops.append((torch.from_numpy(pop.cols.view(np.int32)).to(dev),
+                       torch.from_numpy(pop.offsets.view(np.int32)).to(dev), len(pop), int(pop.cols.size)))
+    counts_full = torch.zeros(P, dtype=torch.int32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(i, ev_k0=None, ev_k1=None):
+        dc, do, n, _ = d_pops[i % n_pops]
+        out = counts_full[:n] if args.shard == "pop" else counts_full
+        if ev_k0 is not None:
+            ev_k0.record(stream)
+        ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp, stream=stream.cuda_stream)
+        if ev_k1 is not None:
+            ev_k1.record(stream)
+        if world > 1:
+            if args.shard == "rows":
+                dist.all_reduce(counts_full, op=dist.ReduceOp.SUM)
+            else:
+                gathered = [torch.empty_like(counts_full[:n]) for _ in range(world)]
+                dist.all_gather(gathered, counts_full[:n])
+
+    # warmup
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = ev.launch_count()
+    cvd = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+    clocks = ClockSampler(cvd[local_rank] if local_rank < len(cvd) else str(local_rank))
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with clocks:
+        w0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush (untimed: outside the step events)
+            starts[i].record(stream)
+            step(i, k0[i], k1[i])
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        wall = time.perf_counter() - w0
+    launches = ev.launch_count() - launches0
+    step_ms = [s.elapsed_time(t) for s, t in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(t) for s, t in zip(k0, k1)]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = P / (ms_per_step / 1e3)
+
+    # roofline of the fitness kernel on this rank
+    sum_len = [int(dp[3]) for dp in d_pops]
+    alg_bytes = [4.0 * (e - b) * sl for sl in sum_len]
+    per_step_bytes = [alg_bytes[i % n_pops] for i in range(args.steps)]
+    kern_avg_s = statistics.mean(kern_ms) / 1e3
+    achieved = statistics.mean(bb / (km / 1e3) for bb, km in zip(per_step_bytes, kern_ms)) / 1e9
+    peak, peak_src = measured_peak()
+
+    # ---- e2e through the public host API -----------------------------------
+    e2e_ms = []
+    if world > 1:
+        sev = ShardedEvaluator(ev, m, mode=args.shard, dist=dist)
+        call = sev.evaluate_population
+    else:
+        call = ev.evaluate_population
+    ev.set_stream(None)
+    for i in range(3):
+        call(pops[i % n_pops], tp)
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        host_counts = call(pops[i % n_pops], tp)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_tot = sum(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_value = P / (e2e_tot / args.steps / 1e3)
+    pop0 = pops[0]
+    h2d = int(pop0.cols.nbytes + pop0.offsets.nbytes)
+    d2h = 4 * P
+
+    # parity spot-check of the device-resident result against the host-API result
+    ev.set_stream(stream.cuda_stream)
+    step(0)
+    torch.cuda.synchronize()
+    dev_counts = counts_full.cpu().numpy().view(np.uint32)
+    ev.set_stream(None)
+    host0 = call(pops[0], tp)
+    parity_dev_vs_host = bool(np.array_equal(dev_counts[:len(host0)], host0)) if args.shard == "rows" else None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if args.shard == "rows" else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "row_checks_per_s": value * R,
+        "config": {"workload": cfg["label"], "rows": R, "cols": Ccols, "population": P,
+                   "parallelism": f"{args.shard}-sharded x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed before every timed step (512 MiB device write, outside the step events)",
+                   "shard": args.shard},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.config, world),
+                     "kernel": "fitness_count_kernel", "kernel_avg_ms": kern_avg_s * 1e3,
+                     "algorithmic_bytes_per_launch": statistics.mean(alg_bytes),
+                     "peak_source": peak_src,
+                     "note": "algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "
+                             "the matrix is re-read from L2 by many candidates, so achieved can exceed HBM peak"},
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_tot / args.steps,
+                "api": "ebic_eval_counts (Evaluator.evaluate_population)" if world == 1
+                       else f"ShardedEvaluator({args.shard}) over ebic_eval_counts + NCCL"},
+        "gpu_launches": int(launches),
+        "wall_ms_timed_region": wall * 1e3,
+        "parity_device_vs_host_api": parity_dev_vs_host,
+    }
+    with_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    if with_cpu:
+        CUR_APPROX[0], CUR_NEG[0] = cfg["approx"], cfg["negative"]
+        run, kind, cores = cpu_eval_setup(m)
+        n, t, cpu_counts = cpu_sample(run, pops[0], float(os.environ.get("EBIC_CPU_BUDGET_S", "12")))
+        gpu_counts = host_counts if len(pops) == 1 else call(pops[0], tp)
+        line["cpu_baseline"] = {
+            "value": n / t, "unit": "evals/s", "cores": cores, "kind": kind,
+            "sample": f"first {n} of {P} candidates of population 0 x all {R} rows, {t:.1f} s "
+                      + ("(unmodified reference evaluate_population on WorkerPool)" if kind == "reference"
+                         else "(C restatement of trend.cpp, pthreads)"),
+            "parity_with_gpu": bool(np.array_equal(cpu_counts, gpu_counts[:n])),
+        }
+    line["clocks"] = clocks.summary()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ev.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--shard", choices=["rows", "pop"], default="rows")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return bench_reference(args, cfg, rank)
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    try:
+        return bench_ours(args, cfg, rank, world, local_rank, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,160 @@
+/*
+ * ebic.h -- C ABI of the B200 batched bicluster-fitness evaluator.
+ *
+ * This is the drop-in boundary for the reference's trend/fitness engine
+ * (/root/reference/proj/include/bicseek/trend.hpp).  The reference has no FFI
+ * of its own: its seam is link-time substitution of the free functions in
+ * trend.hpp.  The C++ TU paper_2105_01196_b200/csrc/bicseek_trend_device.cpp
+ * implements those functions over this ABI, and the
+ * Python mirror (paper_2105_01196_b200/trend.py) binds it with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types.
+ *   - Every entry point returns an int status: EBIC_OK (0) or an EBIC_ERR_*
+ *     code.  ebic_last_error() returns a thread-local message for the last
+ *     failure on the calling thread.
+ *   - A context (ebic_ctx) owns one CUDA device, one stream, one resident
+ *     matrix shard and the pinned staging buffers.  Contexts are independent
+ *     and may be used concurrently from different threads; a single context
+ *     must not be used by two threads at once (like the reference WorkerPool,
+ *     worker_pool.hpp:32).
+ *   - Populations are CSR: candidate i is the column sequence
+ *     cols[offsets[i] .. offsets[i+1]) (reference: std::vector<Chromosome>,
+ *     bicluster.hpp:13-24).  Column indices are uint32, in visiting order.
+ *   - Row indices returned by the row-membership calls are GLOBAL
+ *     (row_base + local row), ascending.
+ *
+ * Numerics: results are bit-exact with the reference CPU path
+ * (trend.cpp:17-46, double-precision `cur > prev - approx*|prev|` with two
+ * rounded ops) for every input the store accepts.  A float32 store is used
+ * only when every value is float32-representable; otherwise the store keeps
+ * float64 (EBIC_STORE_AUTO), so there is no silent precision loss and no CPU
+ * fallback.
+ */
+#ifndef EBIC_H_
+#define EBIC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBIC_ABI_VERSION 1
+
+/* status codes */
+#define EBIC_OK 0
+#define EBIC_ERR_INVALID_ARGUMENT 1 /* bad sizes, out-of-range column, empty candidate, non-finite value */
+#define EBIC_ERR_CUDA 2             /* CUDA runtime / launch failure (message has the CUDA error string) */
+#define EBIC_ERR_NO_MATRIX 3        /* no matrix uploaded in this context */
+#define EBIC_ERR_CAPACITY 4         /* output buffer too small; required size returned */
+#define EBIC_ERR_NOT_EXACT 5        /* EBIC_STORE_F32 requested for a matrix that is not f32-representable */
+#define EBIC_ERR_NO_DEVICE 6        /* no CUDA device / bad device ordinal */
+
+/* matrix store precision */
+#define EBIC_STORE_AUTO 0 /* float32 if every value is exactly representable, else float64 */
+#define EBIC_STORE_F32 1  /* float32 (column-major, rows padded to 32); error if not exact */
+#define EBIC_STORE_F64 2  /* float64 (column-major, rows padded to 32) */
+
+typedef struct ebic_ctx ebic_ctx;
+
+/* ---- library / context ------------------------------------------------- */
+
+int ebic_abi_version(void);
+/* Thread-local message describing the last non-OK status on this thread. */
+const char* ebic_last_error(void);
+/* Number of visible CUDA devices (0 if none). */
+int ebic_device_count(int* n_out);
+
+/* Create a context on `device`.  Owns a non-blocking CUDA stream. */
+int ebic_ctx_create(int device, ebic_ctx** ctx_out);
+int ebic_ctx_destroy(ebic_ctx* ctx);
+/* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream) for
+ * every subsequent launch; NULL restores the context's own stream. */
+int ebic_ctx_set_stream(ebic_ctx* ctx, void* cuda_stream);
+/* Block until all work queued by this context has finished; also reports any
+ * device-side argument error recorded by the *_device entry points. */
+int ebic_ctx_sync(ebic_ctx* ctx);
+
+/* ---- device-resident matrix store (reference: ExpressionMatrix,
+ *      matrix.hpp:13-43, row-major double) ----------------------------------- */
+
+/* Upload `n_rows` x `n_cols` row-major doubles (a whole matrix, or the row
+ * shard [row_base, row_base + n_rows) of a larger one).  Transposes on device
+ * to column-major with rows padded to a multiple of 32.  Non-finite values
+ * are rejected (matrix.cpp:41-42).  *store_out (optional) receives the chosen
+ * EBIC_STORE_F32 / EBIC_STORE_F64.  Replaces any previous matrix. */
+int ebic_matrix_upload_f64(ebic_ctx* ctx, const double* row_major, uint64_t n_rows,
+                           uint64_t n_cols, uint64_t row_base, int store, int* store_out);
+/* Same for row-major float32 input (always exact; stored as float32). */
+int ebic_matrix_upload_f32(ebic_ctx* ctx, const float* row_major, uint64_t n_rows,
+                           uint64_t n_cols, uint64_t row_base);
+/* Shape of the resident matrix.  Any out pointer may be NULL. */
+int ebic_matrix_info(ebic_ctx* ctx, uint64_t* n_rows, uint64_t* n_cols, uint64_t* ld,
+                     int* store, uint64_t* row_base);
+int ebic_matrix_free(ebic_ctx* ctx);
+
+/* ---- fitness counts (reference: evaluate_population, trend.cpp:56-72) ---- */
+
+/* Host pointers, synchronous.  counts_out[i] = number of rows r of the
+ * resident matrix (shard) with row_supports(r, candidate i).  Validates every
+ * column index and candidate length (>= 1) on the host before launching. */
+int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
+                     uint64_t n_cand, double approx, int negative_trends, uint32_t* counts_out);
+
+/* Device pointers, asynchronous on `stream` (NULL = the context's stream).
+ * d_counts is overwritten.  Invalid columns / empty candidates are detected on
+ * device, counted as 0 and reported by the next ebic_ctx_sync(). */
+int ebic_eval_counts_device(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
+                            uint64_t n_cand, double approx, int negative_trends,
+                            uint32_t* d_counts, void* stream);
+
+/* Batch marshaller: asynchronous host-pointer evaluation through pinned
+ * staging slots (ring of EBIC_MARSHAL_SLOTS).  The caller's host arrays are
+ * copied into pinned memory before return, so they may be reused at once;
+ * counts_out is written when ebic_eval_wait(ticket) returns.  Lets the
+ * host-side GA breed the next chunk while this one is evaluated. */
+#define EBIC_MARSHAL_SLOTS 4
+int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
+                     uint64_t n_cand, double approx, int negative_trends, uint32_t* counts_out,
+                     uint64_t* ticket_out);
+int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket);
+
+/* ---- row membership (reference: supporting_rows trend.cpp:48-54,
+ *      row_supports trend.cpp:41-46) --------------------------------------- */
+
+/* Ascending global rows supporting one candidate.  *n_out receives the full
+ * count; if it exceeds `cap`, returns EBIC_ERR_CAPACITY and writes nothing. */
+int ebic_support_rows(ebic_ctx* ctx, const uint32_t* cols, uint32_t len, double approx,
+                      int negative_trends, uint32_t* rows_out, uint64_t cap, uint64_t* n_out);
+
+/* Batched variant (one launch sequence for a whole archive): rows of
+ * candidate i land in rows_out[row_offsets[i] .. row_offsets[i+1]).
+ * row_offsets has n_cand + 1 entries.  If the total exceeds `cap`, returns
+ * EBIC_ERR_CAPACITY with row_offsets filled and rows_out untouched. */
+int ebic_support_rows_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
+                            uint64_t n_cand, double approx, int negative_trends,
+                            uint32_t* rows_out, uint64_t cap, uint64_t* row_offsets);
+
+/* Single (row, candidate) predicate on device.  `row` is a GLOBAL row index
+ * inside the resident shard. */
+int ebic_row_supports(ebic_ctx* ctx, uint64_t row, const uint32_t* cols, uint32_t len,
+                      double approx, int negative_trends, int* supports_out);
+
+/* ---- score (reference: fitness trend.cpp:74-79; host arithmetic, exact) -- */
+double ebic_fitness(uint64_t support_count, uint64_t num_cols, uint64_t min_rows,
+                    uint64_t col_cap);
+
+/* ---- instrumentation ---------------------------------------------------- */
+
+/* Number of kernels this context has launched since creation. */
+int ebic_ctx_launch_count(ebic_ctx* ctx, uint64_t* n_out);
+/* Tuning knob for the fitness kernel: rows per CTA slab (0 = auto). */
+int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EBIC_H_ */

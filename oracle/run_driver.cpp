@@ -1,0 +1,84 @@
+// run_driver.cpp -- end-to-end parity driver for BASELINE config 1 (test
+// infrastructure).  Generates a planted-trend scenario with the reference
+// generator (datagen.cpp:208-264), float32-quantises it, and calls the
+// reference's own bicseek::run (evolution.cpp:305-333).  oracle/Makefile links
+// it twice against the SAME unmodified evolution.cpp:
+//   oracle/_ref/run_ref     with the reference trend.cpp      (CPU evaluator)
+//   oracle/_ref/run_device  with bicseek_trend_device.cpp     (B200 evaluator)
+// and tests/test_run_parity.py requires byte-identical output.
+//
+// Output (stdout, one JSON object): the canonical bicluster JSON of
+// io.cpp:131-150 (restated), generations, termination, evaluation count.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "bicseek/datagen.hpp"
+#include "bicseek/evolution.hpp"
+
+using namespace bicseek;
+
+static std::string bics_json(const BiclusterSet& set) {
+  std::string out = "{\"biclusters\":[";
+  for (std::size_t i = 0; i < set.size(); ++i) {
+    if (i) out += ',';
+    out += "{\"rows\":[";
+    const auto& b = set.biclusters[i];
+    for (std::size_t k = 0; k < b.rows.size(); ++k) out += (k ? "," : "") + std::to_string(b.rows[k]);
+    out += "],\"cols\":[";
+    for (std::size_t k = 0; k < b.cols.size(); ++k) out += (k ? "," : "") + std::to_string(b.cols[k]);
+    out += "]}";
+  }
+  out += "]}";
+  return out;
+}
+
+int main(int argc, char** argv) {
+  ScenarioSpec s;
+  s.scenario = ScenarioKind::six_types;
+  s.pattern = PatternKind::trend;
+  s.matrix_rows = 500;
+  s.matrix_cols = 100;
+  s.bic_rows = 50;
+  s.bic_cols = 8;
+  s.num_biclusters = 3;
+  s.seed = 1;
+  EvolutionParams p;
+  p.max_iterations = 200;
+  bool quantize = true;
+  for (int i = 1; i + 1 < argc; i += 2) {
+    const std::string k = argv[i];
+    const char* v = argv[i + 1];
+    if (k == "--rows") s.matrix_rows = std::strtoull(v, nullptr, 10);
+    else if (k == "--cols") s.matrix_cols = std::strtoull(v, nullptr, 10);
+    else if (k == "--bic-rows") s.bic_rows = std::strtoull(v, nullptr, 10);
+    else if (k == "--bic-cols") s.bic_cols = std::strtoull(v, nullptr, 10);
+    else if (k == "--num-bics") s.num_biclusters = std::strtoull(v, nullptr, 10);
+    else if (k == "--noise") s.noise_sigma = std::strtod(v, nullptr);
+    else if (k == "--data-seed") s.seed = std::strtoull(v, nullptr, 10);
+    else if (k == "--pop") p.population_size = std::strtoull(v, nullptr, 10);
+    else if (k == "--iters") p.max_iterations = std::strtoull(v, nullptr, 10);
+    else if (k == "--tabu") p.tabu_hits_threshold = std::strtoull(v, nullptr, 10);
+    else if (k == "--seed") p.seed = std::strtoull(v, nullptr, 10);
+    else if (k == "--threads") p.threads = static_cast<unsigned>(std::strtoul(v, nullptr, 10));
+    else if (k == "--approx") p.trend.approx = std::strtod(v, nullptr);
+    else if (k == "--negative") p.trend.negative_trends = std::atoi(v) != 0;
+    else if (k == "--quantize") quantize = std::atoi(v) != 0;
+    else {
+      std::fprintf(stderr, "unknown option %s\n", k.c_str());
+      return 2;
+    }
+  }
+  GeneratedDataset d = gen_scenario(s);
+  std::vector<double> v = d.matrix.values();
+  if (quantize)
+    for (double& x : v) x = static_cast<double>(static_cast<float>(x));
+  const ExpressionMatrix m(std::move(v), d.matrix.rows(), d.matrix.cols(), d.matrix.row_labels(),
+                           d.matrix.col_labels());
+  const RunResult r = run(m, p);
+  std::printf("{\"result\":%s,\"generations\":%zu,\"termination\":\"%s\",\"wall_s\":%.6f}\n",
+              bics_json(r.biclusters).c_str(), r.report.generations, r.report.termination.c_str(),
+              r.report.wall_time_seconds);
+  return 0;
+}

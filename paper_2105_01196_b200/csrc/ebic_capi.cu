@@ -1,0 +1,622 @@
+// ebic_capi.cu -- host side of the C ABI declared in include/ebic.h.
+//
+// Replaces the reference's CPU evaluator (trend.cpp:48-72 on the WorkerPool of
+// worker_pool.cpp:20-48) with: a device-resident column-major matrix store, the
+// fitness_count / mask+scatter kernels of ebic_kernels.cuh, and a pinned-memory
+// batch marshaller on one CUDA stream per context.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ebic.h"
+#include "ebic_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define EBIC_CUDA(call)                                                                    \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(EBIC_ERR_CUDA, "%s:%d: %s: %s", __FILE__, __LINE__, #call,               \
+                  cudaGetErrorString(e_));                                                 \
+  } while (0)
+
+#define EBIC_TRY(expr)            \
+  do {                            \
+    int s_ = (expr);              \
+    if (s_ != EBIC_OK) return s_; \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+template <typename T>
+struct HostBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+template <typename T>
+int ensure(DevBuf<T>& b, size_t n) {
+  if (b.n >= n && b.p) return EBIC_OK;
+  b.release();
+  size_t cap = std::max<size_t>(n, 1024);
+  EBIC_CUDA(cudaMalloc(&b.p, cap * sizeof(T)));
+  b.n = cap;
+  return EBIC_OK;
+}
+
+template <typename T>
+int ensure(HostBuf<T>& b, size_t n) {
+  if (b.n >= n && b.p) return EBIC_OK;
+  b.release();
+  size_t cap = std::max<size_t>(n, 1024);
+  EBIC_CUDA(cudaMallocHost(&b.p, cap * sizeof(T)));
+  b.n = cap;
+  return EBIC_OK;
+}
+
+struct Slot {
+  HostBuf<uint32_t> h_cols, h_offs, h_counts;
+  DevBuf<uint32_t> d_cols, d_offs, d_counts;
+  cudaEvent_t done = nullptr;
+  uint64_t ticket = 0;   // ticket currently occupying the slot (0 = free)
+  uint32_t* user_counts = nullptr;
+  uint64_t n_cand = 0;
+};
+
+}  // namespace
+
+struct ebic_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // active stream (own or external)
+  // matrix store
+  void* d_mat = nullptr;
+  int store = 0;  // EBIC_STORE_F32 / EBIC_STORE_F64 (0 = none)
+  uint64_t n_rows = 0, n_cols = 0, ld = 0, row_base = 0;
+  // scratch
+  int* d_err = nullptr;
+  int* d_flags = nullptr;
+  int* d_out1 = nullptr;
+  DevBuf<uint32_t> d_mask, d_rows, d_tmp_cols, d_tmp_offs, d_tmp_counts;
+  DevBuf<uint64_t> d_row_offsets;
+  HostBuf<uint32_t> h_tmp_counts;
+  Slot slots[EBIC_MARSHAL_SLOTS];
+  uint64_t next_ticket = 1;
+  uint64_t launches = 0;
+  uint32_t slab_rows = 0;  // 0 = auto
+};
+
+namespace {
+
+int set_device(ebic_ctx* ctx) {
+  EBIC_CUDA(cudaSetDevice(ctx->device));
+  return EBIC_OK;
+}
+
+ebic::TrendArgs make_args(double approx, int neg) {
+  ebic::TrendArgs ta;
+  ta.approx = approx;
+  ta.a_f = (float)approx;
+  // bracket half-width scale >= (1+|a|) * 2^-20; rounded up by a small factor
+  ta.kscale = (float)((1.0 + std::fabs(approx)) * 0x1p-20 * 1.0001);
+  ta.negative = neg ? 1 : 0;
+  return ta;
+}
+
+int check_approx(double approx) {
+  if (!std::isfinite(approx)) return fail(EBIC_ERR_INVALID_ARGUMENT, "approx must be finite");
+  return EBIC_OK;
+}
+
+uint32_t pick_slab_rows(const ebic_ctx* ctx, uint64_t n_cand) {
+  if (ctx->slab_rows) return ctx->slab_rows;
+  // enough CTAs to fill 148 SMs several times, slabs small enough that the
+  // concurrently resident working set (slab x all columns) stays in L2.
+  const uint64_t groups = (n_cand + ebic::kWarps - 1) / ebic::kWarps;
+  uint64_t slab = 2048;
+  while (slab > ebic::kRowAlign && groups * ((ctx->n_rows + slab - 1) / slab) < 148 * 8) slab /= 2;
+  return (uint32_t)std::max<uint64_t>(slab, ebic::kRowAlign);
+}
+
+template <typename T, int MODE, bool NEG, bool MASK>
+void launch_count_t(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand,
+                    const ebic::TrendArgs& ta, uint32_t* d_counts, uint32_t* d_mask,
+                    cudaStream_t s) {
+  const uint32_t slab = pick_slab_rows(ctx, n_cand);
+  dim3 grid((unsigned)((n_cand + ebic::kWarps - 1) / ebic::kWarps),
+            (unsigned)((ctx->n_rows + slab - 1) / slab));
+  ebic::fitness_count_kernel<T, MODE, NEG, MASK><<<grid, ebic::kThreads, 0, s>>>(
+      static_cast<const T*>(ctx->d_mat), ctx->ld, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols,
+      d_cols, d_offs, (uint32_t)n_cand, slab, ta, d_counts, d_mask, ctx->d_err);
+  ctx->launches++;
+}
+
+template <bool MASK>
+int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand,
+                 double approx, int neg, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+  if (n_cand == 0) return EBIC_OK;
+  if (n_cand > 0xffffffffull / 2) return fail(EBIC_ERR_INVALID_ARGUMENT, "too many candidates");
+  const ebic::TrendArgs ta = make_args(approx, neg);
+  const bool a0 = (approx == 0.0);
+  if (ctx->store == EBIC_STORE_F32) {
+    if (a0) {
+      if (neg) launch_count_t<float, ebic::kModeNative, true, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+      else     launch_count_t<float, ebic::kModeNative, false, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+    } else {
+      if (neg) launch_count_t<float, ebic::kModeFilter, true, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+      else     launch_count_t<float, ebic::kModeFilter, false, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+    }
+  } else {
+    if (a0) {
+      if (neg) launch_count_t<double, ebic::kModeNative, true, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+      else     launch_count_t<double, ebic::kModeNative, false, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+    } else {
+      if (neg) launch_count_t<double, ebic::kModeF64, true, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+      else     launch_count_t<double, ebic::kModeF64, false, MASK>(ctx, d_cols, d_offs, n_cand, ta, d_counts, d_mask, s);
+    }
+  }
+  EBIC_CUDA(cudaGetLastError());
+  return EBIC_OK;
+}
+
+// Host-side validation of a CSR population (trend.hpp callers pass valid
+// chromosomes; bicluster.cpp:8-15 is the reference's validity rule, but
+// evaluate_population itself accepts duplicates and any length >= 1).
+int validate_population(const ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
+                        uint64_t n_cand) {
+  if (n_cand && (!cols || !offsets)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null population pointer");
+  if (n_cand && offsets[0] != 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "offsets[0] must be 0");
+  for (uint64_t i = 0; i < n_cand; ++i) {
+    if (offsets[i + 1] <= offsets[i])
+      return fail(EBIC_ERR_INVALID_ARGUMENT, "candidate %llu is empty or offsets decrease",
+                  (unsigned long long)i);
+    for (uint32_t k = offsets[i]; k < offsets[i + 1]; ++k)
+      if (cols[k] >= ctx->n_cols)
+        return fail(EBIC_ERR_INVALID_ARGUMENT, "candidate %llu: column %u out of range (cols=%llu)",
+                    (unsigned long long)i, cols[k], (unsigned long long)ctx->n_cols);
+  }
+  return EBIC_OK;
+}
+
+int need_matrix(const ebic_ctx* ctx) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (!ctx->d_mat) return fail(EBIC_ERR_NO_MATRIX, "no matrix uploaded in this context");
+  return EBIC_OK;
+}
+
+template <typename TI>
+int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols, uint64_t row_base,
+                int store, int* store_out) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (!host && n_rows * n_cols) return fail(EBIC_ERR_INVALID_ARGUMENT, "null matrix pointer");
+  if (n_rows == 0 || n_cols == 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "matrix must be non-empty");
+  if (n_rows >= (1ull << 31) || n_cols >= (1ull << 31) || row_base + n_rows >= (1ull << 32))
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "matrix too large for 32-bit row/column indices");
+  if (store < EBIC_STORE_AUTO || store > EBIC_STORE_F64)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "bad store mode %d", store);
+  EBIC_TRY(set_device(ctx));
+  ebic_matrix_free(ctx);
+  cudaStream_t s = ctx->stream;
+  const uint64_t n = n_rows * n_cols;
+
+  TI* d_in = nullptr;
+  EBIC_CUDA(cudaMalloc(&d_in, n * sizeof(TI)));
+  cudaError_t ce = cudaMemcpyAsync(d_in, host, n * sizeof(TI), cudaMemcpyHostToDevice, s);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s);
+  if (ce != cudaSuccess) {
+    cudaFree(d_in);
+    return fail(EBIC_ERR_CUDA, "matrix upload: %s", cudaGetErrorString(ce));
+  }
+  {
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    ebic::check_values_kernel<TI><<<blocks, 256, 0, s>>>(d_in, n, ctx->d_flags);
+    ctx->launches++;
+  }
+  int flags = 0;
+  ce = cudaMemcpyAsync(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) {
+    cudaFree(d_in);
+    return fail(EBIC_ERR_CUDA, "matrix check: %s", cudaGetErrorString(ce));
+  }
+  if (flags & 1) {
+    cudaFree(d_in);
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "ExpressionMatrix: non-finite value");
+  }
+  const bool exact = !(flags & 2);
+  int chosen = store;
+  if (chosen == EBIC_STORE_AUTO) chosen = exact ? EBIC_STORE_F32 : EBIC_STORE_F64;
+  if (chosen == EBIC_STORE_F32 && !exact) {
+    cudaFree(d_in);
+    return fail(EBIC_ERR_NOT_EXACT, "matrix has values that are not float32-representable");
+  }
+  const uint64_t ld = (n_rows + ebic::kRowAlign - 1) / ebic::kRowAlign * ebic::kRowAlign;
+  const size_t esz = chosen == EBIC_STORE_F32 ? sizeof(float) : sizeof(double);
+  void* d_mat = nullptr;
+  ce = cudaMalloc(&d_mat, ld * n_cols * esz);
+  if (ce != cudaSuccess) {
+    cudaFree(d_in);
+    return fail(EBIC_ERR_CUDA, "matrix store alloc (%llu bytes): %s",
+                (unsigned long long)(ld * n_cols * esz), cudaGetErrorString(ce));
+  }
+  dim3 block(32, 8), grid((unsigned)((n_cols + 31) / 32), (unsigned)(ld / 32));
+  if (chosen == EBIC_STORE_F32)
+    ebic::transpose_kernel<TI, float><<<grid, block, 0, s>>>(d_in, n_rows, n_cols, (float*)d_mat, ld, ld);
+  else
+    ebic::transpose_kernel<TI, double><<<grid, block, 0, s>>>(d_in, n_rows, n_cols, (double*)d_mat, ld, ld);
+  ctx->launches++;
+  ce = cudaGetLastError();
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  cudaFree(d_in);
+  if (ce != cudaSuccess) {
+    cudaFree(d_mat);
+    return fail(EBIC_ERR_CUDA, "matrix transpose: %s", cudaGetErrorString(ce));
+  }
+  ctx->d_mat = d_mat;
+  ctx->store = chosen;
+  ctx->n_rows = n_rows;
+  ctx->n_cols = n_cols;
+  ctx->ld = ld;
+  ctx->row_base = row_base;
+  if (store_out) *store_out = chosen;
+  return EBIC_OK;
+}
+
+int wait_slot(ebic_ctx* ctx, Slot& sl) {
+  if (!sl.ticket) return EBIC_OK;
+  EBIC_CUDA(cudaEventSynchronize(sl.done));
+  if (sl.user_counts) std::memcpy(sl.user_counts, sl.h_counts.p, sl.n_cand * sizeof(uint32_t));
+  sl.ticket = 0;
+  sl.user_counts = nullptr;
+  (void)ctx;
+  return EBIC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ebic_abi_version(void) { return EBIC_ABI_VERSION; }
+
+const char* ebic_last_error(void) { return g_last_error.c_str(); }
+
+int ebic_device_count(int* n_out) {
+  if (!n_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null n_out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *n_out = n;
+  return EBIC_OK;
+}
+
+int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
+  if (!ctx_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null ctx_out");
+  *ctx_out = nullptr;
+  int n = 0;
+  ebic_device_count(&n);
+  if (device < 0 || device >= n)
+    return fail(EBIC_ERR_NO_DEVICE, "CUDA device %d not available (%d visible)", device, n);
+  ebic_ctx* ctx = new ebic_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 3 * sizeof(int));
+  if (e == cudaSuccess) {
+    ctx->d_flags = ctx->d_err + 1;
+    ctx->d_out1 = ctx->d_err + 2;
+    e = cudaMemset(ctx->d_err, 0, 3 * sizeof(int));
+  }
+  for (int i = 0; i < EBIC_MARSHAL_SLOTS && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&ctx->slots[i].done, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    ebic_ctx_destroy(ctx);
+    return fail(EBIC_ERR_CUDA, "context creation on device %d: %s", device, cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own_stream;
+  *ctx_out = ctx;
+  return EBIC_OK;
+}
+
+int ebic_ctx_destroy(ebic_ctx* ctx) {
+  if (!ctx) return EBIC_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& sl : ctx->slots) {
+    sl.h_cols.release();
+    sl.h_offs.release();
+    sl.h_counts.release();
+    sl.d_cols.release();
+    sl.d_offs.release();
+    sl.d_counts.release();
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
+  ebic_matrix_free(ctx);
+  ctx->d_mask.release();
+  ctx->d_rows.release();
+  ctx->d_tmp_cols.release();
+  ctx->d_tmp_offs.release();
+  ctx->d_tmp_counts.release();
+  ctx->d_row_offsets.release();
+  ctx->h_tmp_counts.release();
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return EBIC_OK;
+}
+
+int ebic_ctx_set_stream(ebic_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  return EBIC_OK;
+}
+
+int ebic_ctx_sync(ebic_ctx* ctx) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  EBIC_TRY(set_device(ctx));
+  EBIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  EBIC_CUDA(cudaDeviceSynchronize());
+  int err = 0;
+  EBIC_CUDA(cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    EBIC_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)));
+    return fail(EBIC_ERR_INVALID_ARGUMENT,
+                "device detected an empty candidate or an out-of-range column index");
+  }
+  return EBIC_OK;
+}
+
+int ebic_matrix_upload_f64(ebic_ctx* ctx, const double* row_major, uint64_t n_rows, uint64_t n_cols,
+                           uint64_t row_base, int store, int* store_out) {
+  return upload_impl<double>(ctx, row_major, n_rows, n_cols, row_base, store, store_out);
+}
+
+int ebic_matrix_upload_f32(ebic_ctx* ctx, const float* row_major, uint64_t n_rows, uint64_t n_cols,
+                           uint64_t row_base) {
+  return upload_impl<float>(ctx, row_major, n_rows, n_cols, row_base, EBIC_STORE_F32, nullptr);
+}
+
+int ebic_matrix_info(ebic_ctx* ctx, uint64_t* n_rows, uint64_t* n_cols, uint64_t* ld, int* store,
+                     uint64_t* row_base) {
+  EBIC_TRY(need_matrix(ctx));
+  if (n_rows) *n_rows = ctx->n_rows;
+  if (n_cols) *n_cols = ctx->n_cols;
+  if (ld) *ld = ctx->ld;
+  if (store) *store = ctx->store;
+  if (row_base) *row_base = ctx->row_base;
+  return EBIC_OK;
+}
+
+int ebic_matrix_free(ebic_ctx* ctx) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (ctx->d_mat) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_mat);
+  }
+  ctx->d_mat = nullptr;
+  ctx->store = 0;
+  ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
+  return EBIC_OK;
+}
+
+int ebic_eval_counts_device(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
+                            uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
+                            void* stream) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  if (n_cand && (!d_cols || !d_offsets || !d_counts))
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "null device pointer");
+  EBIC_TRY(set_device(ctx));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  if (n_cand == 0) return EBIC_OK;
+  EBIC_CUDA(cudaMemsetAsync(d_counts, 0, n_cand * sizeof(uint32_t), s));
+  return launch_count<false>(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, d_counts,
+                             nullptr, s);
+}
+
+int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
+                     double approx, int negative_trends, uint32_t* counts_out, uint64_t* ticket_out) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  if (n_cand && !counts_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null counts_out");
+  EBIC_TRY(validate_population(ctx, cols, offsets, n_cand));
+  EBIC_TRY(set_device(ctx));
+  const uint64_t ticket = ctx->next_ticket++;
+  Slot& sl = ctx->slots[ticket % EBIC_MARSHAL_SLOTS];
+  EBIC_TRY(wait_slot(ctx, sl));  // ring full: retire the oldest submission first
+  const uint64_t n_idx = n_cand ? offsets[n_cand] : 0;
+  EBIC_TRY(ensure(sl.h_cols, n_idx));
+  EBIC_TRY(ensure(sl.h_offs, n_cand + 1));
+  EBIC_TRY(ensure(sl.h_counts, n_cand));
+  EBIC_TRY(ensure(sl.d_cols, n_idx));
+  EBIC_TRY(ensure(sl.d_offs, n_cand + 1));
+  EBIC_TRY(ensure(sl.d_counts, n_cand));
+  if (n_cand) {
+    std::memcpy(sl.h_cols.p, cols, n_idx * sizeof(uint32_t));
+    std::memcpy(sl.h_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t));
+  }
+  cudaStream_t s = ctx->stream;
+  if (n_cand) {
+    EBIC_CUDA(cudaMemcpyAsync(sl.d_cols.p, sl.h_cols.p, n_idx * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, s));
+    EBIC_CUDA(cudaMemcpyAsync(sl.d_offs.p, sl.h_offs.p, (n_cand + 1) * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, s));
+    EBIC_CUDA(cudaMemsetAsync(sl.d_counts.p, 0, n_cand * sizeof(uint32_t), s));
+    EBIC_TRY(launch_count<false>(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends,
+                                 sl.d_counts.p, nullptr, s));
+    EBIC_CUDA(cudaMemcpyAsync(sl.h_counts.p, sl.d_counts.p, n_cand * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, s));
+  }
+  EBIC_CUDA(cudaEventRecord(sl.done, s));
+  sl.ticket = ticket;
+  sl.user_counts = counts_out;
+  sl.n_cand = n_cand;
+  if (ticket_out) *ticket_out = ticket;
+  return EBIC_OK;
+}
+
+int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  Slot& sl = ctx->slots[ticket % EBIC_MARSHAL_SLOTS];
+  if (sl.ticket != ticket) {
+    if (ticket == 0 || ticket >= ctx->next_ticket)
+      return fail(EBIC_ERR_INVALID_ARGUMENT, "unknown ticket %llu", (unsigned long long)ticket);
+    return EBIC_OK;  // already retired (its slot was reused)
+  }
+  EBIC_TRY(set_device(ctx));
+  return wait_slot(ctx, sl);
+}
+
+int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
+                     double approx, int negative_trends, uint32_t* counts_out) {
+  uint64_t t = 0;
+  EBIC_TRY(ebic_eval_submit(ctx, cols, offsets, n_cand, approx, negative_trends, counts_out, &t));
+  return ebic_eval_wait(ctx, t);
+}
+
+int ebic_support_rows_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
+                            uint64_t n_cand, double approx, int negative_trends, uint32_t* rows_out,
+                            uint64_t cap, uint64_t* row_offsets) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  if (!row_offsets) return fail(EBIC_ERR_INVALID_ARGUMENT, "null row_offsets");
+  EBIC_TRY(validate_population(ctx, cols, offsets, n_cand));
+  EBIC_TRY(set_device(ctx));
+  row_offsets[0] = 0;
+  if (n_cand == 0) return EBIC_OK;
+  cudaStream_t s = ctx->stream;
+  const uint64_t n_idx = offsets[n_cand];
+  const uint64_t wpc = ctx->ld / 32;  // mask words per candidate
+  EBIC_TRY(ensure(ctx->d_tmp_cols, n_idx));
+  EBIC_TRY(ensure(ctx->d_tmp_offs, n_cand + 1));
+  EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
+  EBIC_TRY(ensure(ctx->h_tmp_counts, n_cand));
+  EBIC_TRY(ensure(ctx->d_mask, n_cand * wpc));
+  EBIC_TRY(ensure(ctx->d_row_offsets, n_cand + 1));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, cols, n_idx * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s));
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_tmp_counts.p, 0, n_cand * sizeof(uint32_t), s));
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_mask.p, 0, n_cand * wpc * sizeof(uint32_t), s));
+  EBIC_TRY(launch_count<true>(ctx, ctx->d_tmp_cols.p, ctx->d_tmp_offs.p, n_cand, approx,
+                              negative_trends, ctx->d_tmp_counts.p, ctx->d_mask.p, s));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->h_tmp_counts.p, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+  EBIC_CUDA(cudaStreamSynchronize(s));
+  for (uint64_t i = 0; i < n_cand; ++i) row_offsets[i + 1] = row_offsets[i] + ctx->h_tmp_counts.p[i];
+  const uint64_t total = row_offsets[n_cand];
+  if (total > cap) return fail(EBIC_ERR_CAPACITY, "need %llu row slots, have %llu",
+                               (unsigned long long)total, (unsigned long long)cap);
+  if (total == 0) return EBIC_OK;
+  if (!rows_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null rows_out");
+  EBIC_TRY(ensure(ctx->d_rows, total));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->d_row_offsets.p, row_offsets, (n_cand + 1) * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, s));
+  const uint64_t n_words_valid = (ctx->n_rows + 31) / 32;
+  ebic::scatter_rows_kernel<<<(unsigned)n_cand, ebic::kScatterThreads, 0, s>>>(
+      ctx->d_mask.p, wpc, n_words_valid, ctx->d_row_offsets.p, ctx->row_base, ctx->d_rows.p);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  EBIC_CUDA(cudaMemcpyAsync(rows_out, ctx->d_rows.p, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  EBIC_CUDA(cudaStreamSynchronize(s));
+  return EBIC_OK;
+}
+
+int ebic_support_rows(ebic_ctx* ctx, const uint32_t* cols, uint32_t len, double approx,
+                      int negative_trends, uint32_t* rows_out, uint64_t cap, uint64_t* n_out) {
+  const uint32_t offs[2] = {0, len};
+  uint64_t ro[2] = {0, 0};
+  int st = ebic_support_rows_batch(ctx, cols, offs, 1, approx, negative_trends, rows_out, cap, ro);
+  if (n_out && (st == EBIC_OK || st == EBIC_ERR_CAPACITY)) *n_out = ro[1];
+  return st;
+}
+
+int ebic_row_supports(ebic_ctx* ctx, uint64_t row, const uint32_t* cols, uint32_t len, double approx,
+                      int negative_trends, int* supports_out) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  if (!supports_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null supports_out");
+  if (row < ctx->row_base || row >= ctx->row_base + ctx->n_rows)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "row %llu outside the resident shard",
+                (unsigned long long)row);
+  const uint32_t offs[2] = {0, len};
+  EBIC_TRY(validate_population(ctx, cols, offs, 1));
+  EBIC_TRY(set_device(ctx));
+  cudaStream_t s = ctx->stream;
+  EBIC_TRY(ensure(ctx->d_tmp_cols, len));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, cols, len * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  const uint64_t lr = row - ctx->row_base;
+  if (ctx->store == EBIC_STORE_F32)
+    ebic::row_supports_kernel<float><<<1, 32, 0, s>>>((const float*)ctx->d_mat, ctx->ld, lr,
+                                                       ctx->d_tmp_cols.p, len, approx,
+                                                       negative_trends, ctx->d_out1);
+  else
+    ebic::row_supports_kernel<double><<<1, 32, 0, s>>>((const double*)ctx->d_mat, ctx->ld, lr,
+                                                        ctx->d_tmp_cols.p, len, approx,
+                                                        negative_trends, ctx->d_out1);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  int out = 0;
+  EBIC_CUDA(cudaMemcpyAsync(&out, ctx->d_out1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EBIC_CUDA(cudaStreamSynchronize(s));
+  *supports_out = out;
+  return EBIC_OK;
+}
+
+double ebic_fitness(uint64_t support_count, uint64_t num_cols, uint64_t min_rows, uint64_t col_cap) {
+  if (support_count < min_rows) return 0.0;
+  const int bonus = (int)std::min(num_cols, col_cap);
+  return std::ldexp((double)support_count, bonus);
+}
+
+int ebic_ctx_launch_count(ebic_ctx* ctx, uint64_t* n_out) {
+  if (!ctx || !n_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+  *n_out = ctx->launches;
+  return EBIC_OK;
+}
+
+int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (slab_rows % ebic::kRowAlign)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "slab_rows must be a multiple of %u", ebic::kRowAlign);
+  ctx->slab_rows = slab_rows;
+  return EBIC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,297 @@
+"""Python mirror of the reference trend/fitness API (proj/include/bicseek/trend.hpp)
+over the B200 evaluator.
+
+Reference interface -> this module
+  TrendParams            trend.hpp:13-25 (validate trend.cpp:8-13)  -> TrendParams
+  row_supports           trend.hpp:30-31 / trend.cpp:41-46           -> row_supports / Evaluator.row_supports
+  supporting_rows        trend.hpp:33-35 / trend.cpp:48-54           -> supporting_rows / Evaluator.supporting_rows
+  evaluate_population    trend.hpp:37-45 / trend.cpp:56-72           -> evaluate_population / Evaluator.evaluate_population
+  fitness                trend.hpp:47-50 / trend.cpp:74-79           -> fitness
+  ExpressionMatrix       matrix.hpp:13-43 (row-major double)         -> numpy (R, C) array, uploaded once per Evaluator
+  Chromosome             bicluster.hpp:13-24                         -> sequence of ints / Population (CSR)
+
+Same names, argument meaning and error behaviour (ValueError for what the
+reference raises std::invalid_argument for).  Every evaluating call runs on the
+GPU through libebic.so; there is no CPU path in this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import EBIC_STORE_AUTO, EBIC_STORE_F32, EBIC_STORE_F64, EbicError, check
+
+
+@dataclass
+class TrendParams:
+    """trend.hpp:13-25."""
+
+    approx: float = 0.03
+    negative_trends: bool = False
+    min_rows: int = 10
+    col_cap: int = 8
+
+    def validate(self) -> None:  # trend.cpp:8-13
+        if not (self.approx >= 0.0 and self.approx < 1.0):
+            raise ValueError("TrendParams: approx must be in [0, 1)")
+        if self.min_rows < 2:
+            raise ValueError("TrendParams: min_rows must be >= 2")
+        if self.col_cap < 2:
+            raise ValueError("TrendParams: col_cap must be >= 2")
+
+
+class Population:
+    """A batch of candidate column sequences in CSR form (uint32 cols, uint32 offsets)."""
+
+    __slots__ = ("cols", "offsets")
+
+    def __init__(self, cols: np.ndarray, offsets: np.ndarray):
+        self.cols = np.ascontiguousarray(cols, dtype=np.uint32)
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.uint32)
+        if self.offsets.ndim != 1 or self.offsets.size < 1 or self.offsets[0] != 0:
+            raise ValueError("Population: offsets must start at 0")
+        if int(self.offsets[-1]) != self.cols.size:
+            raise ValueError("Population: offsets[-1] must equal len(cols)")
+
+    @classmethod
+    def from_sequences(cls, seqs: Iterable[Sequence[int]]) -> "Population":
+        seqs = [list(s) for s in seqs]
+        offs = np.zeros(len(seqs) + 1, dtype=np.uint32)
+        if seqs:
+            offs[1:] = np.cumsum([len(s) for s in seqs])
+        cols = np.fromiter((c for s in seqs for c in s), dtype=np.int64, count=int(offs[-1]))
+        if cols.size and (cols.min() < 0 or cols.max() >= 2**32):
+            raise ValueError("Population: column index out of range")
+        return cls(cols.astype(np.uint32), offs)
+
+    def __len__(self) -> int:
+        return self.offsets.size - 1
+
+    def sequence(self, i: int) -> np.ndarray:
+        return self.cols[self.offsets[i]:self.offsets[i + 1]]
+
+    def lengths(self) -> np.ndarray:
+        return np.diff(self.offsets)
+
+
+def _as_population(pop) -> Population:
+    if isinstance(pop, Population):
+        return pop
+    return Population.from_sequences(pop)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(_lib.lib().ebic_device_count(C.byref(n)))
+    return n.value
+
+
+class Evaluator:
+    """One device context + one resident matrix (or row shard).
+
+    The matrix is stored column-major in HBM: float32 when every value is
+    float32-representable (always for float32 input), otherwise float64, so
+    results are bit-exact with the reference for any finite input.
+    """
+
+    def __init__(self, device: int = 0):
+        self._L = _lib.lib()
+        h = C.c_void_p()
+        check(self._L.ebic_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+        self.n_rows = 0
+        self.n_cols = 0
+        self.row_base = 0
+        self.store = 0
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.ebic_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def set_stream(self, cuda_stream: int | None) -> None:
+        check(self._L.ebic_ctx_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
+
+    def sync(self) -> None:
+        check(self._L.ebic_ctx_sync(self._h))
+
+    def launch_count(self) -> int:
+        n = C.c_uint64(0)
+        check(self._L.ebic_ctx_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def set_slab_rows(self, slab_rows: int) -> None:
+        check(self._L.ebic_ctx_set_slab_rows(self._h, int(slab_rows)))
+
+    # -- matrix store ------------------------------------------------------
+    def upload(self, matrix: np.ndarray, row_base: int = 0, store: int = EBIC_STORE_AUTO) -> int:
+        """Upload a row-major (R, C) matrix (float64 or float32).  Returns the store mode."""
+        m = np.asarray(matrix)
+        if m.ndim != 2:
+            raise ValueError("matrix must be 2-D (rows, cols)")
+        if m.dtype == np.float32:
+            m = np.ascontiguousarray(m)
+            if store == EBIC_STORE_F64:
+                m = m.astype(np.float64)
+            else:
+                check(self._L.ebic_matrix_upload_f32(self._h, _ptr(m), m.shape[0], m.shape[1], row_base))
+                self._set_shape(m.shape, row_base, EBIC_STORE_F32)
+                return EBIC_STORE_F32
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        out = C.c_int(0)
+        check(self._L.ebic_matrix_upload_f64(self._h, _ptr(m), m.shape[0], m.shape[1], row_base,
+                                             int(store), C.byref(out)))
+        self._set_shape(m.shape, row_base, out.value)
+        return out.value
+
+    def _set_shape(self, shape, row_base, store):
+        self.n_rows, self.n_cols = int(shape[0]), int(shape[1])
+        self.row_base = int(row_base)
+        self.store = int(store)
+
+    def matrix_info(self) -> dict:
+        r, c, ld, rb = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        st = C.c_int()
+        check(self._L.ebic_matrix_info(self._h, C.byref(r), C.byref(c), C.byref(ld), C.byref(st), C.byref(rb)))
+        return {"rows": r.value, "cols": c.value, "ld": ld.value, "store": st.value, "row_base": rb.value}
+
+    # -- evaluation --------------------------------------------------------
+    def evaluate_population(self, pop, params: TrendParams | None = None) -> np.ndarray:
+        """trend.cpp:56-72: uint32 support count per candidate (host arrays, synchronous)."""
+        p = params or TrendParams()
+        pop = _as_population(pop)
+        out = np.zeros(len(pop), dtype=np.uint32)
+        if len(pop) == 0:
+            return out
+        check(self._L.ebic_eval_counts(self._h, _ptr(pop.cols), _ptr(pop.offsets), len(pop),
+                                       float(p.approx), int(bool(p.negative_trends)), _ptr(out)))
+        return out
+
+    def evaluate_population_device(self, d_cols: int, d_offsets: int, n_cand: int, d_counts: int,
+                                   params: TrendParams | None = None, stream: int | None = None) -> None:
+        """Device pointers (e.g. torch tensors' data_ptr()), asynchronous on `stream`."""
+        p = params or TrendParams()
+        check(self._L.ebic_eval_counts_device(self._h, C.c_void_p(d_cols), C.c_void_p(d_offsets), int(n_cand),
+                                              float(p.approx), int(bool(p.negative_trends)),
+                                              C.c_void_p(d_counts), C.c_void_p(stream or 0)))
+
+    def submit(self, pop: Population, out: np.ndarray, params: TrendParams | None = None) -> int:
+        """Batch marshaller: async evaluation; `out` (uint32, len(pop)) is filled by wait()."""
+        p = params or TrendParams()
+        if out.dtype != np.uint32 or out.size < len(pop) or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous uint32 array of len(pop)")
+        t = C.c_uint64(0)
+        check(self._L.ebic_eval_submit(self._h, _ptr(pop.cols), _ptr(pop.offsets), len(pop), float(p.approx),
+                                       int(bool(p.negative_trends)), _ptr(out), C.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        check(self._L.ebic_eval_wait(self._h, int(ticket)))
+
+    def supporting_rows(self, chromosome: Sequence[int], params: TrendParams | None = None) -> np.ndarray:
+        """trend.cpp:48-54: ascending (global) rows supporting one candidate."""
+        p = params or TrendParams()
+        cols = np.ascontiguousarray(chromosome, dtype=np.uint32)
+        rows = np.empty(max(self.n_rows, 1), dtype=np.uint32)
+        n = C.c_uint64(0)
+        check(self._L.ebic_support_rows(self._h, _ptr(cols), cols.size, float(p.approx),
+                                        int(bool(p.negative_trends)), _ptr(rows), rows.size, C.byref(n)))
+        return rows[:n.value].copy()
+
+    def supporting_rows_batch(self, pop, params: TrendParams | None = None) -> list[np.ndarray]:
+        p = params or TrendParams()
+        pop = _as_population(pop)
+        n = len(pop)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        cap = 0
+        rows = np.empty(1, dtype=np.uint32)
+        while True:
+            st = self._L.ebic_support_rows_batch(self._h, _ptr(pop.cols), _ptr(pop.offsets), n, float(p.approx),
+                                                 int(bool(p.negative_trends)), _ptr(rows), cap, _ptr(offs))
+            if st == _lib.EBIC_ERR_CAPACITY:
+                cap = int(offs[-1])
+                rows = np.empty(max(cap, 1), dtype=np.uint32)
+                continue
+            check(st)
+            break
+        return [rows[offs[i]:offs[i + 1]].copy() for i in range(n)]
+
+    def row_supports(self, row: int, chromosome: Sequence[int], params: TrendParams | None = None) -> bool:
+        p = params or TrendParams()
+        cols = np.ascontiguousarray(chromosome, dtype=np.uint32)
+        out = C.c_int(0)
+        check(self._L.ebic_row_supports(self._h, int(row), _ptr(cols), cols.size, float(p.approx),
+                                        int(bool(p.negative_trends)), C.byref(out)))
+        return bool(out.value)
+
+
+# ---------------------------------------------------------------------------
+# free functions with the reference signatures (matrix passed on every call;
+# a module-level Evaluator caches the device copy, keyed by identity AND
+# content, exactly like the C++ drop-in TU)
+# ---------------------------------------------------------------------------
+_default: Evaluator | None = None
+_default_key = None
+
+
+def _bind(m: np.ndarray) -> Evaluator:
+    global _default, _default_key
+    m = np.asarray(m)
+    if _default is None:
+        _default = Evaluator(0)
+    key = (m.dtype.str, m.shape)
+    if _default_key is None or _default_key[0] != key or not np.array_equal(_default_key[1], m):
+        _default.upload(m)
+        _default_key = (key, m.copy())
+    return _default
+
+
+def row_supports(m: np.ndarray, row: int, c: Sequence[int], p: TrendParams) -> bool:
+    return _bind(m).row_supports(row, c, p)
+
+
+def supporting_rows(m: np.ndarray, c: Sequence[int], p: TrendParams) -> np.ndarray:
+    return _bind(m).supporting_rows(c, p)
+
+
+def evaluate_population(m: np.ndarray, pop, p: TrendParams, pool=None) -> np.ndarray:
+    """`pool` (the reference WorkerPool) is accepted and ignored: the GPU grid replaces it."""
+    return _bind(m).evaluate_population(pop, p)
+
+
+def fitness(support_count: int, num_cols: int, p: TrendParams) -> float:
+    """trend.cpp:74-79 (exact: count * 2^min(num_cols, col_cap), 0 below min_rows)."""
+    return float(_lib.lib().ebic_fitness(int(support_count), int(num_cols), int(p.min_rows), int(p.col_cap)))
+
+
+__all__ = [
+    "TrendParams", "Population", "Evaluator", "EbicError", "device_count",
+    "row_supports", "supporting_rows", "evaluate_population", "fitness",
+    "EBIC_STORE_AUTO", "EBIC_STORE_F32", "EBIC_STORE_F64",
+]

@@ -1,0 +1,301 @@
+"""Parity of the CUDA path (through the C ABI) with the reference / the pinned oracle.
+
+Bar: bit-exact integer counts and identical ascending row lists.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_cases, load_golden
+from paper_2105_01196_b200 import (EBIC_STORE_AUTO, EBIC_STORE_F32, EBIC_STORE_F64, EbicError, Population,
+                                   TrendParams)
+from paper_2105_01196_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _tp(s):
+    return TrendParams(approx=s["approx"], negative_trends=s["negative"])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+@pytest.mark.parametrize("store", [EBIC_STORE_AUTO, EBIC_STORE_F64])
+def test_counts_and_rows_match_reference_golden(evaluator, name, store):
+    z, settings = load_golden(name)
+    m = z["matrix"]
+    chosen = evaluator.upload(m, store=store)
+    exact = np.array_equal(m.astype(np.float32).astype(np.float64), m)
+    assert chosen == (EBIC_STORE_F32 if (exact and store == EBIC_STORE_AUTO) else EBIC_STORE_F64)
+    pop = Population(z["cols"], z["offsets"])
+    for k, s in enumerate(settings):
+        counts = evaluator.evaluate_population(pop, _tp(s))
+        np.testing.assert_array_equal(counts, z[f"counts_{k}"], err_msg=f"{name} {s}")
+        idx = z[f"rows_idx_{k}"]
+        ro = z[f"rows_offsets_{k}"]
+        batch = evaluator.supporting_rows_batch(Population.from_sequences([pop.sequence(i) for i in idx]), _tp(s))
+        for j, i in enumerate(idx):
+            want = z[f"rows_{k}"][ro[j]:ro[j + 1]]
+            np.testing.assert_array_equal(batch[j], want)
+            np.testing.assert_array_equal(evaluator.supporting_rows(pop.sequence(i), _tp(s)), want)
+
+
+def test_row_supports_hand_vectors(evaluator):
+    # test_trend.cpp:60-81
+    def rs(rows, seq, approx, neg=False):
+        evaluator.upload(np.array(rows, dtype=np.float64))
+        return evaluator.row_supports(0, seq, TrendParams(approx=approx, negative_trends=neg))
+
+    assert rs([[1.0, 2.0, 3.0]], [0, 1, 2], 0.0)
+    assert not rs([[1.0, 2.0, 3.0]], [2, 1, 0], 0.0)
+    assert rs([[3.0, 1.0, 2.0]], [1, 2, 0], 0.0)
+    assert not rs([[1.0, 1.0]], [0, 1], 0.0)
+    assert rs([[1.0, 1.0]], [0, 1], 0.05)
+    assert not rs([[2.0, 2.0, 2.0]], [0, 1, 2], 0.0, True)
+
+
+def _random_case(rng, R, Cn, f32=True, max_len=12):
+    m = rng.standard_normal((R, Cn))
+    if f32:
+        m = m.astype(np.float32).astype(np.float64)
+    m[rng.random(m.shape) < 0.03] = 0.0
+    seqs = [rng.choice(Cn, size=int(rng.integers(1, min(Cn, max_len) + 1)), replace=False) for _ in range(300)]
+    return m, Population.from_sequences(seqs)
+
+
+@pytest.mark.parametrize("R", [1, 31, 256, 257, 1000, 4097])
+@pytest.mark.parametrize("f32", [True, False])
+def test_random_shapes_vs_oracle(evaluator, R, f32):
+    rng = np.random.default_rng(R * 7 + f32)
+    m, pop = _random_case(rng, R, 40, f32)
+    evaluator.upload(m)
+    for approx in (0.0, 0.03, float(rng.uniform(0, 0.5)), 0.999):
+        for neg in (False, True):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+            np.testing.assert_array_equal(got, want, err_msg=f"R={R} approx={approx} neg={neg}")
+
+
+def _near_threshold_matrix(rng, R, Cn, approx):
+    """Rows where each next value sits within a few float32 ulps of the reference
+    threshold RN64(prev - RN64(approx*|prev|)) -- every pair lands in the float32
+    filter's uncertain band and must be resolved by the exact double path."""
+    m = np.empty((R, Cn), dtype=np.float64)
+    x = rng.standard_normal(R).astype(np.float32)
+    m[:, 0] = x
+    for c in range(1, Cn):
+        prev = m[:, c - 1]
+        thr = prev - approx * np.abs(prev)
+        t32 = thr.astype(np.float32)
+        jitter = rng.integers(-2, 3, size=R)
+        cur = t32.copy()
+        for _ in range(2):
+            cur = np.where(jitter > 0, np.nextafter(cur, np.float32(np.inf)), cur)
+            cur = np.where(jitter < 0, np.nextafter(cur, np.float32(-np.inf)), cur)
+            jitter = jitter - np.sign(jitter)
+        m[:, c] = cur.astype(np.float64)
+    return m
+
+
+@pytest.mark.parametrize("approx", [0.03, 0.1, 0.5, 2**-20])
+def test_filter_uncertain_band_is_exact(evaluator, approx):
+    rng = np.random.default_rng(11)
+    m = _near_threshold_matrix(rng, 3000, 12, approx)
+    assert np.array_equal(m.astype(np.float32).astype(np.float64), m)
+    assert evaluator.upload(m) == EBIC_STORE_F32
+    seqs = [list(range(a, b)) for a in range(0, 6) for b in range(a + 2, 13)]
+    seqs += [list(range(b - 1, a - 1, -1)) for a in range(0, 6) for b in range(a + 2, 13)]
+    pop = Population.from_sequences(seqs)
+    for neg in (False, True):
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+        got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+        np.testing.assert_array_equal(got, want)
+        assert want.sum() > 0
+
+
+def test_subnormal_and_huge_values(evaluator):
+    rng = np.random.default_rng(5)
+    vals = np.array([0.0, -0.0, 1e-45, -1e-45, 1.2e-38, -1.2e-38, 3.4e38, -3.4e38, 1.0, -1.0, 5e-40, -5e-40],
+                    dtype=np.float32).astype(np.float64)
+    m = rng.choice(vals, size=(2000, 12))
+    assert evaluator.upload(m) == EBIC_STORE_F32
+    seqs = [rng.choice(12, size=int(rng.integers(2, 7)), replace=False) for _ in range(500)]
+    pop = Population.from_sequences(seqs)
+    for approx in (0.0, 0.03, 0.999, 1e-8):
+        for neg in (False, True):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+            np.testing.assert_array_equal(got, want)
+
+
+def test_long_sequences_cross_smem_chunks(evaluator):
+    rng = np.random.default_rng(9)
+    m = rng.standard_normal((5000, 300)).astype(np.float32)
+    # sorted rows make long trends survive, so the column loop runs past the 64-index SMEM chunk
+    m[:2500] = np.sort(m[:2500], axis=1)
+    evaluator.upload(m)
+    seqs = [np.sort(rng.choice(300, size=L, replace=False)) for L in (63, 64, 65, 128, 129, 200, 300)]
+    seqs += [s[::-1] for s in seqs]
+    pop = Population.from_sequences(seqs)
+    for approx, neg in ((0.0, False), (0.03, True), (0.0, True)):
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+        got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+        np.testing.assert_array_equal(got, want)
+        assert want.max() >= 2500
+
+
+def _config_matrix(rows, cols, bic_rows, bic_cols, seed=1):
+    if oracle.reference_available():
+        # the reference generator (datagen.cpp:208-264), float32-quantised
+        return oracle.ref_gen_scenario(rows, cols, bic_rows, bic_cols, 3, seed=seed, quantize=True)
+    m, _ = synth.planted_trend_matrix(rows, cols, 3, bic_rows, bic_cols, seed=seed)
+    return m
+
+
+def test_config2_bit_exact(evaluator):
+    """BASELINE config 2: 10k x 500, P=4096, bit-exact counts vs the CPU oracle."""
+    m = _config_matrix(10_000, 500, 500, 20)
+    if oracle.reference_available():
+        cols, offs = oracle.ref_init_population(4096, 500, seed=42)
+        pop = Population(cols, offs)
+    else:
+        pop = synth.random_population(4096, 500, seed=42)
+    assert evaluator.upload(m) == EBIC_STORE_F32
+    for approx in (0.0, 0.03):
+        for neg in (False, True):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+            np.testing.assert_array_equal(got, want)
+
+
+def test_config3_full_size_bit_exact(evaluator):
+    """BASELINE config 3 at full size on one GPU: 20k x 1000, P=16384."""
+    m, _ = synth.planted_trend_matrix(20_000, 1000, 3, 500, 20, seed=3)
+    pop = synth.random_population(16384, 1000, seed=42)
+    evaluator.upload(m)
+    tp = TrendParams(approx=0.03)
+    want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
+    np.testing.assert_array_equal(evaluator.evaluate_population(pop, tp), want)
+
+
+def test_config4_full_size_properties(evaluator):
+    """BASELINE config 4 (200k x 2000, 1.6 GB f32, P=32768): bit-exact on a candidate
+    sample, plus size-independent properties over the whole population."""
+    rng = np.random.default_rng(4)
+    m = rng.standard_normal((200_000, 2000), dtype=np.float32)
+    evaluator.upload(m)
+    pop = synth.random_population(32768, 2000, seed=42)
+    tp = TrendParams(approx=0.03)
+    base = evaluator.evaluate_population(pop, tp)
+    neg = evaluator.evaluate_population(pop, TrendParams(approx=0.03, negative_trends=True))
+    loose = evaluator.evaluate_population(pop, TrendParams(approx=0.2))
+    strict = evaluator.evaluate_population(pop, TrendParams(approx=0.0))
+    assert (neg >= base).all() and (loose >= base).all() and (base >= strict).all()
+    sample = rng.choice(32768, size=96, replace=False)
+    sub = Population.from_sequences([pop.sequence(i) for i in sample])
+    want = oracle.evaluate_population(m, sub.cols, sub.offsets, 0.03, False)
+    np.testing.assert_array_equal(base[sample], want)
+    # row-shard additivity: two shards summed == whole (the row-sharded exchange)
+    half = 100_000
+    evaluator.upload(m[:half], row_base=0)
+    a = evaluator.evaluate_population(pop, tp)
+    evaluator.upload(m[half:], row_base=half)
+    b = evaluator.evaluate_population(pop, tp)
+    np.testing.assert_array_equal(a + b, base)
+
+
+@pytest.mark.parametrize("R", [1024, 65536, 1_000_000])
+def test_microbench_shapes(evaluator, R):
+    rng = np.random.default_rng(R)
+    m = rng.standard_normal((R, 64), dtype=np.float32)
+    evaluator.upload(m)
+    for L in (2, 16, 50):
+        pop = synth.exact_len_population(64 if R > 100_000 else 256, 64, L, seed=L)
+        for approx in (0.0, 0.03):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, False)
+            got = evaluator.evaluate_population(pop, TrendParams(approx=approx))
+            np.testing.assert_array_equal(got, want)
+
+
+def test_support_rows_are_global_and_ascending(evaluator):
+    rng = np.random.default_rng(2)
+    m = rng.standard_normal((6000, 20)).astype(np.float32)
+    seqs = [rng.choice(20, size=3, replace=False) for _ in range(20)]
+    tp = TrendParams(approx=0.03, negative_trends=True)
+    full = [oracle.supporting_rows(m, s, 0.03, True) for s in seqs]
+    evaluator.upload(m[2000:], row_base=2000)
+    got = evaluator.supporting_rows_batch(seqs, tp)
+    for s, g, f in zip(seqs, got, full):
+        np.testing.assert_array_equal(g, f[f >= 2000])
+        assert (np.diff(g.astype(np.int64)) > 0).all()
+    assert evaluator.row_supports(2000 + 5, seqs[0], tp) == oracle.row_supports(m, 2005, seqs[0], 0.03, True)
+
+
+def test_device_pointer_path_and_external_stream(evaluator):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal((10_000, 100)).astype(np.float32)
+    evaluator.upload(m)
+    pop = synth.random_population(2000, 100, seed=1)
+    want = evaluator.evaluate_population(pop)
+    d_cols = torch.from_numpy(pop.cols.view(np.int32)).cuda()
+    d_offs = torch.from_numpy(pop.offsets.view(np.int32)).cuda()
+    d_counts = torch.full((len(pop),), -1, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        evaluator.evaluate_population_device(d_cols.data_ptr(), d_offs.data_ptr(), len(pop), d_counts.data_ptr(),
+                                             TrendParams(), stream=s.cuda_stream)
+    s.synchronize()
+    np.testing.assert_array_equal(d_counts.cpu().numpy().view(np.uint32), want)
+    evaluator.set_stream(s.cuda_stream)
+    np.testing.assert_array_equal(evaluator.evaluate_population(pop), want)
+    evaluator.set_stream(None)
+    # a bad column on the device path is detected on device and reported by sync()
+    bad = d_cols.clone()
+    bad[0] = 100
+    evaluator.evaluate_population_device(bad.data_ptr(), d_offs.data_ptr(), len(pop), d_counts.data_ptr())
+    with pytest.raises(EbicError):
+        evaluator.sync()
+    evaluator.sync()  # flag cleared
+
+
+def test_marshaller_ring(evaluator):
+    rng = np.random.default_rng(4)
+    m = rng.standard_normal((4000, 50)).astype(np.float32)
+    evaluator.upload(m)
+    pops = [synth.random_population(int(rng.integers(1, 900)), 50, seed=i) for i in range(7)]
+    outs = [np.zeros(len(p), dtype=np.uint32) for p in pops]
+    tickets = [evaluator.submit(p, o) for p, o in zip(pops, outs)]  # more than EBIC_MARSHAL_SLOTS in flight
+    for t in tickets:
+        evaluator.wait(t)
+    for p, o in zip(pops, outs):
+        np.testing.assert_array_equal(o, oracle.evaluate_population(m, p.cols, p.offsets, 0.03, False))
+
+
+def test_errors_are_reported_not_undefined(evaluator):
+    m = np.random.default_rng(0).standard_normal((100, 10))
+    evaluator.upload(m)
+    with pytest.raises(EbicError, match="out of range"):
+        evaluator.evaluate_population([[0, 10]])
+    with pytest.raises(EbicError, match="empty"):
+        evaluator.evaluate_population(Population(np.array([1], np.uint32), np.array([0, 0, 1], np.uint32)))
+    with pytest.raises(EbicError, match="finite"):
+        evaluator.evaluate_population([[0, 1]], TrendParams(approx=float("nan")))
+    bad = m.copy()
+    bad[3, 3] = np.inf
+    with pytest.raises(EbicError, match="non-finite"):
+        evaluator.upload(bad)
+    with pytest.raises(EbicError) as ei:
+        evaluator.upload(m, store=EBIC_STORE_F32)
+    assert ei.value.status == 5
+    # the failed uploads left no matrix behind
+    with pytest.raises(EbicError) as ei:
+        evaluator.evaluate_population([[0, 1]])
+    assert ei.value.status == 3
+
+
+def test_launches_are_counted(evaluator):
+    m = np.random.default_rng(0).standard_normal((1000, 10)).astype(np.float32)
+    evaluator.upload(m)
+    n0 = evaluator.launch_count()
+    evaluator.evaluate_population([[0, 1, 2]] * 10)
+    assert evaluator.launch_count() == n0 + 1

@@ -1,0 +1,46 @@
+"""The reference's own hot-path test suite and its end-to-end run(), relinked
+against the device drop-in TU (csrc/bicseek_trend_device.cpp in place of
+proj/src/trend.cpp) -- the strongest drop-in evidence: UNCHANGED reference
+tests and UNCHANGED evolution.cpp, running on the B200 evaluator.
+
+The binaries are built in the build container by oracle/Makefile (`device`)
+from the reference sources and travel to the GPU box prebuilt.
+"""
+import json
+import subprocess
+
+import pytest
+
+from conftest import GOLDEN, REPO
+
+pytestmark = pytest.mark.gpu
+
+REF = REPO / "oracle" / "_ref"
+
+
+def _need(name):
+    exe = REF / name
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (reference tree absent at build time)")
+    return exe
+
+
+def test_reference_test_trend_passes_on_device():
+    exe = _need("test_trend_device")
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "| 0 failed" in res.stdout, res.stdout
+
+
+@pytest.mark.parametrize("label", ["default", "forced200", "neg_forced60"])
+def test_run_config1_byte_identical_to_reference(label):
+    """BASELINE config 1: full run() (tournament, mutation/crossover, tabu list,
+    top-rank archive) with device evaluation == the reference CPU run."""
+    exe = _need("run_device")
+    golden = json.loads((GOLDEN / "run_cfg1.json").read_text())[label]
+    out = subprocess.run([str(exe), *golden["args"]], check=True, capture_output=True, text=True,
+                         timeout=600).stdout
+    got = json.loads(out)
+    assert json.dumps(got["result"], sort_keys=True) == json.dumps(golden["result"], sort_keys=True)
+    assert got["generations"] == golden["generations"]
+    assert got["termination"] == golden["termination"]
