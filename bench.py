@@ -262,8 +262,17 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     b, e = row_range(R, rank, world) if args.shard == "rows" else (0, R)
 
     ev = Evaluator(local_rank)
+    ev.set_path({"auto": 0, "value": 1, "plane": 2}[args.path])
+    t0 = time.perf_counter()
     ev.upload(np.ascontiguousarray(m[b:e]), row_base=b)
-    stream = torch.cuda.current_stream(dev)
+    upload_ms = (time.perf_counter() - t0) * 1e3
+    # per-(matrix, approx) index: the exact rank plane (built once per GA run; outside the steps)
+    t0 = time.perf_counter()
+    ev.prepare(cfg["approx"])
+    prepare_ms = (time.perf_counter() - t0) * 1e3
+    # a dedicated (non-default) stream: kernels, NCCL and the timing events all run on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ev.set_stream(stream.cuda_stream)
 
     # device-resident populations
@@ -387,10 +396,11 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         "config": {"workload": cfg["label"], "rows": R, "cols": Ccols, "population": P,
                    "parallelism": f"{args.shard}-sharded x{world}" if world > 1 else "1 GPU",
                    "l2": "flushed before every timed step (512 MiB device write, outside the step events)",
-                   "shard": args.shard},
+                   "shard": args.shard, "path": args.path},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, world),
-                     "kernel": "fitness_count_kernel", "kernel_avg_ms": kern_avg_s * 1e3,
+                     "kernel": "slab_count_kernel (rank plane)" if (args.path != "value" and Ccols <= 8192)
+                     else "fitness_count_kernel (value)", "kernel_avg_ms": kern_avg_s * 1e3,
                      "algorithmic_bytes_per_launch": statistics.mean(alg_bytes),
                      "peak_source": peak_src,
                      "note": "algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "
@@ -400,6 +410,9 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                 "api": "ebic_eval_counts (Evaluator.evaluate_population)" if world == 1
                        else f"ShardedEvaluator({args.shard}) over ebic_eval_counts + NCCL"},
         "gpu_launches": int(launches),
+        "store": {"upload_ms": upload_ms, "rank_plane_build_ms": prepare_ms,
+                  "note": "one-time per matrix (upload+transpose) and per (matrix, approx) (rank plane); "
+                          "not part of a step, like the reference's matrix construction"},
         "wall_ms_timed_region": wall * 1e3,
         "parity_device_vs_host_api": parity_dev_vs_host,
     }
@@ -432,6 +445,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--shard", choices=["rows", "pop"], default="rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", choices=["auto", "value", "plane"], default="auto",
+                    help="evaluation kernel: rank-plane slab kernel (auto for <= 8192 cols) or float value kernel")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 

@@ -150,8 +150,22 @@ double ebic_fitness(uint64_t support_count, uint64_t num_cols, uint64_t min_rows
 
 /* Number of kernels this context has launched since creation. */
 int ebic_ctx_launch_count(ebic_ctx* ctx, uint64_t* n_out);
-/* Tuning knob for the fitness kernel: rows per CTA slab (0 = auto). */
+/* Tuning knob for the value-path kernel: rows per CTA slab (0 = auto). */
 int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
+
+/* Evaluation path.  AUTO: the rank-plane slab kernel whenever the matrix has
+ * <= 8192 columns, else the value kernel.  VALUE / PLANE force one (PLANE
+ * fails with EBIC_ERR_INVALID_ARGUMENT if the matrix is too wide).  Both are
+ * bit-exact; the knob exists for cross-checking and benchmarking. */
+#define EBIC_PATH_AUTO 0
+#define EBIC_PATH_VALUE 1
+#define EBIC_PATH_PLANE 2
+int ebic_ctx_set_path(ebic_ctx* ctx, int path);
+
+/* Build (or reuse) the rank plane of the resident matrix for `approx` now,
+ * instead of lazily on the first evaluation with that approx.  The plane is a
+ * per-(matrix, approx) index: a GA run uses one approx for all generations. */
+int ebic_matrix_prepare(ebic_ctx* ctx, double approx);
 
 #ifdef __cplusplus
 }

@@ -49,7 +49,13 @@ SIGNATURES = {
     "ebic_fitness": (C.c_double, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ebic_ctx_launch_count": (C.c_int, [_vp, _u64p]),
     "ebic_ctx_set_slab_rows": (C.c_int, [_vp, C.c_uint32]),
+    "ebic_ctx_set_path": (C.c_int, [_vp, C.c_int]),
+    "ebic_matrix_prepare": (C.c_int, [_vp, C.c_double]),
 }
+
+EBIC_PATH_AUTO = 0
+EBIC_PATH_VALUE = 1
+EBIC_PATH_PLANE = 2
 
 
 class EbicError(RuntimeError):

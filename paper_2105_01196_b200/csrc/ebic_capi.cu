@@ -10,12 +10,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "ebic.h"
 #include "ebic_kernels.cuh"
+#include "ebic_plane.cuh"
 
 namespace {
 
@@ -116,7 +118,14 @@ struct ebic_ctx {
   Slot slots[EBIC_MARSHAL_SLOTS];
   uint64_t next_ticket = 1;
   uint64_t launches = 0;
-  uint32_t slab_rows = 0;  // 0 = auto
+  uint32_t slab_rows = 0;  // 0 = auto (value path)
+  // rank plane (per matrix x approx)
+  uint32_t* d_plane = nullptr;
+  bool plane_valid = false;
+  double plane_approx = 0.0;
+  int path = EBIC_PATH_AUTO;
+  int n_sms = 148;
+  size_t smem_optin = 227 * 1024;
 };
 
 namespace {
@@ -164,11 +173,142 @@ void launch_count_t(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_off
   ctx->launches++;
 }
 
+// ---- rank plane ------------------------------------------------------------
+bool plane_fits(const ebic_ctx* ctx) { return ctx->n_cols >= 1 && ctx->n_cols <= ebic::kPlaneMaxCols; }
+
+int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
+  // bitwise comparison: -0.0 and 0.0 give identical thresholds, but keep it simple and exact
+  if (ctx->plane_valid && std::memcmp(&ctx->plane_approx, &approx, sizeof(double)) == 0) return EBIC_OK;
+  ctx->plane_valid = false;
+  if (!ctx->d_plane) {
+    EBIC_CUDA(cudaMalloc(&ctx->d_plane, ctx->ld * ctx->n_cols * sizeof(uint32_t)));
+  }
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_plane, 0, ctx->ld * ctx->n_cols * sizeof(uint32_t), s));
+  uint32_t pow2 = 1;
+  while (pow2 < ctx->n_cols) pow2 <<= 1;
+  const size_t esz = ctx->store == EBIC_STORE_F32 ? sizeof(float) : sizeof(double);
+  const size_t smem = pow2 * esz;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ctx->n_rows, (uint64_t)ctx->n_sms * 8);
+  if (ctx->store == EBIC_STORE_F32) {
+    EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ebic::build_plane_kernel<float><<<grid, 256, smem, s>>>((const float*)ctx->d_mat, ctx->ld, (uint32_t)ctx->n_rows,
+                                                           (uint32_t)ctx->n_cols, pow2, approx, ctx->d_plane);
+  } else {
+    EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ebic::build_plane_kernel<double><<<grid, 256, smem, s>>>((const double*)ctx->d_mat, ctx->ld, (uint32_t)ctx->n_rows,
+                                                            (uint32_t)ctx->n_cols, pow2, approx, ctx->d_plane);
+  }
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  ctx->plane_valid = true;
+  ctx->plane_approx = approx;
+  return EBIC_OK;
+}
+
+struct SlabCfg {
+  int rpl = 1, sub = 1;
+  uint32_t rt = 32;
+  uint32_t chunk = 0;
+  size_t smem = 0;
+  bool ok = false;
+};
+
+SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
+  // Shared memory: the slab (RT rows x all C columns of plane words) plus 20 B per
+  // candidate of the chunk (16 B record + 4 B count).  Prefer more rows per lane
+  // (fewer per-candidate overheads per row) while the slab stays <= 128 KB.
+  SlabCfg c;
+  const size_t budget = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 1024;
+  const size_t C = ctx->n_cols;
+  const size_t kSlabCap = 128 * 1024;
+  bool found = false;
+  const int rpls[3] = {4, 2, 1};
+  for (int rpl : rpls) {
+    if (mask && rpl != 1) continue;
+    if (C * 32 * rpl * 4 <= kSlabCap) {
+      c.rpl = rpl;
+      c.sub = 1;
+      found = true;
+      break;
+    }
+  }
+  if (!found) {
+    if (mask) return c;
+    if (C * 16 * 4 <= 160 * 1024) { c.rpl = 1; c.sub = 2; }
+    else if (C * 8 * 4 <= 160 * 1024) { c.rpl = 1; c.sub = 4; }
+    else return c;
+  }
+  c.rt = (32 / c.sub) * c.rpl;
+  const size_t slab = C * c.rt * 4;
+  if (slab + 20 * 64 > budget) return c;
+  const uint64_t cmax = std::min<uint64_t>((budget - slab) / 20, 16384);
+  const uint64_t n_chunks = (n_cand + cmax - 1) / cmax;
+  c.chunk = (uint32_t)((n_cand + n_chunks - 1) / n_chunks);
+  c.smem = slab + (size_t)c.chunk * 20;
+  c.ok = true;
+  return c;
+}
+
+template <int RPL, int SUB, bool NEG, bool MASK>
+int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
+                  uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+  auto kern = ebic::slab_count_kernel<RPL, SUB, NEG, MASK>;
+  EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
+  ebic::SlabArgs a;
+  a.plane = ctx->d_plane;
+  a.ld = ctx->ld;
+  a.n_rows = (uint32_t)ctx->n_rows;
+  a.n_cols = (uint32_t)ctx->n_cols;
+  a.cols = d_cols;
+  a.offs = d_offs;
+  a.n_cand = (uint32_t)n_cand;
+  a.chunk = cfg.chunk;
+  a.n_chunks = (uint32_t)((n_cand + cfg.chunk - 1) / cfg.chunk);
+  a.n_slabs = (uint32_t)((ctx->n_rows + cfg.rt - 1) / cfg.rt);
+  a.counts = d_counts;
+  a.mask = d_mask;
+  a.mask_wpc = ctx->ld / 32;
+  a.err = ctx->d_err;
+  const uint64_t units = (uint64_t)a.n_chunks * a.n_slabs;
+  const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
+  kern<<<grid, ebic::kSlabThreads, cfg.smem, s>>>(a);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  return EBIC_OK;
+}
+
+template <bool NEG, bool MASK>
+int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
+                uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+  if constexpr (MASK) {
+    return launch_slab_t<1, 1, NEG, true>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+  } else {
+    if (cfg.sub == 1) {
+      if (cfg.rpl == 4) return launch_slab_t<4, 1, NEG, false>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+      if (cfg.rpl == 2) return launch_slab_t<2, 1, NEG, false>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+      return launch_slab_t<1, 1, NEG, false>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+    }
+    if (cfg.sub == 2) return launch_slab_t<1, 2, NEG, false>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+    return launch_slab_t<1, 4, NEG, false>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+  }
+}
+
 template <bool MASK>
 int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand,
                  double approx, int neg, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
   if (n_cand == 0) return EBIC_OK;
   if (n_cand > 0xffffffffull / 2) return fail(EBIC_ERR_INVALID_ARGUMENT, "too many candidates");
+  if (ctx->path != EBIC_PATH_VALUE && plane_fits(ctx)) {
+    const SlabCfg cfg = choose_slab(ctx, n_cand, MASK);
+    if (cfg.ok) {
+      EBIC_TRY(ensure_plane(ctx, approx, s));
+      if (neg) return launch_slab<true, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+      return launch_slab<false, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+    }
+  }
+  if (ctx->path == EBIC_PATH_PLANE)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "rank-plane path unavailable for a %llu-column matrix",
+                (unsigned long long)ctx->n_cols);
   const ebic::TrendArgs ta = make_args(approx, neg);
   const bool a0 = (approx == 0.0);
   if (ctx->store == EBIC_STORE_F32) {
@@ -349,6 +489,14 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     return fail(EBIC_ERR_CUDA, "context creation on device %d: %s", device, cudaGetErrorString(e));
   }
   ctx->stream = ctx->own_stream;
+  {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) ctx->n_sms = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)
+      ctx->smem_optin = (size_t)v;
+    const char* e = std::getenv("EBIC_PATH");
+    if (e) ctx->path = std::atoi(e);
+  }
   *ctx_out = ctx;
   return EBIC_OK;
 }
@@ -429,6 +577,9 @@ int ebic_matrix_free(ebic_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->d_mat);
   }
+  if (ctx->d_plane) cudaFree(ctx->d_plane);
+  ctx->d_plane = nullptr;
+  ctx->plane_valid = false;
   ctx->d_mat = nullptr;
   ctx->store = 0;
   ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
@@ -616,6 +767,23 @@ int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows) {
   if (slab_rows % ebic::kRowAlign)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "slab_rows must be a multiple of %u", ebic::kRowAlign);
   ctx->slab_rows = slab_rows;
+  return EBIC_OK;
+}
+
+int ebic_ctx_set_path(ebic_ctx* ctx, int path) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_PLANE) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
+  ctx->path = path;
+  return EBIC_OK;
+}
+
+int ebic_matrix_prepare(ebic_ctx* ctx, double approx) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  EBIC_TRY(set_device(ctx));
+  if (ctx->path == EBIC_PATH_VALUE || !plane_fits(ctx)) return EBIC_OK;
+  EBIC_TRY(ensure_plane(ctx, approx, ctx->stream));
+  EBIC_CUDA(cudaStreamSynchronize(ctx->stream));
   return EBIC_OK;
 }
 

@@ -149,6 +149,14 @@ class Evaluator:
     def set_slab_rows(self, slab_rows: int) -> None:
         check(self._L.ebic_ctx_set_slab_rows(self._h, int(slab_rows)))
 
+    def set_path(self, path: int) -> None:
+        """EBIC_PATH_AUTO (rank-plane slab kernel when C <= 8192) / _VALUE / _PLANE."""
+        check(self._L.ebic_ctx_set_path(self._h, int(path)))
+
+    def prepare(self, approx: float) -> None:
+        """Build the rank plane for `approx` now (otherwise built on first use)."""
+        check(self._L.ebic_matrix_prepare(self._h, float(approx)))
+
     # -- matrix store ------------------------------------------------------
     def upload(self, matrix: np.ndarray, row_base: int = 0, store: int = EBIC_STORE_AUTO) -> int:
         """Upload a row-major (R, C) matrix (float64 or float32).  Returns the store mode."""

@@ -13,6 +13,8 @@ timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fitness_count -s 5 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slab_count|fitness_count" -s 5 -c 1 \
     -o $OUT/prof_c3_$TAG -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1
 echo done
+timeout 600 python bench.py --steps 10 --warmup 3 --path value --no-cpu-baseline > $OUT/bench_value_$TAG.json 2> $OUT/bench_value_$TAG.err
+for c in c2 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_${c}_$TAG.json 2> $OUT/bench_${c}_$TAG.err; done

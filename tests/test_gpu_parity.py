@@ -10,8 +10,18 @@ from conftest import golden_cases, load_golden
 from paper_2105_01196_b200 import (EBIC_STORE_AUTO, EBIC_STORE_F32, EBIC_STORE_F64, EbicError, Population,
                                    TrendParams)
 from paper_2105_01196_b200 import synth
+from paper_2105_01196_b200._lib import EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_VALUE
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=[EBIC_PATH_AUTO, EBIC_PATH_VALUE], ids=["plane", "value"])
+def path_evaluator(evaluator, request):
+    """The same checks on both exact evaluation paths: the rank-plane slab kernel
+    (default for <= 8192 columns) and the float value kernel."""
+    evaluator.set_path(request.param)
+    yield evaluator
+    evaluator.set_path(EBIC_PATH_AUTO)
 
 
 def _tp(s):
@@ -20,7 +30,8 @@ def _tp(s):
 
 @pytest.mark.parametrize("name", golden_cases())
 @pytest.mark.parametrize("store", [EBIC_STORE_AUTO, EBIC_STORE_F64])
-def test_counts_and_rows_match_reference_golden(evaluator, name, store):
+def test_counts_and_rows_match_reference_golden(path_evaluator, name, store):
+    evaluator = path_evaluator
     z, settings = load_golden(name)
     m = z["matrix"]
     chosen = evaluator.upload(m, store=store)
@@ -64,7 +75,8 @@ def _random_case(rng, R, Cn, f32=True, max_len=12):
 
 @pytest.mark.parametrize("R", [1, 31, 256, 257, 1000, 4097])
 @pytest.mark.parametrize("f32", [True, False])
-def test_random_shapes_vs_oracle(evaluator, R, f32):
+def test_random_shapes_vs_oracle(path_evaluator, R, f32):
+    evaluator = path_evaluator
     rng = np.random.default_rng(R * 7 + f32)
     m, pop = _random_case(rng, R, 40, f32)
     evaluator.upload(m)
@@ -97,7 +109,8 @@ def _near_threshold_matrix(rng, R, Cn, approx):
 
 
 @pytest.mark.parametrize("approx", [0.03, 0.1, 0.5, 2**-20])
-def test_filter_uncertain_band_is_exact(evaluator, approx):
+def test_filter_uncertain_band_is_exact(path_evaluator, approx):
+    evaluator = path_evaluator
     rng = np.random.default_rng(11)
     m = _near_threshold_matrix(rng, 3000, 12, approx)
     assert np.array_equal(m.astype(np.float32).astype(np.float64), m)
@@ -112,7 +125,8 @@ def test_filter_uncertain_band_is_exact(evaluator, approx):
         assert want.sum() > 0
 
 
-def test_subnormal_and_huge_values(evaluator):
+def test_subnormal_and_huge_values(path_evaluator):
+    evaluator = path_evaluator
     rng = np.random.default_rng(5)
     vals = np.array([0.0, -0.0, 1e-45, -1e-45, 1.2e-38, -1.2e-38, 3.4e38, -3.4e38, 1.0, -1.0, 5e-40, -5e-40],
                     dtype=np.float32).astype(np.float64)
@@ -127,7 +141,8 @@ def test_subnormal_and_huge_values(evaluator):
             np.testing.assert_array_equal(got, want)
 
 
-def test_long_sequences_cross_smem_chunks(evaluator):
+def test_long_sequences_cross_smem_chunks(path_evaluator):
+    evaluator = path_evaluator
     rng = np.random.default_rng(9)
     m = rng.standard_normal((5000, 300)).astype(np.float32)
     # sorted rows make long trends survive, so the column loop runs past the 64-index SMEM chunk
@@ -151,7 +166,8 @@ def _config_matrix(rows, cols, bic_rows, bic_cols, seed=1):
     return m
 
 
-def test_config2_bit_exact(evaluator):
+def test_config2_bit_exact(path_evaluator):
+    evaluator = path_evaluator
     """BASELINE config 2: 10k x 500, P=4096, bit-exact counts vs the CPU oracle."""
     m = _config_matrix(10_000, 500, 500, 20)
     if oracle.reference_available():
@@ -204,7 +220,8 @@ def test_config4_full_size_properties(evaluator):
 
 
 @pytest.mark.parametrize("R", [1024, 65536, 1_000_000])
-def test_microbench_shapes(evaluator, R):
+def test_microbench_shapes(path_evaluator, R):
+    evaluator = path_evaluator
     rng = np.random.default_rng(R)
     m = rng.standard_normal((R, 64), dtype=np.float32)
     evaluator.upload(m)
@@ -296,6 +313,38 @@ def test_errors_are_reported_not_undefined(evaluator):
 def test_launches_are_counted(evaluator):
     m = np.random.default_rng(0).standard_normal((1000, 10)).astype(np.float32)
     evaluator.upload(m)
+    evaluator.prepare(0.03)  # builds the rank plane for approx 0.03 (one launch)
     n0 = evaluator.launch_count()
     evaluator.evaluate_population([[0, 1, 2]] * 10)
     assert evaluator.launch_count() == n0 + 1
+    evaluator.set_path(EBIC_PATH_VALUE)
+    evaluator.evaluate_population([[0, 1, 2]] * 10)
+    assert evaluator.launch_count() == n0 + 2
+    evaluator.set_path(EBIC_PATH_AUTO)
+
+
+def test_plane_is_rebuilt_per_approx_and_matrix(evaluator):
+    rng = np.random.default_rng(8)
+    m = rng.standard_normal((3000, 30)).astype(np.float32)
+    pop = synth.random_population(500, 30, seed=3)
+    evaluator.upload(m)
+    evaluator.set_path(EBIC_PATH_PLANE)
+    try:
+        for approx in (0.03, 0.0, 0.03, 0.5):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, True)
+            np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, True)), want)
+        m2 = m[::-1].copy()
+        evaluator.upload(m2)
+        want = oracle.evaluate_population(m2, pop.cols, pop.offsets, 0.5, True)
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(0.5, True)), want)
+        # wider than the plane's column limit -> PLANE is refused, AUTO falls back to the value kernel
+        wide = rng.standard_normal((64, 9000)).astype(np.float32)
+        evaluator.upload(wide)
+        with pytest.raises(EbicError):
+            evaluator.evaluate_population([[0, 1, 8999]])
+        evaluator.set_path(EBIC_PATH_AUTO)
+        want = oracle.evaluate_population(wide, np.array([0, 1, 8999], np.uint32), np.array([0, 3], np.uint32), 0.03,
+                                          False)
+        np.testing.assert_array_equal(evaluator.evaluate_population([[0, 1, 8999]]), want)
+    finally:
+        evaluator.set_path(EBIC_PATH_AUTO)
