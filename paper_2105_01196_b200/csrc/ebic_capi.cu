@@ -240,11 +240,13 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
   }
   c.rt = (32 / c.sub) * c.rpl;
   const size_t slab = C * c.rt * 4;
-  if (slab + 20 * 64 > budget) return c;
-  const uint64_t cmax = std::min<uint64_t>((budget - slab) / 20, 16384);
+  // records: chunk + class padding (ebic::kClasses x sweep stride), 16 B each; counts: chunk + 1
+  const size_t fixed = slab + (size_t)ebic::kClasses * ebic::kSlabWarps * c.sub * 16 + 16;
+  if (fixed + 20 * 64 > budget) return c;
+  const uint64_t cmax = std::min<uint64_t>((budget - fixed) / 20, 16384);
   const uint64_t n_chunks = (n_cand + cmax - 1) / cmax;
   c.chunk = (uint32_t)((n_cand + n_chunks - 1) / n_chunks);
-  c.smem = slab + (size_t)c.chunk * 20;
+  c.smem = fixed + (size_t)c.chunk * 20;
   c.ok = true;
   return c;
 }

@@ -95,14 +95,6 @@ build_plane_kernel(const T* __restrict__ store, uint64_t ld, uint32_t n_rows, ui
   }
 }
 
-// ---------------------------------------------------------------------------
-// slab kernel
-//   RPL : consecutive rows per lane (1, 2, 4)   -> LDS.32 / .64 / .128
-//   SUB : candidates per warp (1, 2, 4)          -> 32/SUB lanes per candidate
-//   RT  = (32 / SUB) * RPL rows per slab
-// work unit = (candidate chunk, row slab), linearised chunk-major; CTA b owns
-// units [b*U/G, (b+1)*U/G).
-// ---------------------------------------------------------------------------
 template <int RPL> struct LdsVec;
 template <> struct LdsVec<1> { using V = uint32_t; };
 template <> struct LdsVec<2> { using V = uint2; };
@@ -110,6 +102,25 @@ template <> struct LdsVec<4> { using V = uint4; };
 __device__ __forceinline__ uint32_t vel(const uint32_t& v, int) { return v; }
 __device__ __forceinline__ uint32_t vel(const uint2& v, int i) { return i == 0 ? v.x : v.y; }
 __device__ __forceinline__ uint32_t vel(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+// explicit shared-space loads on 32-bit shared addresses (no generic->shared
+// conversion inside the candidate loop)
+__device__ __forceinline__ uint32_t lds_v(uint32_t addr, uint32_t*) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v(uint32_t addr, uint2*) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v(uint32_t addr, uint4*) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+template <typename V> __device__ __forceinline__ V lds(uint32_t addr) { return lds_v(addr, (V*)nullptr); }
 
 struct SlabArgs {
   const uint32_t* plane;
@@ -127,19 +138,140 @@ struct SlabArgs {
   int* err;
 };
 
+// One consecutive-pair test on RPL rows: forward needs c > thr(p), reversed p > thr(c).
+template <int RPL, bool NEG, typename V>
+__device__ __forceinline__ void pair_test(const V& wp, const V& wc, uint32_t& okf, uint32_t& okr) {
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const uint32_t p = vel(wp, r), c = vel(wc, r);
+    if (!(c > plane_key(p))) okf &= ~(1u << r);
+    if (NEG && !(p > plane_key(c))) okr &= ~(1u << r);
+  }
+}
+
+// Fixed-length body: all L loads issued first (ILP), then the L-1 pair tests.
+// Returns the RPL support bits of this lane's rows (before validity masking).
+// u16 halves of a record word, one PRMT each
+__device__ __forceinline__ uint32_t lo16(uint32_t x) { return __byte_perm(x, 0u, 0x4410); }
+__device__ __forceinline__ uint32_t hi16(uint32_t x) { return __byte_perm(x, 0u, 0x4432); }
+
+template <int L, int RPL, bool NEG, uint32_t COLSHIFT>
+__device__ __forceinline__ uint32_t eval_fixed(uint32_t lane_base, const uint4& rec) {
+  using V = typename LdsVec<RPL>::V;
+  const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
+                                 hi16(rec.z), lo16(rec.w), hi16(rec.w)};
+  V w[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) w[k] = lds<V>(lane_base + (cc[k] << COLSHIFT));
+  if constexpr (RPL == 1) {
+    bool f = true, r = NEG;
+#pragma unroll
+    for (int k = 1; k < L; ++k) {
+      f = f && (w[k] > plane_key(w[k - 1]));
+      if (NEG) r = r && (w[k - 1] > plane_key(w[k]));
+    }
+    return (f || r) ? 1u : 0u;
+  } else {
+    uint32_t okf = (1u << RPL) - 1u, okr = NEG ? okf : 0u;
+#pragma unroll
+    for (int k = 1; k < L; ++k) pair_test<RPL, NEG>(w[k - 1], w[k], okf, okr);
+    return okf | okr;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// slab kernel
+//   RPL : consecutive rows per lane (1, 2, 4)   -> LDS.32 / .64 / .128
+//   SUB : candidates per warp (1, 2, 4)          -> 32/SUB lanes per candidate
+//   RT  = (32 / SUB) * RPL rows per slab
+// work unit = (candidate chunk, row slab), linearised chunk-major; CTA b owns
+// units [b*U/G, (b+1)*U/G).
+// ---------------------------------------------------------------------------
+// Per-length record classes: class L (2..7) holds candidates of exactly L
+// columns, class 1 length-1 candidates, class 8 everything longer (first 7
+// columns in the record, the tail read from the CSR).  Sorting a chunk's
+// records by class once lets the sweep run a branch-free, fully unrolled body
+// per class instead of dispatching on the length of every candidate.
+constexpr int kClasses = 9;  // 0 (invalid) .. 8
+
+template <int RPL, int SUB, bool NEG, bool MASK, int L, uint32_t COLSHIFT>
+__device__ __forceinline__ void sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_base, uint32_t* s_cnt,
+                                            uint32_t n_padded, uint32_t class_base, uint32_t c_begin,
+                                            uint32_t row0, uint32_t vmask, int warp, int lane, int sub, int rl) {
+  // Each class list is padded to a multiple of the sweep stride with dummy
+  // records (candidate slot `chunk`, a scratch count), so every (warp, sub)
+  // slot has a record on every iteration: no bounds checks in the loop.
+  constexpr int LPC = 32 / SUB;
+  using V = typename LdsVec<RPL>::V;
+  constexpr uint32_t stride = kSlabWarps * SUB;
+  for (uint32_t t = warp * SUB + sub; t < n_padded; t += stride) {
+    const uint4 rec = lds<uint4>(sa_rec + (class_base + t) * 16);
+    const uint32_t j = lo16(rec.x);
+    uint32_t ok;
+    if constexpr (L == 1) {
+      ok = vmask;  // no pair: every row supports (the trend.cpp:19 loop never runs)
+    } else if constexpr (L < 8) {
+      ok = eval_fixed<L, RPL, NEG, COLSHIFT>(lane_base, rec) & vmask;
+    } else {
+      // >= 8 columns: the first 7 from the record, the tail from the CSR
+      uint32_t okf = vmask, okr = NEG ? vmask : 0u;
+      const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
+                                     hi16(rec.z), lo16(rec.w), hi16(rec.w)};
+      V wp = lds<V>(lane_base + (cc[0] << COLSHIFT));
+#pragma unroll
+      for (int k = 1; k < kRecCols; ++k) {
+        const V wc = lds<V>(lane_base + (cc[k] << COLSHIFT));
+        pair_test<RPL, NEG>(wp, wc, okf, okr);
+        wp = wc;
+      }
+      if (j < a.chunk) {
+        const uint32_t b = a.offs[c_begin + j], e = a.offs[c_begin + j + 1];
+        for (uint32_t k = b + kRecCols; k < e; ++k) {
+          if ((okf | okr) == 0u) break;  // this lane's rows are all decided
+          const V wc = lds<V>(lane_base + (__ldg(a.cols + k) << COLSHIFT));
+          pair_test<RPL, NEG>(wp, wc, okf, okr);
+          wp = wc;
+        }
+      }
+      ok = okf | okr;
+    }
+    if constexpr (MASK) {
+      static_assert(!MASK || (RPL == 1 && SUB == 1), "mask output needs one row per lane");
+      const uint32_t word = __ballot_sync(kFull, ok & 1u);
+      if (lane == 0 && j < a.chunk) {
+        a.mask[(uint64_t)(c_begin + j) * a.mask_wpc + row0 / 32] = word;
+        atomicAdd(&s_cnt[j], (uint32_t)__popc(word));
+      }
+    } else if constexpr (RPL == 1) {
+      const uint32_t b = __ballot_sync(kFull, ok & 1u);
+      const uint32_t n = SUB == 1 ? __popc(b) : __popc((b >> (sub * LPC)) & ((1u << LPC) - 1u));
+      if (rl == 0) atomicAdd(&s_cnt[j], n);  // sole owner of candidate j in this CTA
+    } else {
+      static_assert(RPL == 1 || SUB == 1, "multi-row lanes use whole warps");
+      const uint32_t n = __reduce_add_sync(kFull, (uint32_t)__popc(ok));
+      if (lane == 0) atomicAdd(&s_cnt[j], n);
+    }
+  }
+}
+
 template <int RPL, int SUB, bool NEG, bool MASK>
 __global__ void __launch_bounds__(kSlabThreads, 1)
 slab_count_kernel(const SlabArgs a) {
   constexpr int LPC = 32 / SUB;        // lanes per candidate
   constexpr uint32_t RT = LPC * RPL;   // rows per slab
-  using V = typename LdsVec<RPL>::V;
+  constexpr uint32_t COLSHIFT = RT == 8 ? 5 : RT == 16 ? 6 : RT == 32 ? 7 : RT == 64 ? 8 : 9;  // log2(RT*4)
+  static_assert((4u * RT) == (1u << COLSHIFT), "RT must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][RT]
-  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + (size_t)a.n_cols * RT);  // [chunk]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rec + a.chunk);          // [chunk]
+  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + (size_t)a.n_cols * RT);  // [chunk], sorted by class
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rec + a.chunk + kClasses * kSlabWarps * SUB);  // [chunk+1]
+  __shared__ uint32_t s_hist[kClasses], s_base[kClasses], s_fill[kClasses];
+  const uint32_t sa_slab = (uint32_t)__cvta_generic_to_shared(s_slab);
+  const uint32_t sa_rec = (uint32_t)__cvta_generic_to_shared(s_rec);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / LPC, rl = lane % LPC;
+  const uint32_t lane_base = sa_slab + rl * RPL * 4;
   const uint64_t U = (uint64_t)a.n_chunks * a.n_slabs;
   const uint64_t u_begin = blockIdx.x * U / gridDim.x, u_end = (blockIdx.x + 1) * U / gridDim.x;
 
@@ -150,6 +282,13 @@ slab_count_kernel(const SlabArgs a) {
     for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x)
       if (s_cnt[j]) atomicAdd(&a.counts[c_begin + j], s_cnt[j]);
   };
+  auto class_of = [&](uint32_t i, uint32_t& len, bool& bad) -> uint32_t {
+    const uint32_t b = a.offs[i], e = a.offs[i + 1];
+    len = e > b ? e - b : 0;
+    bad = len == 0;
+    for (uint32_t k = b; k < e && !bad; ++k) bad |= a.cols[k] >= a.n_cols;
+    return bad ? 0u : min(len, 8u);
+  };
 
   for (uint64_t u = u_begin; u < u_end; ++u) {
     const uint32_t chunk = (uint32_t)(u / a.n_slabs), slab = (uint32_t)(u % a.n_slabs);
@@ -157,117 +296,86 @@ slab_count_kernel(const SlabArgs a) {
     __syncthreads();  // previous slab / counts fully consumed
     if (chunk != cur_chunk) {
       flush();
+      if (threadIdx.x < kClasses) s_hist[threadIdx.x] = 0;
       __syncthreads();
       cur_chunk = chunk;
       c_begin = chunk * a.chunk;
       c_n = min(a.chunk, a.n_cand - c_begin);
-      // pack candidate records: 7 x u16 columns + u16 length
+      // pass 1: class histogram (+ validation)
       for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
-        const uint32_t i = c_begin + j;
-        const uint32_t b = a.offs[i], e = a.offs[i + 1];
-        const uint32_t len = e > b ? e - b : 0;
-        uint32_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        bool bad = len == 0 || len > 0xFFFFu;
-#pragma unroll
-        for (int k = 0; k < kRecCols; ++k) {
-          if ((uint32_t)k < len) {
-            h[k] = a.cols[b + k];
-            bad |= h[k] >= a.n_cols;
-          }
-        }
-        for (uint32_t k = kRecCols; k < len && !bad; ++k) bad |= a.cols[b + k] >= a.n_cols;
-        if (bad) {
-          atomicOr(a.err, 1);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) h[k] = 0;  // len 0: counted as 0
-        } else {
-          h[7] = len;
-        }
-        s_rec[j] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+        uint32_t len;
+        bool bad;
+        const uint32_t cl = class_of(c_begin + j, len, bad);
+        if (bad) atomicOr(a.err, 1);
+        atomicAdd(&s_hist[cl], 1u);
         s_cnt[j] = 0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int c = 0; c < kClasses; ++c) {
+          s_base[c] = acc;
+          s_fill[c] = 0;
+          s_hist[c] = (s_hist[c] + kSlabWarps * SUB - 1) / (kSlabWarps * SUB) * (kSlabWarps * SUB);
+          acc += s_hist[c];
+        }
+        s_cnt[a.chunk] = 0;  // scratch count of the padding records
+      }
+      __syncthreads();
+      // padding records: candidate slot `chunk`, every column 0
+      for (int c = 1; c < kClasses; ++c)
+        for (uint32_t t = threadIdx.x; t < s_hist[c]; t += blockDim.x)
+          s_rec[s_base[c] + t] = make_uint4(a.chunk, 0u, 0u, 0u);
+      __syncthreads();
+      // pass 2: records {u16 candidate, 7 x u16 columns}, scattered by class
+      for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
+        uint32_t len;
+        bool bad;
+        const uint32_t cl = class_of(c_begin + j, len, bad);
+        const uint32_t b = a.offs[c_begin + j];
+        uint32_t h[8] = {j, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < kRecCols; ++k)
+          if (!bad && (uint32_t)k < len) h[k + 1] = a.cols[b + k];
+        const uint32_t pos = s_base[cl] + atomicAdd(&s_fill[cl], 1u);
+        s_rec[pos] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
       }
     }
     // stage the slab: rows [row0, row0+RT) of every column (RT*4 bytes contiguous per column)
     {
       constexpr uint32_t V4 = RT / 4;  // uint4 per column
-      const uint64_t total = (uint64_t)a.n_cols * V4;
+      const uint32_t total = a.n_cols * V4;
       const uint4* src = reinterpret_cast<const uint4*>(a.plane);
       uint4* dst = reinterpret_cast<uint4*>(s_slab);
-      for (uint64_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint64_t c = t / V4, q = t % V4;
-        dst[t] = __ldg(src + (c * a.ld + row0) / 4 + q);
+      const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
+#pragma unroll 4
+      for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint32_t c = t / V4, q = t % V4;
+        dst[t] = __ldg(src + c * ld4 + r4 + q);
       }
     }
     __syncthreads();
 
     const uint32_t valid_rows = min(RT, a.n_rows - row0);
-    // per-lane row validity bits
-    uint32_t vmask = 0;
+    uint32_t vmask = 0;  // validity bits of this lane's RPL rows
 #pragma unroll
     for (int j = 0; j < RPL; ++j) vmask |= (rl * RPL + j < valid_rows ? 1u : 0u) << j;
 
-    const uint32_t n_iter = (c_n + kSlabWarps * SUB - 1) / (kSlabWarps * SUB);
-    for (uint32_t it = 0; it < n_iter; ++it) {
-      const uint32_t j = (it * kSlabWarps + warp) * SUB + sub;  // candidate within chunk
-      const bool have = j < c_n;
-      uint32_t okf = 0, okr = 0;
-      if (have) {
-        const uint4 rec = s_rec[j];
-        const uint32_t len = rec.w >> 16;
-        uint32_t cc[kRecCols] = {rec.x & 0xFFFFu, rec.x >> 16, rec.y & 0xFFFFu, rec.y >> 16,
-                                 rec.z & 0xFFFFu, rec.z >> 16, rec.w & 0xFFFFu};
-        const uint32_t lane_off = rl * RPL;
-        V wp = *reinterpret_cast<const V*>(s_slab + cc[0] * RT + lane_off);
-        okf = len ? vmask : 0u;
-        okr = NEG ? okf : 0u;
-#pragma unroll
-        for (int k = 1; k < kRecCols; ++k) {
-          if ((uint32_t)k < len) {
-            const V wc = *reinterpret_cast<const V*>(s_slab + cc[k] * RT + lane_off);
-#pragma unroll
-            for (int r = 0; r < RPL; ++r) {
-              const uint32_t p = vel(wp, r), c = vel(wc, r);
-              okf &= ~((c > plane_key(p) ? 0u : 1u) << r);
-              if (NEG) okr &= ~((p > plane_key(c) ? 0u : 1u) << r);
-            }
-            wp = wc;
-          }
-        }
-        if (len > kRecCols) {
-          // long candidate: continue from the CSR (rare; evolved populations have L <= ~10)
-          const uint32_t* gc = a.cols + a.offs[c_begin + j];
-          for (uint32_t k = kRecCols; k < len; ++k) {
-            if ((okf | okr) == 0u) break;  // per-lane: nothing left to decide
-            const V wc = *reinterpret_cast<const V*>(s_slab + gc[k] * RT + lane_off);
-#pragma unroll
-            for (int r = 0; r < RPL; ++r) {
-              const uint32_t p = vel(wp, r), c = vel(wc, r);
-              okf &= ~((c > plane_key(p) ? 0u : 1u) << r);
-              if (NEG) okr &= ~((p > plane_key(c) ? 0u : 1u) << r);
-            }
-            wp = wc;
-          }
-        }
-      }
-      const uint32_t ok = okf | okr;  // RPL bits, one per row of this lane
-      if (MASK) {
-        static_assert(!MASK || (RPL == 1 && SUB == 1), "mask output needs one row per lane");
-        const uint32_t word = __ballot_sync(kFull, ok & 1u);
-        if (have && lane == 0) a.mask[(uint64_t)(c_begin + j) * a.mask_wpc + row0 / 32] = word;
-        if (have && lane == 0 && word) s_cnt[j] += __popc(word);
-      } else {
-        uint32_t n;
-        if (RPL == 1) {
-          const uint32_t b = __ballot_sync(kFull, ok & 1u);
-          n = SUB == 1 ? __popc(b) : __popc((b >> (sub * LPC)) & (LPC == 32 ? 0xffffffffu : ((1u << LPC) - 1u)));
-        } else {
-          n = __popc(ok);
-          // reduce within the lanes of this candidate
-#pragma unroll
-          for (int s = LPC / 2; s > 0; s >>= 1) n += __shfl_xor_sync(kFull, n, s);
-        }
-        if (have && rl == 0 && n) s_cnt[j] += n;
-      }
+#define EBIC_SWEEP(L)                                                                                   \
+  sweep_class<RPL, SUB, NEG, MASK, L, COLSHIFT>(a, sa_rec, lane_base, s_cnt, s_hist[L], s_base[L], c_begin, \
+                                                row0, vmask, warp, lane, sub, rl)
+    EBIC_SWEEP(4);
+    EBIC_SWEEP(3);
+    EBIC_SWEEP(5);
+    EBIC_SWEEP(2);
+    EBIC_SWEEP(6);
+    EBIC_SWEEP(7);
+    EBIC_SWEEP(8);
+    EBIC_SWEEP(1);
+#undef EBIC_SWEEP
+    if constexpr (MASK) {
+      // invalid candidates (class 0) still need their mask words cleared: the
+      // host memsets the mask before the launch, so nothing to do here.
     }
   }
   __syncthreads();
