@@ -358,7 +358,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     else:
         call = ev.evaluate_population
     ev.set_stream(None)
-    for i in range(3):
+    for i in range(max(args.warmup, 8)):  # >= 2x the marshaller ring: every pinned slot allocated
         call(pops[i % n_pops], tp)
     for i in range(args.steps):
         flush.fill_(float(i))
@@ -399,8 +399,8 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                    "shard": args.shard, "path": args.path},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, world),
-                     "kernel": "slab_count_kernel (rank plane)" if (args.path != "value" and Ccols <= 8192)
-                     else "fitness_count_kernel (value)", "kernel_avg_ms": kern_avg_s * 1e3,
+                     "kernel": ("slab_simd_kernel (packed rank pairs)" if Ccols <= 1024 else "slab_count_kernel (rank plane)")
+                     if (args.path != "value" and Ccols <= 8192) else "fitness_count_kernel (value)", "kernel_avg_ms": kern_avg_s * 1e3,
                      "algorithmic_bytes_per_launch": statistics.mean(alg_bytes),
                      "peak_source": peak_src,
                      "note": "algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "

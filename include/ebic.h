@@ -153,13 +153,16 @@ int ebic_ctx_launch_count(ebic_ctx* ctx, uint64_t* n_out);
 /* Tuning knob for the value-path kernel: rows per CTA slab (0 = auto). */
 int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
 
-/* Evaluation path.  AUTO: the rank-plane slab kernel whenever the matrix has
- * <= 8192 columns, else the value kernel.  VALUE / PLANE force one (PLANE
- * fails with EBIC_ERR_INVALID_ARGUMENT if the matrix is too wide).  Both are
+/* Evaluation path.  AUTO: the rank-plane slab kernels whenever the matrix has
+ * <= 8192 columns (packed 16-bit rank pairs when a 32-row slab fits in shared
+ * memory, else 32-bit plane words), otherwise the value kernel.  VALUE, PLANE
+ * and PLANE_U32 (32-bit plane words only) force one; the plane paths fail
+ * with EBIC_ERR_INVALID_ARGUMENT if the matrix is too wide.  All are
  * bit-exact; the knob exists for cross-checking and benchmarking. */
 #define EBIC_PATH_AUTO 0
 #define EBIC_PATH_VALUE 1
 #define EBIC_PATH_PLANE 2
+#define EBIC_PATH_PLANE_U32 3
 int ebic_ctx_set_path(ebic_ctx* ctx, int path);
 
 /* Build (or reuse) the rank plane of the resident matrix for `approx` now,

@@ -56,6 +56,7 @@ SIGNATURES = {
 EBIC_PATH_AUTO = 0
 EBIC_PATH_VALUE = 1
 EBIC_PATH_PLANE = 2
+EBIC_PATH_PLANE_U32 = 3
 
 
 class EbicError(RuntimeError):

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include "ebic.h"
 #include "ebic_kernels.cuh"
 #include "ebic_plane.cuh"
+#include "ebic_simd.cuh"
 
 namespace {
 
@@ -72,8 +74,9 @@ struct HostBuf {
 template <typename T>
 int ensure(DevBuf<T>& b, size_t n) {
   if (b.n >= n && b.p) return EBIC_OK;
+  const size_t old = b.n;
   b.release();
-  size_t cap = std::max<size_t>(n, 1024);
+  size_t cap = std::max<size_t>(std::max<size_t>(n, 1024), old + old / 2);
   EBIC_CUDA(cudaMalloc(&b.p, cap * sizeof(T)));
   b.n = cap;
   return EBIC_OK;
@@ -82,8 +85,9 @@ int ensure(DevBuf<T>& b, size_t n) {
 template <typename T>
 int ensure(HostBuf<T>& b, size_t n) {
   if (b.n >= n && b.p) return EBIC_OK;
+  const size_t old = b.n;
   b.release();
-  size_t cap = std::max<size_t>(n, 1024);
+  size_t cap = std::max<size_t>(std::max<size_t>(n, 1024), old + old / 2);
   EBIC_CUDA(cudaMallocHost(&b.p, cap * sizeof(T)));
   b.n = cap;
   return EBIC_OK;
@@ -206,6 +210,8 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
 }
 
 struct SlabCfg {
+  bool simd = false;  // packed 16-bit rank pairs (slab_simd_kernel); p = pair-words per lane
+  int p = 1;
   int rpl = 1, sub = 1;
   uint32_t rt = 32;
   uint32_t chunk = 0;
@@ -222,6 +228,32 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
   const size_t C = ctx->n_cols;
   const size_t kSlabCap = 128 * 1024;
   bool found = false;
+  if (!mask && ctx->path != EBIC_PATH_PLANE_U32) {
+    // packed pairs: the largest slab (most rows per lane) that fits
+    struct Opt { int p, sub; uint32_t rt; };
+    // (P = 4 would need > 64 registers per thread at 1024 threads: spills)
+    const Opt opts[3] = {{2, 1, 128}, {1, 1, 64}, {1, 2, 32}};
+    for (const Opt& o : opts) {
+      if (C * o.rt * 4 <= kSlabCap) {
+        c.simd = true;
+        c.p = o.p;
+        c.sub = o.sub;
+        c.rt = o.rt;
+        found = true;
+        break;
+      }
+    }
+  }
+  if (found) {
+    const size_t slab = C * c.rt * 4;
+    const size_t fixed = slab + (size_t)ebic::kClasses * ebic::kSlabWarps * c.sub * 16 + 16;
+    const uint64_t cmax = std::min<uint64_t>((budget - fixed) / 20, 16384);
+    const uint64_t n_chunks = (n_cand + cmax - 1) / cmax;
+    c.chunk = (uint32_t)((n_cand + n_chunks - 1) / n_chunks);
+    c.smem = fixed + (size_t)c.chunk * 20;
+    c.ok = true;
+    return c;
+  }
   const int rpls[3] = {4, 2, 1};
   for (int rpl : rpls) {
     if (mask && rpl != 1) continue;
@@ -251,11 +283,8 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
   return c;
 }
 
-template <int RPL, int SUB, bool NEG, bool MASK>
-int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
-                  uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
-  auto kern = ebic::slab_count_kernel<RPL, SUB, NEG, MASK>;
-  EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
+ebic::SlabArgs make_slab_args(const ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols,
+                              const uint32_t* d_offs, uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask) {
   ebic::SlabArgs a;
   a.plane = ctx->d_plane;
   a.ld = ctx->ld;
@@ -271,6 +300,40 @@ int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, con
   a.mask = d_mask;
   a.mask_wpc = ctx->ld / 32;
   a.err = ctx->d_err;
+  return a;
+}
+
+template <int RPL, int SUB, bool NEG, bool MASK>
+int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
+                  uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+  auto kern = ebic::slab_count_kernel<RPL, SUB, NEG, MASK>;
+  // raise the dynamic shared-memory limit once per (kernel, device), to the opt-in maximum
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t bit = 1ull << (ctx->device & 63);
+  if (!(attr_done.load(std::memory_order_relaxed) & bit)) {
+    EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ctx->smem_optin - 1024)));
+    attr_done.fetch_or(bit);
+  }
+  ebic::SlabArgs a = make_slab_args(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask);
+  const uint64_t units = (uint64_t)a.n_chunks * a.n_slabs;
+  const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
+  kern<<<grid, ebic::kSlabThreads, cfg.smem, s>>>(a);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  return EBIC_OK;
+}
+
+template <int P, int SUB, bool NEG>
+int launch_simd_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
+                  uint64_t n_cand, uint32_t* d_counts, cudaStream_t s) {
+  auto kern = ebic::slab_simd_kernel<P, SUB, NEG>;
+  static std::atomic<uint64_t> attr_done{0};
+  const uint64_t bit = 1ull << (ctx->device & 63);
+  if (!(attr_done.load(std::memory_order_relaxed) & bit)) {
+    EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ctx->smem_optin - 1024)));
+    attr_done.fetch_or(bit);
+  }
+  ebic::SlabArgs a = make_slab_args(ctx, cfg, d_cols, d_offs, n_cand, d_counts, nullptr);
   const uint64_t units = (uint64_t)a.n_chunks * a.n_slabs;
   const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
   kern<<<grid, ebic::kSlabThreads, cfg.smem, s>>>(a);
@@ -282,6 +345,13 @@ int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, con
 template <bool NEG, bool MASK>
 int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
                 uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+  if constexpr (!MASK) {
+    if (cfg.simd) {
+      if (cfg.p == 2) return launch_simd_t<2, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      if (cfg.sub == 1) return launch_simd_t<1, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      return launch_simd_t<1, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+    }
+  }
   if constexpr (MASK) {
     return launch_slab_t<1, 1, NEG, true>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
   } else {
@@ -308,7 +378,7 @@ int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
       return launch_slab<false, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
     }
   }
-  if (ctx->path == EBIC_PATH_PLANE)
+  if (ctx->path == EBIC_PATH_PLANE || ctx->path == EBIC_PATH_PLANE_U32)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "rank-plane path unavailable for a %llu-column matrix",
                 (unsigned long long)ctx->n_cols);
   const ebic::TrendArgs ta = make_args(approx, neg);
@@ -614,12 +684,16 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
   Slot& sl = ctx->slots[ticket % EBIC_MARSHAL_SLOTS];
   EBIC_TRY(wait_slot(ctx, sl));  // ring full: retire the oldest submission first
   const uint64_t n_idx = n_cand ? offsets[n_cand] : 0;
-  EBIC_TRY(ensure(sl.h_cols, n_idx));
-  EBIC_TRY(ensure(sl.h_offs, n_cand + 1));
-  EBIC_TRY(ensure(sl.h_counts, n_cand));
-  EBIC_TRY(ensure(sl.d_cols, n_idx));
-  EBIC_TRY(ensure(sl.d_offs, n_cand + 1));
-  EBIC_TRY(ensure(sl.d_counts, n_cand));
+  // Grow every slot of the ring together (cudaMallocHost costs milliseconds):
+  // after the first submission of a given size, no later submission allocates.
+  for (Slot& any : ctx->slots) {
+    EBIC_TRY(ensure(any.h_cols, n_idx));
+    EBIC_TRY(ensure(any.h_offs, n_cand + 1));
+    EBIC_TRY(ensure(any.h_counts, n_cand));
+    EBIC_TRY(ensure(any.d_cols, n_idx));
+    EBIC_TRY(ensure(any.d_offs, n_cand + 1));
+    EBIC_TRY(ensure(any.d_counts, n_cand));
+  }
   if (n_cand) {
     std::memcpy(sl.h_cols.p, cols, n_idx * sizeof(uint32_t));
     std::memcpy(sl.h_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t));
@@ -774,7 +848,7 @@ int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows) {
 
 int ebic_ctx_set_path(ebic_ctx* ctx, int path) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
-  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_PLANE) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
+  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_PLANE_U32) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
   ctx->path = path;
   return EBIC_OK;
 }

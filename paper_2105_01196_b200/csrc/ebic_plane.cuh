@@ -254,6 +254,63 @@ __device__ __forceinline__ void sweep_class(const SlabArgs& a, uint32_t sa_rec, 
   }
 }
 
+// Pack one chunk of the CSR population into shared-memory records
+// {u16 candidate slot, 7 x u16 columns}, sorted into length classes (counting
+// sort) and each class padded to a multiple of STRIDE with dummy records
+// (slot = chunk, all columns 0).  Zeroes the chunk's shared counts.  Invalid
+// candidates (empty, or a column >= n_cols) raise the device error flag and
+// land in class 0, which is never swept (count 0).  Called by every thread.
+template <uint32_t STRIDE>
+__device__ void pack_chunk(const SlabArgs& a, uint32_t c_begin, uint32_t c_n, uint4* s_rec, uint32_t* s_cnt,
+                           uint32_t* s_hist, uint32_t* s_base, uint32_t* s_fill) {
+  auto class_of = [&](uint32_t i, uint32_t& len, bool& bad) -> uint32_t {
+    const uint32_t b = a.offs[i], e = a.offs[i + 1];
+    len = e > b ? e - b : 0;
+    bad = len == 0;
+    for (uint32_t k = b; k < e && !bad; ++k) bad |= a.cols[k] >= a.n_cols;
+    return bad ? 0u : min(len, 8u);
+  };
+  if (threadIdx.x < kClasses) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  // pass 1: class histogram (+ validation)
+  for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
+    uint32_t len;
+    bool bad;
+    const uint32_t cl = class_of(c_begin + j, len, bad);
+    if (bad) atomicOr(a.err, 1);
+    atomicAdd(&s_hist[cl], 1u);
+    s_cnt[j] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int c = 0; c < kClasses; ++c) {
+      s_base[c] = acc;
+      s_fill[c] = 0;
+      s_hist[c] = (s_hist[c] + STRIDE - 1) / STRIDE * STRIDE;
+      acc += s_hist[c];
+    }
+    s_cnt[a.chunk] = 0;  // scratch count of the padding records
+  }
+  __syncthreads();
+  for (int c = 1; c < kClasses; ++c)
+    for (uint32_t t = threadIdx.x; t < s_hist[c]; t += blockDim.x) s_rec[s_base[c] + t] = make_uint4(a.chunk, 0u, 0u, 0u);
+  __syncthreads();
+  // pass 2: records scattered by class
+  for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
+    uint32_t len;
+    bool bad;
+    const uint32_t cl = class_of(c_begin + j, len, bad);
+    const uint32_t b = a.offs[c_begin + j];
+    uint32_t h[8] = {j, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < kRecCols; ++k)
+      if (!bad && (uint32_t)k < len) h[k + 1] = a.cols[b + k];
+    const uint32_t pos = s_base[cl] + atomicAdd(&s_fill[cl], 1u);
+    s_rec[pos] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+  }
+}
+
 template <int RPL, int SUB, bool NEG, bool MASK>
 __global__ void __launch_bounds__(kSlabThreads, 1)
 slab_count_kernel(const SlabArgs a) {
@@ -282,64 +339,16 @@ slab_count_kernel(const SlabArgs a) {
     for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x)
       if (s_cnt[j]) atomicAdd(&a.counts[c_begin + j], s_cnt[j]);
   };
-  auto class_of = [&](uint32_t i, uint32_t& len, bool& bad) -> uint32_t {
-    const uint32_t b = a.offs[i], e = a.offs[i + 1];
-    len = e > b ? e - b : 0;
-    bad = len == 0;
-    for (uint32_t k = b; k < e && !bad; ++k) bad |= a.cols[k] >= a.n_cols;
-    return bad ? 0u : min(len, 8u);
-  };
-
   for (uint64_t u = u_begin; u < u_end; ++u) {
     const uint32_t chunk = (uint32_t)(u / a.n_slabs), slab = (uint32_t)(u % a.n_slabs);
     const uint32_t row0 = slab * RT;
     __syncthreads();  // previous slab / counts fully consumed
     if (chunk != cur_chunk) {
       flush();
-      if (threadIdx.x < kClasses) s_hist[threadIdx.x] = 0;
-      __syncthreads();
       cur_chunk = chunk;
       c_begin = chunk * a.chunk;
       c_n = min(a.chunk, a.n_cand - c_begin);
-      // pass 1: class histogram (+ validation)
-      for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
-        uint32_t len;
-        bool bad;
-        const uint32_t cl = class_of(c_begin + j, len, bad);
-        if (bad) atomicOr(a.err, 1);
-        atomicAdd(&s_hist[cl], 1u);
-        s_cnt[j] = 0;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t acc = 0;
-        for (int c = 0; c < kClasses; ++c) {
-          s_base[c] = acc;
-          s_fill[c] = 0;
-          s_hist[c] = (s_hist[c] + kSlabWarps * SUB - 1) / (kSlabWarps * SUB) * (kSlabWarps * SUB);
-          acc += s_hist[c];
-        }
-        s_cnt[a.chunk] = 0;  // scratch count of the padding records
-      }
-      __syncthreads();
-      // padding records: candidate slot `chunk`, every column 0
-      for (int c = 1; c < kClasses; ++c)
-        for (uint32_t t = threadIdx.x; t < s_hist[c]; t += blockDim.x)
-          s_rec[s_base[c] + t] = make_uint4(a.chunk, 0u, 0u, 0u);
-      __syncthreads();
-      // pass 2: records {u16 candidate, 7 x u16 columns}, scattered by class
-      for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
-        uint32_t len;
-        bool bad;
-        const uint32_t cl = class_of(c_begin + j, len, bad);
-        const uint32_t b = a.offs[c_begin + j];
-        uint32_t h[8] = {j, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int k = 0; k < kRecCols; ++k)
-          if (!bad && (uint32_t)k < len) h[k + 1] = a.cols[b + k];
-        const uint32_t pos = s_base[cl] + atomicAdd(&s_fill[cl], 1u);
-        s_rec[pos] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-      }
+      pack_chunk<kSlabWarps * SUB>(a, c_begin, c_n, s_rec, s_cnt, s_hist, s_base, s_fill);
     }
     // stage the slab: rows [row0, row0+RT) of every column (RT*4 bytes contiguous per column)
     {

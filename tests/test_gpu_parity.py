@@ -10,15 +10,16 @@ from conftest import golden_cases, load_golden
 from paper_2105_01196_b200 import (EBIC_STORE_AUTO, EBIC_STORE_F32, EBIC_STORE_F64, EbicError, Population,
                                    TrendParams)
 from paper_2105_01196_b200 import synth
-from paper_2105_01196_b200._lib import EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_VALUE
+from paper_2105_01196_b200._lib import EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[EBIC_PATH_AUTO, EBIC_PATH_VALUE], ids=["plane", "value"])
+@pytest.fixture(params=[EBIC_PATH_AUTO, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE], ids=["plane", "plane_u32", "value"])
 def path_evaluator(evaluator, request):
-    """The same checks on both exact evaluation paths: the rank-plane slab kernel
-    (default for <= 8192 columns) and the float value kernel."""
+    """The same checks on every exact evaluation path: the default rank-plane
+    kernels (packed 16-bit rank pairs where the slab fits), the 32-bit-word
+    plane kernel, and the float value kernel."""
     evaluator.set_path(request.param)
     yield evaluator
     evaluator.set_path(EBIC_PATH_AUTO)
@@ -348,3 +349,23 @@ def test_plane_is_rebuilt_per_approx_and_matrix(evaluator):
         np.testing.assert_array_equal(evaluator.evaluate_population([[0, 1, 8999]]), want)
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
+
+
+@pytest.mark.parametrize("n_cols", [600, 1000, 1024, 1100, 3000, 6000])
+def test_wide_matrices_every_slab_variant(path_evaluator, n_cols):
+    """Column counts that select each slab layout: packed pairs with two
+    candidates per warp (C <= 1024), 32-bit words with 16/8-row slabs above."""
+    evaluator = path_evaluator
+    rng = np.random.default_rng(n_cols)
+    R = 1500
+    m = rng.standard_normal((R, n_cols)).astype(np.float32)
+    m[: R // 3] = np.sort(m[: R // 3], axis=1)  # long trends survive
+    m[rng.random(m.shape) < 0.01] = 0.0
+    seqs = [rng.choice(n_cols, size=int(rng.integers(1, 13)), replace=False) for _ in range(700)]
+    seqs += [np.sort(rng.choice(n_cols, size=L, replace=False)) for L in (8, 9, 20, 40)]
+    pop = Population.from_sequences(seqs)
+    evaluator.upload(m)
+    for approx, neg in ((0.03, False), (0.0, True), (0.2, True)):
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+        got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+        np.testing.assert_array_equal(got, want, err_msg=f"C={n_cols} approx={approx} neg={neg}")
