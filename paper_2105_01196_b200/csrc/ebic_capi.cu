@@ -95,6 +95,7 @@ int ensure(HostBuf<T>& b, size_t n) {
 
 struct Slot {
   HostBuf<uint32_t> h_cols, h_offs, h_counts;
+  HostBuf<int> h_err;  // device-detected argument errors of this submission
   DevBuf<uint32_t> d_cols, d_offs, d_counts;
   cudaEvent_t done = nullptr;
   uint64_t ticket = 0;   // ticket currently occupying the slot (0 = free)
@@ -232,7 +233,7 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
     // packed pairs: the largest slab (most rows per lane) that fits
     struct Opt { int p, sub; uint32_t rt; };
     // (P = 4 would need > 64 registers per thread at 1024 threads: spills)
-    const Opt opts[3] = {{2, 1, 128}, {1, 1, 64}, {1, 2, 32}};
+    const Opt opts[4] = {{2, 1, 128}, {1, 1, 64}, {1, 2, 32}, {1, 4, 16}};
     for (const Opt& o : opts) {
       if (C * o.rt * 4 <= kSlabCap) {
         c.simd = true;
@@ -349,7 +350,8 @@ int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const
     if (cfg.simd) {
       if (cfg.p == 2) return launch_simd_t<2, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
       if (cfg.sub == 1) return launch_simd_t<1, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
-      return launch_simd_t<1, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      if (cfg.sub == 2) return launch_simd_t<1, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      return launch_simd_t<1, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
     }
   }
   if constexpr (MASK) {
@@ -408,17 +410,18 @@ int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
 // chromosomes; bicluster.cpp:8-15 is the reference's validity rule, but
 // evaluate_population itself accepts duplicates and any length >= 1).
 int validate_population(const ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
-                        uint64_t n_cand) {
+                        uint64_t n_cand, bool check_cols = true) {
   if (n_cand && (!cols || !offsets)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null population pointer");
   if (n_cand && offsets[0] != 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "offsets[0] must be 0");
   for (uint64_t i = 0; i < n_cand; ++i) {
     if (offsets[i + 1] <= offsets[i])
       return fail(EBIC_ERR_INVALID_ARGUMENT, "candidate %llu is empty or offsets decrease",
                   (unsigned long long)i);
-    for (uint32_t k = offsets[i]; k < offsets[i + 1]; ++k)
-      if (cols[k] >= ctx->n_cols)
-        return fail(EBIC_ERR_INVALID_ARGUMENT, "candidate %llu: column %u out of range (cols=%llu)",
-                    (unsigned long long)i, cols[k], (unsigned long long)ctx->n_cols);
+    if (check_cols)
+      for (uint32_t k = offsets[i]; k < offsets[i + 1]; ++k)
+        if (cols[k] >= ctx->n_cols)
+          return fail(EBIC_ERR_INVALID_ARGUMENT, "candidate %llu: column %u out of range (cols=%llu)",
+                      (unsigned long long)i, cols[k], (unsigned long long)ctx->n_cols);
   }
   return EBIC_OK;
 }
@@ -511,9 +514,14 @@ int wait_slot(ebic_ctx* ctx, Slot& sl) {
   if (!sl.ticket) return EBIC_OK;
   EBIC_CUDA(cudaEventSynchronize(sl.done));
   if (sl.user_counts) std::memcpy(sl.user_counts, sl.h_counts.p, sl.n_cand * sizeof(uint32_t));
+  const int err = sl.h_err.p ? sl.h_err.p[0] : 0;
   sl.ticket = 0;
   sl.user_counts = nullptr;
   (void)ctx;
+  if (err)
+    return fail(EBIC_ERR_INVALID_ARGUMENT,
+                "a candidate has a column index out of range (cols=%llu); its count is 0",
+                (unsigned long long)ctx->n_cols);
   return EBIC_OK;
 }
 
@@ -581,6 +589,7 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
     sl.h_cols.release();
     sl.h_offs.release();
     sl.h_counts.release();
+    sl.h_err.release();
     sl.d_cols.release();
     sl.d_offs.release();
     sl.d_counts.release();
@@ -678,7 +687,9 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   if (n_cand && !counts_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null counts_out");
-  EBIC_TRY(validate_population(ctx, cols, offsets, n_cand));
+  // offsets on the host (they bound every device read); column indices are
+  // validated on device while packing and reported by ebic_eval_wait
+  EBIC_TRY(validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false));
   EBIC_TRY(set_device(ctx));
   const uint64_t ticket = ctx->next_ticket++;
   Slot& sl = ctx->slots[ticket % EBIC_MARSHAL_SLOTS];
@@ -693,6 +704,7 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
     EBIC_TRY(ensure(any.d_cols, n_idx));
     EBIC_TRY(ensure(any.d_offs, n_cand + 1));
     EBIC_TRY(ensure(any.d_counts, n_cand));
+    EBIC_TRY(ensure(any.h_err, 1));
   }
   if (n_cand) {
     std::memcpy(sl.h_cols.p, cols, n_idx * sizeof(uint32_t));
@@ -709,6 +721,10 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
                                  sl.d_counts.p, nullptr, s));
     EBIC_CUDA(cudaMemcpyAsync(sl.h_counts.p, sl.d_counts.p, n_cand * sizeof(uint32_t),
                               cudaMemcpyDeviceToHost, s));
+    EBIC_CUDA(cudaMemcpyAsync(sl.h_err.p, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
+  } else {
+    sl.h_err.p[0] = 0;
   }
   EBIC_CUDA(cudaEventRecord(sl.done, s));
   sl.ticket = ticket;

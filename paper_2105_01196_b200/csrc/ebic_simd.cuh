@@ -13,7 +13,8 @@
 //
 // Lane mapping: LPC = 32/SUB lanes per candidate, each lane owns P pair-words
 // (2P rows), so a slab holds RT = LPC * 2P rows:
-//   SUB=2, P=1: RT = 32  (C <= ~1500)  two candidates per warp instruction
+//   SUB=4, P=1: RT = 16  (C <= 2048)  four candidates per warp instruction
+//   SUB=2, P=1: RT = 32  (C <= 1024)  two candidates per warp instruction
 //   SUB=1, P=1: RT = 64  (C <= 512)
 //   SUB=1, P=2: RT = 128 (C <= 256)
 // Shared memory per column: [RT/2 words of Rg][RT/2 words of T] (== 4 B per
@@ -142,11 +143,15 @@ __device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_
       if (NEG) or_into<P>(f, r);
       ok = f;
     }
-    // count: per-lane popcount, summed per candidate with one REDUX for both
-    // half-warps (SUB=2 packs half 1's sum into the upper 16 bits)
-    const uint32_t n = popc_words<P>(ok) << (16 * sub);
+    // count: per-lane popcount, summed per candidate with ONE REDUX for all SUB
+    // candidates of the warp: candidate `sub` owns bit field [sub*FW, (sub+1)*FW)
+    // (a slab count is <= RT = 2*P*LPC rows, which fits its field)
+    constexpr uint32_t FW = 32 / SUB;
+    static_assert(SUB == 1 || (2u * P * LPC) < (1u << FW), "count field too narrow");
+    const uint32_t n = popc_words<P>(ok) << (FW * sub);
     const uint32_t tot = __reduce_add_sync(kFull, n);
-    if (lane % LPC == 0) atomicAdd(&s_cnt[j], SUB == 1 ? tot : (sub ? tot >> 16 : tot & 0xFFFFu));
+    if (lane % LPC == 0)
+      atomicAdd(&s_cnt[j], SUB == 1 ? tot : (tot >> (FW * sub)) & ((1u << (FW % 32)) - 1u));
   }
 }
 
@@ -158,7 +163,7 @@ slab_simd_kernel(const SlabArgs a) {
   constexpr uint32_t RT = LPC * 2 * P;             // rows per slab
   constexpr uint32_t CW = RT;                      // words per column: RT/2 Rg + RT/2 T
   constexpr uint32_t TOFF = RT * 2;                // bytes from a column's Rg words to its T words
-  constexpr uint32_t COLSHIFT = CW == 32 ? 7 : CW == 64 ? 8 : CW == 128 ? 9 : 10;  // log2(CW*4)
+  constexpr uint32_t COLSHIFT = CW == 16 ? 6 : CW == 32 ? 7 : CW == 64 ? 8 : CW == 128 ? 9 : 10;  // log2(CW*4)
   static_assert((1u << COLSHIFT) == CW * 4, "column stride must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][Rg(RT/2) | T(RT/2)]

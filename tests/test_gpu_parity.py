@@ -351,10 +351,11 @@ def test_plane_is_rebuilt_per_approx_and_matrix(evaluator):
         evaluator.set_path(EBIC_PATH_AUTO)
 
 
-@pytest.mark.parametrize("n_cols", [600, 1000, 1024, 1100, 3000, 6000])
+@pytest.mark.parametrize("n_cols", [600, 1000, 1024, 1100, 2048, 3000, 5000])
 def test_wide_matrices_every_slab_variant(path_evaluator, n_cols):
-    """Column counts that select each slab layout: packed pairs with two
-    candidates per warp (C <= 1024), 32-bit words with 16/8-row slabs above."""
+    """Column counts that select each slab layout: packed rank pairs with two
+    (C <= 1024) and four (C <= 2048) candidates per warp instruction, and
+    32-bit plane words with 16- and 8-row slabs above that."""
     evaluator = path_evaluator
     rng = np.random.default_rng(n_cols)
     R = 1500
