@@ -17,12 +17,13 @@
 //   SUB=2, P=1: RT = 32  (C <= 1024)  two candidates per warp instruction
 //   SUB=1, P=1: RT = 64  (C <= 512)
 //   SUB=1, P=2: RT = 128 (C <= 256)
-// Shared memory per column: [RT/2 words of Rg][RT/2 words of T] (== 4 B per
-// element, the same as the u32 plane), so the slab footprint is unchanged
-// while each lane does half the instructions per row.  (SUB=2: the two
-// half-warps read two random columns per LDS, a 2-way bank conflict half of
-// the time -- ~1.5 wavefronts per load, still half the issue slots of the
-// one-row-per-lane kernel.)
+// Shared memory: an Rg plane [C][RT/2 words] and a T plane [C][RT/2 words]
+// (== 4 B per element, the same as the u32 plane), so the slab footprint is
+// unchanged while each lane does half the instructions per row.  Separate
+// planes (rather than one [Rg|T] line per column, which would put every
+// candidate's Rg in the same banks) make the SUB candidates of one LDS collide
+// only when their columns share a bank group: ~1.5 wavefronts per load at
+// SUB=2, ~2 at SUB=4.
 #pragma once
 #include <cstdint>
 
@@ -69,8 +70,8 @@ __device__ __forceinline__ uint32_t popc_words(const V& v) {
 // additionally Rg(c0) / T(c_{L-1}) for the reversed direction.  TOFF is the
 // byte distance from a column's Rg words to its T words.  Returns the guard bits of
 // the lane's row pairs that support the candidate.
-template <int L, int P, bool NEG, uint32_t COLSHIFT, uint32_t TOFF>
-__device__ __forceinline__ typename PairVec<P>::V simd_eval(uint32_t lane_rg, const uint4& rec,
+template <int L, int P, bool NEG, uint32_t COLSHIFT>
+__device__ __forceinline__ typename PairVec<P>::V simd_eval(uint32_t lane_rg, uint32_t TOFF, const uint4& rec,
                                                           typename PairVec<P>::V vmask) {
   using V = typename PairVec<P>::V;
   const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
@@ -97,8 +98,8 @@ __device__ __forceinline__ typename PairVec<P>::V simd_eval(uint32_t lane_rg, co
   return f;
 }
 
-template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT, uint32_t TOFF>
-__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_rg,
+template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT>
+__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_rg, uint32_t TOFF,
                                                  uint32_t* s_cnt, uint32_t n_padded, uint32_t class_base,
                                                  uint32_t c_begin, typename PairVec<P>::V vmask, int warp,
                                                  int lane, int sub) {
@@ -112,7 +113,7 @@ __device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_
     if constexpr (L == 1) {
       ok = vmask;  // no pair: every row supports (the trend.cpp:19 loop never runs)
     } else if constexpr (L < 8) {
-      ok = simd_eval<L, P, NEG, COLSHIFT, TOFF>(lane_rg, rec, vmask);
+      ok = simd_eval<L, P, NEG, COLSHIFT>(lane_rg, TOFF, rec, vmask);
     } else {
       // >= 8 columns: first 7 from the record, the tail from the CSR
       const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
@@ -161,17 +162,20 @@ slab_simd_kernel(const SlabArgs a) {
   using V = typename PairVec<P>::V;
   constexpr int LPC = 32 / SUB;
   constexpr uint32_t RT = LPC * 2 * P;             // rows per slab
-  constexpr uint32_t CW = RT;                      // words per column: RT/2 Rg + RT/2 T
-  constexpr uint32_t TOFF = RT * 2;                // bytes from a column's Rg words to its T words
-  constexpr uint32_t COLSHIFT = CW == 16 ? 6 : CW == 32 ? 7 : CW == 64 ? 8 : CW == 128 ? 9 : 10;  // log2(CW*4)
-  static_assert((1u << COLSHIFT) == CW * 4, "column stride must be a power of two");
+  constexpr uint32_t CWP = RT / 2;                 // words per column per plane
+  constexpr uint32_t COLSHIFT = CWP == 8 ? 5 : CWP == 16 ? 6 : CWP == 32 ? 7 : CWP == 64 ? 8 : 9;  // log2(CWP*4)
+  static_assert((1u << COLSHIFT) == CWP * 4, "column stride must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][Rg(RT/2) | T(RT/2)]
-  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + (size_t)a.n_cols * CW);
+  // T plane offset: Rg plane size rounded so that T(c) sits 16 banks away from Rg(c)
+  const uint32_t rg_words = a.n_cols * CWP;
+  const uint32_t t_words = rg_words + ((48u - rg_words % 32u) % 32u);  // == 16 (mod 32)
+  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // Rg plane, then T plane
+  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + t_words + rg_words + 16);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rec + a.chunk + kClasses * kSlabWarps * SUB);
   __shared__ uint32_t s_hist[kClasses], s_base[kClasses], s_fill[kClasses];
   const uint32_t sa_slab = (uint32_t)__cvta_generic_to_shared(s_slab);
   const uint32_t sa_rec = (uint32_t)__cvta_generic_to_shared(s_rec);
+  const uint32_t TOFF = t_words * 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / LPC, rl = lane % LPC;
@@ -211,9 +215,8 @@ slab_simd_kernel(const SlabArgs a) {
         const uint2 rg = make_uint2(__byte_perm(w.x, w.y, 0x7632) | 0x80008000u,
                                     __byte_perm(w.z, w.w, 0x7632) | 0x80008000u);
         const uint2 tt = make_uint2(__byte_perm(w.x, w.y, 0x5410), __byte_perm(w.z, w.w, 0x5410));
-        uint32_t* col = s_slab + (size_t)c * CW;
-        *reinterpret_cast<uint2*>(col + 2 * q) = rg;
-        *reinterpret_cast<uint2*>(col + RT / 2 + 2 * q) = tt;
+        *reinterpret_cast<uint2*>(s_slab + c * CWP + 2 * q) = rg;
+        *reinterpret_cast<uint2*>(s_slab + t_words + c * CWP + 2 * q) = tt;
       }
     }
     __syncthreads();
@@ -228,8 +231,8 @@ slab_simd_kernel(const SlabArgs a) {
     }
 
 #define EBIC_SIMD_SWEEP(L)                                                                                  \
-  simd_sweep_class<P, SUB, NEG, L, COLSHIFT, TOFF>(a, sa_rec, lane_rg, s_cnt, s_hist[L], s_base[L], c_begin, \
-                                                   vmask, warp, lane, sub)
+  simd_sweep_class<P, SUB, NEG, L, COLSHIFT>(a, sa_rec, lane_rg, TOFF, s_cnt, s_hist[L], s_base[L], c_begin, \
+                                             vmask, warp, lane, sub)
     EBIC_SIMD_SWEEP(4);
     EBIC_SIMD_SWEEP(3);
     EBIC_SIMD_SWEEP(5);
