@@ -253,6 +253,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     from paper_2105_01196_b200 import Evaluator, TrendParams
     from paper_2105_01196_b200.shard import ShardedEvaluator, row_range
 
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)  # gloo test mode: ranks may share a GPU
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     tp = TrendParams(approx=cfg["approx"], negative_trends=cfg["negative"])
@@ -445,6 +446,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--shard", choices=["rows", "pop"], default="rows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collective backend for N > 1 (gloo lets N ranks share one GPU to test the sharded path)")
     ap.add_argument("--path", choices=["auto", "value", "plane"], default="auto",
                     help="evaluation kernel: rank-plane slab kernel (auto for <= 8192 cols) or float value kernel")
     args = ap.parse_args()
@@ -462,8 +465,13 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        n_dev = torch.cuda.device_count()
+        dev_idx = local_rank % max(n_dev, 1)
+        torch.cuda.set_device(dev_idx)
+        if args.backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            tdist.init_process_group("gloo")
         dist = tdist
     try:
         return bench_ours(args, cfg, rank, world, local_rank, dist)

@@ -1,5 +1,6 @@
 #!/bin/bash
-# One gpurun call: GPU tests, smoke, bench, ncu launch list + one full capture.
+# Round-level GPU call: tests, smoke, bench (+reference arm), 2-rank gloo run of the
+# sharded bench path, ncu launch list and one full capture of the hot kernel per config.
 # usage (from the repo root, on the GPU box): bash scripts/gpu_check.sh [tag]
 set -u
 TAG=${1:-r1}
@@ -11,10 +12,17 @@ timeout 1500 python -m pytest tests -q -m gpu -rs > $OUT/pytest_gpu_$TAG.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke exit $?" >> $OUT/smoke_$TAG.log
 timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
+for sh in rows pop; do
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 \
+      bench.py --gpus 2 --steps 5 --warmup 3 --backend gloo --shard $sh > $OUT/bench_gloo2_${sh}_$TAG.json 2> $OUT/bench_gloo2_${sh}_$TAG.err
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c3_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slab_count|fitness_count" -s 5 -c 1 \
-    -o $OUT/prof_c3_$TAG -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1
+for c in c3 c2 c4 c5; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slab_" -s 5 -c 1 \
+      -o $OUT/prof_${c}_$TAG -f python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_${c}_$TAG.log 2>&1
+done
+for c in c2 c4 c5; do
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_${c}_$TAG.json 2> $OUT/bench_${c}_$TAG.err
+done
 echo done
-timeout 600 python bench.py --steps 10 --warmup 3 --path value --no-cpu-baseline > $OUT/bench_value_$TAG.json 2> $OUT/bench_value_$TAG.err
-for c in c2 c4 c5; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_${c}_$TAG.json 2> $OUT/bench_${c}_$TAG.err; done
