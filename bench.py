@@ -92,59 +92,82 @@ def ncu_traffic(config: str, world: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled DURING the timed region.
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML (nvidia-ml-py) polled every ~1 ms from a thread -- the timed region is
+    only tens of milliseconds, too short for `nvidia-smi -lms`; nvidia-smi is
+    the fallback when NVML is unavailable.
+    """
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    HW_SLOWDOWN, SW_POWER_CAP, SW_THERMAL, HW_THERMAL = 0x8, 0x4, 0x20, 0x40
+
+    def __init__(self, torch_device_index: int):
+        self.dev_index = torch_device_index
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._handle = None
+        self._nvml = None
+
+    def _open(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        self._nvml = pynvml
+        handle = None
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(self.dev_index).uuid)
+            handle = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            cvd = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+            idx = cvd[self.dev_index] if self.dev_index < len(cvd) else str(self.dev_index)
+            handle = (pynvml.nvmlDeviceGetHandleByUUID(idx) if idx.startswith("GPU-")
+                      else pynvml.nvmlDeviceGetHandleByIndex(int(idx)))
+        self._handle = handle
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(handle, pynvml.NVML_CLOCK_SM)
+
+    def _reasons(self):
+        f = getattr(self._nvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            self._nvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        return f(self._handle)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((self._nvml.nvmlDeviceGetClockInfo(self._handle, self._nvml.NVML_CLOCK_SM),
+                                     self._reasons()))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self._open()
+            self._stop.clear()
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self._handle = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._handle is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        rows = []
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                rows.append(dict(sm=float(f[1]), smax=float(f[2]), hw=f[5], hwt=f[6], swt=f[7], pcap=f[8]))
-            except ValueError:
-                continue
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        reasons = []
-        for key, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
-                          ("pcap", "sw_power_cap")):
-            if any(r[key].lower() == "active" for r in rows):
-                reasons.append(name)
-        return {"sm_mhz": statistics.median(r["sm"] for r in rows), "sm_max_mhz": max(r["smax"] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        mask = 0
+        for _, r in self.samples:
+            mask |= int(r)
+        reasons = [name for bit, name in ((self.HW_SLOWDOWN, "hw_slowdown"), (self.HW_THERMAL, "hw_thermal_slowdown"),
+                                          (self.SW_THERMAL, "sw_thermal_slowdown"), (self.SW_POWER_CAP, "sw_power_cap"))
+                   if mask & bit]
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, ~1 ms polling"}
 
 
 def make_inputs(cfg, n_pops: int):
@@ -187,19 +210,34 @@ CUR_APPROX = [0.03]
 CUR_NEG = [False]
 
 
-def cpu_sample(run, pop, budget_s: float):
-    """Evaluate a prefix of `pop` sized to ~budget_s seconds; returns (n, seconds, counts)."""
+def cpu_sample(run, pops, budget_s: float, cap=None):
+    """Evaluate whole populations (then a prefix of the next one) until ~budget_s
+    seconds of CPU work; returns (n_candidates, seconds, counts of pops[0] prefix)."""
     from paper_2105_01196_b200.shard import slice_population
 
-    n = min(len(pop), 32)
+    if not isinstance(pops, (list, tuple)):
+        pops = [pops]
+    probe_n = min(len(pops[0]), 64)
     t0 = time.perf_counter()
-    run(slice_population(pop, 0, n))
-    probe = time.perf_counter() - t0
-    n = int(max(1, min(len(pop), n * budget_s / max(probe, 1e-6))))
-    sub = slice_population(pop, 0, n)
-    t0 = time.perf_counter()
-    counts = run(sub)
-    return n, time.perf_counter() - t0, counts
+    run(slice_population(pops[0], 0, probe_n))
+    per_cand = max((time.perf_counter() - t0) / probe_n, 1e-9)
+    want = int(max(1, budget_s / per_cand))
+    if cap:
+        want = min(want, cap)
+    n_done, secs, first = 0, 0.0, None
+    i = 0
+    while n_done < want:
+        pop = pops[i % len(pops)]
+        take = min(len(pop), want - n_done)
+        sub = slice_population(pop, 0, take)
+        t0 = time.perf_counter()
+        out = run(sub)
+        secs += time.perf_counter() - t0
+        if first is None:
+            first = out
+        n_done += take
+        i += 1
+    return n_done, secs, first
 
 
 def bench_reference(args, cfg, rank):
@@ -211,20 +249,13 @@ def bench_reference(args, cfg, rank):
     pop = pops[0]
     per_step = float(os.environ.get("EBIC_REF_STEP_S", "3.0"))
     for _ in range(args.warmup):
-        cpu_sample(run, pop, min(per_step, 1.0))
+        cpu_sample(run, pop, min(per_step, 1.0), cap=len(pop))
     tot_n, tot_t = 0, 0.0
     n_step = None
     for _ in range(args.steps):
-        if n_step is None:
-            n_step, t, _ = cpu_sample(run, pop, per_step)
-        else:
-            from paper_2105_01196_b200.shard import slice_population
-
-            sub = slice_population(pop, 0, n_step)
-            t0 = time.perf_counter()
-            run(sub)
-            t = time.perf_counter() - t0
-        tot_n += n_step
+        n, t, _ = cpu_sample(run, pop, per_step, cap=len(pop) if n_step is None else n_step)
+        n_step = n
+        tot_n += n
         tot_t += t
     value = tot_n / tot_t
     line = {
@@ -316,8 +347,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = ev.launch_count()
-    cvd = [x for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
-    clocks = ClockSampler(cvd[local_rank] if local_rank < len(cvd) else str(local_rank))
+    clocks = ClockSampler(local_rank)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -421,14 +451,14 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     if with_cpu:
         CUR_APPROX[0], CUR_NEG[0] = cfg["approx"], cfg["negative"]
         run, kind, cores = cpu_eval_setup(m)
-        n, t, cpu_counts = cpu_sample(run, pops[0], float(os.environ.get("EBIC_CPU_BUDGET_S", "12")))
-        gpu_counts = host_counts if len(pops) == 1 else call(pops[0], tp)
+        n, t, cpu_counts = cpu_sample(run, pops, float(os.environ.get("EBIC_CPU_BUDGET_S", "12")))
+        gpu_counts = call(pops[0], tp)
         line["cpu_baseline"] = {
             "value": n / t, "unit": "evals/s", "cores": cores, "kind": kind,
-            "sample": f"first {n} of {P} candidates of population 0 x all {R} rows, {t:.1f} s "
+            "sample": f"{n} candidates (whole {P}-candidate populations, cycled) x all {R} rows, {t:.1f} s "
                       + ("(unmodified reference evaluate_population on WorkerPool)" if kind == "reference"
                          else "(C restatement of trend.cpp, pthreads)"),
-            "parity_with_gpu": bool(np.array_equal(cpu_counts, gpu_counts[:n])),
+            "parity_with_gpu": bool(np.array_equal(cpu_counts, gpu_counts[:len(cpu_counts)])),
         }
     line["clocks"] = clocks.summary()
     if rank == 0:
