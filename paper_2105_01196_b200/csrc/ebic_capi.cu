@@ -246,7 +246,7 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
     }
   }
   if (found) {
-    const size_t slab = C * c.rt * 4 + 256;  // + T-plane bank alignment pad
+    const size_t slab = C * c.rt * 4;
     const size_t fixed = slab + (size_t)ebic::kClasses * ebic::kSlabWarps * c.sub * 16 + 16;
     const uint64_t cmax = std::min<uint64_t>((budget - fixed) / 20, 16384);
     const uint64_t n_chunks = (n_cand + cmax - 1) / cmax;

@@ -1,15 +1,15 @@
 // ebic_simd.cuh -- two rows per 32-bit word: the packed-rank slab kernel.
 //
 // Same rank-plane test as slab_count_kernel (R(y) > T(x) <=> v_y > thr(v_x),
-// see ebic_plane.cuh), but the slab is restaged as two 16-bit planes:
-//   Rg[c][i] = (R(2i)   | 0x8000) | (R(2i+1) | 0x8000) << 16   ("guarded" ranks)
-//   T [c][i] =  T(2i)             |  T(2i+1)           << 16
-// so one 32-bit word holds a row PAIR.  For a consecutive pair (p, c) of a
-// candidate, D = Rg[c] - T[p] - 0x00010001 has bit 15 set iff R_lo(c) > T_lo(p)
-// and bit 31 set iff R_hi(c) > T_hi(p): the guard bit absorbs the borrow, so
-// the halves never interact (R, T <= C <= 8192 < 2^15).  One IADD3 tests two
-// rows; AND-ing the D's of all pairs (LOP3, 3 inputs) and keeping bits 15/31
-// gives the forward verdict of both rows.  Reversed uses Rg[p] - T[c].
+// see ebic_plane.cuh), but each slab column is restaged as one line of
+// 16-bit row PAIRS:
+//   Rg[i] = (R(2i) | 0x8000) | (R(2i+1) | 0x8000) << 16        ("guarded" ranks)
+//   NT[i] = 0 - (T(2i) | T(2i+1) << 16) - 0x00010001            (negated thresholds)
+// For a consecutive pair (p, c) of a candidate, D = Rg[c] + NT[p] (mod 2^32)
+// = Rg - T - 0x00010001 has bit 15 set iff R_lo(c) > T_lo(p) and bit 31 set
+// iff R_hi(c) > T_hi(p): the guard bit absorbs the borrow, so the halves never
+// interact (R, T <= C <= 8192 < 2^15).  One IADD tests two rows; AND-ing the
+// D's of all pairs and keeping bits 15/31 gives the verdict of both rows.
 //
 // Lane mapping: LPC = 32/SUB lanes per candidate, each lane owns P pair-words
 // (2P rows), so a slab holds RT = LPC * 2P rows:
@@ -17,13 +17,18 @@
 //   SUB=2, P=1: RT = 32  (C <= 1024)  two candidates per warp instruction
 //   SUB=1, P=1: RT = 64  (C <= 512)
 //   SUB=1, P=2: RT = 128 (C <= 256)
-// Shared memory: an Rg plane [C][RT/2 words] and a T plane [C][RT/2 words]
-// (== 4 B per element, the same as the u32 plane), so the slab footprint is
-// unchanged while each lane does half the instructions per row.  Separate
-// planes (rather than one [Rg|T] line per column, which would put every
-// candidate's Rg in the same banks) make the SUB candidates of one LDS collide
-// only when their columns share a bank group: ~1.5 wavefronts per load at
-// SUB=2, ~2 at SUB=4.
+// Shared memory: one line per column, [RT/2 words Rg | RT/2 words NT] (4 B per
+// element, the same footprint as the u32 plane) while each lane does half the
+// instructions per row.
+//
+// Bank conflicts with several candidates per instruction: at SUB=2 a line is
+// 128 B, Rg in banks 0-15 and NT in banks 16-31 for EVERY column.  Because
+// D = Rg + NT is commutative, even sub-groups load (NT, Rg) and odd sub-groups
+// load (Rg, NT) for each column -- via per-lane base offsets, not branches --
+// and odd sub-groups get their candidate record with the columns REVERSED, so
+// the identical instruction sequence computes the same set of pair tests for
+// both.  Every LDS then has one half-warp in banks 0-15 and the other in 16-31:
+// conflict-free for any columns (at SUB=4 the same trick halves the conflicts).
 #pragma once
 #include <cstdint>
 
@@ -66,43 +71,50 @@ __device__ __forceinline__ uint32_t popc_words(const V& v) {
   return n;
 }
 
-// Fixed-length body.  Loads T(c0), Rg(c1), T(c1), ..., Rg(c_{L-1}) (forward) and
-// additionally Rg(c0) / T(c_{L-1}) for the reversed direction.  TOFF is the
-// byte distance from a column's Rg words to its T words.  Returns the guard bits of
-// the lane's row pairs that support the candidate.
+// D = Rg + NT (two rows at once); keep the guard bits 15/31
+__device__ __forceinline__ uint32_t sum2(uint32_t a, uint32_t b) { return (a + b) & 0x80008000u; }
+
+template <int P, typename V>
+__device__ __forceinline__ void and_sum(V& acc, const V& x, const V& y) {
+#pragma unroll
+  for (int q = 0; q < P; ++q) wref(acc, q) &= sum2(wget(x, q), wget(y, q));
+}
+
+// Fixed-length body.  w1[k] / w2[k] are the two words of column rec[k] in this
+// sub-group's load order (even: NT then Rg; odd: Rg then NT, with the record
+// reversed).  Forward pair j is w1[j] + w2[j+1], reversed pair j is
+// w2[j] + w1[j+1] -- for both sub-groups.  Returns the guard bits of the lane's
+// row pairs that support the candidate.
 template <int L, int P, bool NEG, uint32_t COLSHIFT>
-__device__ __forceinline__ typename PairVec<P>::V simd_eval(uint32_t lane_rg, uint32_t TOFF, const uint4& rec,
+__device__ __forceinline__ typename PairVec<P>::V simd_eval(uint32_t base1, uint32_t base2, const uint4& rec,
                                                           typename PairVec<P>::V vmask) {
   using V = typename PairVec<P>::V;
   const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
                                  hi16(rec.z), lo16(rec.w), hi16(rec.w)};
-  uint32_t addr[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) addr[k] = lane_rg + (cc[k] << COLSHIFT);
-  V rg[L], t[L];
+  V w1[L], w2[L];
 #pragma unroll
   for (int k = 0; k < L; ++k) {
-    const bool need_rg = NEG || k > 0, need_t = NEG || k + 1 < L;
-    if (need_rg) rg[k] = lds<V>(addr[k]);
-    if (need_t) t[k] = lds<V>(addr[k] + TOFF);
+    const uint32_t off = cc[k] << COLSHIFT;
+    if (NEG || k + 1 < L) w1[k] = lds<V>(base1 + off);
+    if (NEG || k > 0) w2[k] = lds<V>(base2 + off);
   }
   V f = vmask;
 #pragma unroll
-  for (int k = 1; k < L; ++k) and_gt<P>(f, rg[k], t[k - 1]);
+  for (int k = 1; k < L; ++k) and_sum<P>(f, w1[k - 1], w2[k]);
   if constexpr (NEG) {
     V r = vmask;
 #pragma unroll
-    for (int k = 1; k < L; ++k) and_gt<P>(r, rg[k - 1], t[k]);
+    for (int k = 1; k < L; ++k) and_sum<P>(r, w2[k - 1], w1[k]);
     or_into<P>(f, r);
   }
   return f;
 }
 
-template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT>
-__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_rg, uint32_t TOFF,
-                                                 uint32_t* s_cnt, uint32_t n_padded, uint32_t class_base,
-                                                 uint32_t c_begin, typename PairVec<P>::V vmask, int warp,
-                                                 int lane, int sub) {
+template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT, uint32_t NTOFF>
+__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_line,
+                                                 uint32_t base1, uint32_t base2, uint32_t* s_cnt,
+                                                 uint32_t n_padded, uint32_t class_base, uint32_t c_begin,
+                                                 typename PairVec<P>::V vmask, int warp, int lane, int sub) {
   using V = typename PairVec<P>::V;
   constexpr int LPC = 32 / SUB;
   constexpr uint32_t stride = kSlabWarps * SUB;
@@ -113,21 +125,22 @@ __device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_
     if constexpr (L == 1) {
       ok = vmask;  // no pair: every row supports (the trend.cpp:19 loop never runs)
     } else if constexpr (L < 8) {
-      ok = simd_eval<L, P, NEG, COLSHIFT>(lane_rg, TOFF, rec, vmask);
+      ok = simd_eval<L, P, NEG, COLSHIFT>(base1, base2, rec, vmask);
     } else {
-      // >= 8 columns: first 7 from the record, the tail from the CSR
+      // >= 8 columns (record not reversed): first 7 from the record, the tail
+      // from the CSR; fixed Rg/NT offsets (bank conflicts accepted on this rare path)
       const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
                                      hi16(rec.z), lo16(rec.w), hi16(rec.w)};
       V f = vmask, r = NEG ? vmask : V{};
-      uint32_t ap = lane_rg + (cc[0] << COLSHIFT);
-      V rgp = NEG ? lds<V>(ap) : V{}, tp = lds<V>(ap + TOFF);
+      const uint32_t ap = lane_line + (cc[0] << COLSHIFT);
+      V rgp = NEG ? lds<V>(ap) : V{}, ntp = lds<V>(ap + NTOFF);
       auto step = [&](uint32_t col) {
-        const uint32_t ac = lane_rg + (col << COLSHIFT);
-        const V rgc = lds<V>(ac), tc = lds<V>(ac + TOFF);
-        and_gt<P>(f, rgc, tp);
-        if (NEG) and_gt<P>(r, rgp, tc);
+        const uint32_t ac = lane_line + (col << COLSHIFT);
+        const V rgc = lds<V>(ac), ntc = lds<V>(ac + NTOFF);
+        and_sum<P>(f, rgc, ntp);
+        if (NEG) and_sum<P>(r, rgp, ntc);
         rgp = rgc;
-        tp = tc;
+        ntp = ntc;
       };
 #pragma unroll
       for (int k = 1; k < kRecCols; ++k) step(cc[k]);
@@ -162,24 +175,24 @@ slab_simd_kernel(const SlabArgs a) {
   using V = typename PairVec<P>::V;
   constexpr int LPC = 32 / SUB;
   constexpr uint32_t RT = LPC * 2 * P;             // rows per slab
-  constexpr uint32_t CWP = RT / 2;                 // words per column per plane
-  constexpr uint32_t COLSHIFT = CWP == 8 ? 5 : CWP == 16 ? 6 : CWP == 32 ? 7 : CWP == 64 ? 8 : 9;  // log2(CWP*4)
-  static_assert((1u << COLSHIFT) == CWP * 4, "column stride must be a power of two");
+  constexpr uint32_t CW = RT;                      // words per column line: RT/2 Rg + RT/2 NT
+  constexpr uint32_t NTOFF = RT * 2;                // bytes from a line's Rg words to its NT words
+  constexpr uint32_t COLSHIFT = CW == 16 ? 6 : CW == 32 ? 7 : CW == 64 ? 8 : CW == 128 ? 9 : 10;  // log2(CW*4)
+  static_assert((1u << COLSHIFT) == CW * 4, "column stride must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // T plane offset: Rg plane size rounded so that T(c) sits 16 banks away from Rg(c)
-  const uint32_t rg_words = a.n_cols * CWP;
-  const uint32_t t_words = rg_words + ((48u - rg_words % 32u) % 32u);  // == 16 (mod 32)
-  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // Rg plane, then T plane
-  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + t_words + rg_words + 16);
+  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][Rg | NT]
+  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + (size_t)a.n_cols * CW);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rec + a.chunk + kClasses * kSlabWarps * SUB);
   __shared__ uint32_t s_hist[kClasses], s_base[kClasses], s_fill[kClasses];
   const uint32_t sa_slab = (uint32_t)__cvta_generic_to_shared(s_slab);
   const uint32_t sa_rec = (uint32_t)__cvta_generic_to_shared(s_rec);
-  const uint32_t TOFF = t_words * 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / LPC, rl = lane % LPC;
-  const uint32_t lane_rg = sa_slab + rl * P * 4;
+  const uint32_t lane_line = sa_slab + rl * P * 4;  // this lane's Rg words in column 0
+  // per-lane load order: even sub-groups (NT, Rg), odd sub-groups (Rg, NT)
+  const uint32_t base1 = lane_line + ((sub & 1) ? 0u : NTOFF);
+  const uint32_t base2 = lane_line + ((sub & 1) ? NTOFF : 0u);
   const uint64_t U = (uint64_t)a.n_chunks * a.n_slabs;
   const uint64_t u_begin = blockIdx.x * U / gridDim.x, u_end = (blockIdx.x + 1) * U / gridDim.x;
   uint32_t cur_chunk = 0xffffffffu, c_begin = 0, c_n = 0;
@@ -199,7 +212,7 @@ slab_simd_kernel(const SlabArgs a) {
       cur_chunk = chunk;
       c_begin = chunk * a.chunk;
       c_n = min(a.chunk, a.n_cand - c_begin);
-      pack_chunk<kSlabWarps * SUB>(a, c_begin, c_n, s_rec, s_cnt, s_hist, s_base, s_fill);
+      pack_chunk<kSlabWarps * SUB, SUB>(a, c_begin, c_n, s_rec, s_cnt, s_hist, s_base, s_fill);
     }
     // stage + repack: each thread takes 4 consecutive rows (one uint4 of plane
     // words) of one column and writes 2 pair-words to each 16-bit half-plane
@@ -214,9 +227,10 @@ slab_simd_kernel(const SlabArgs a) {
         const uint4 w = __ldg(src + c * ld4 + r4 + q);
         const uint2 rg = make_uint2(__byte_perm(w.x, w.y, 0x7632) | 0x80008000u,
                                     __byte_perm(w.z, w.w, 0x7632) | 0x80008000u);
-        const uint2 tt = make_uint2(__byte_perm(w.x, w.y, 0x5410), __byte_perm(w.z, w.w, 0x5410));
-        *reinterpret_cast<uint2*>(s_slab + c * CWP + 2 * q) = rg;
-        *reinterpret_cast<uint2*>(s_slab + t_words + c * CWP + 2 * q) = tt;
+        const uint2 nt = make_uint2(0u - __byte_perm(w.x, w.y, 0x5410) - 0x00010001u,
+                                    0u - __byte_perm(w.z, w.w, 0x5410) - 0x00010001u);
+        *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + 2 * q) = rg;
+        *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + RT / 2 + 2 * q) = nt;
       }
     }
     __syncthreads();
@@ -231,8 +245,8 @@ slab_simd_kernel(const SlabArgs a) {
     }
 
 #define EBIC_SIMD_SWEEP(L)                                                                                  \
-  simd_sweep_class<P, SUB, NEG, L, COLSHIFT>(a, sa_rec, lane_rg, TOFF, s_cnt, s_hist[L], s_base[L], c_begin, \
-                                             vmask, warp, lane, sub)
+  simd_sweep_class<P, SUB, NEG, L, COLSHIFT, NTOFF>(a, sa_rec, lane_line, base1, base2, s_cnt, s_hist[L], \
+                                                    s_base[L], c_begin, vmask, warp, lane, sub)
     EBIC_SIMD_SWEEP(4);
     EBIC_SIMD_SWEEP(3);
     EBIC_SIMD_SWEEP(5);
