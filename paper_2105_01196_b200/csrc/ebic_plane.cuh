@@ -254,6 +254,19 @@ __device__ __forceinline__ void sweep_class(const SlabArgs& a, uint32_t sa_rec, 
   }
 }
 
+// Warm L2 with the plane rows of the CTA's NEXT work unit while the current one
+// is swept (matters when the plane does not fit in L2, e.g. 200k x 2000).
+template <uint32_t RT>
+__device__ __forceinline__ void prefetch_next_slab(const SlabArgs& a, uint64_t u_next, uint64_t u_end) {
+  if (u_next >= u_end) return;
+  const uint32_t row0 = (uint32_t)(u_next % a.n_slabs) * RT;
+  constexpr uint32_t LINES = (RT * 4 + 127) / 128;
+  for (uint32_t t = threadIdx.x; t < a.n_cols * LINES; t += blockDim.x) {
+    const uint32_t c = t / LINES, l = t % LINES;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.plane + (uint64_t)c * a.ld + row0 + l * 32));
+  }
+}
+
 // Pack one chunk of the CSR population into shared-memory records
 // {u16 candidate slot, 7 x u16 columns}, sorted into length classes (counting
 // sort) and each class padded to a multiple of STRIDE with dummy records
@@ -368,6 +381,7 @@ slab_count_kernel(const SlabArgs a) {
       }
     }
     __syncthreads();
+    prefetch_next_slab<RT>(a, u + 1, u_end);
 
     const uint32_t valid_rows = min(RT, a.n_rows - row0);
     uint32_t vmask = 0;  // validity bits of this lane's RPL rows

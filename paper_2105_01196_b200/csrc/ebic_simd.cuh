@@ -234,6 +234,7 @@ slab_simd_kernel(const SlabArgs a) {
       }
     }
     __syncthreads();
+    prefetch_next_slab<RT>(a, u + 1, u_end);
 
     // validity guard bits of this lane's row pairs (rows beyond n_rows never count)
     const uint32_t valid_rows = min(RT, a.n_rows - row0);
