@@ -131,6 +131,7 @@ struct ebic_ctx {
   int path = EBIC_PATH_AUTO;
   int n_sms = 148;
   size_t smem_optin = 227 * 1024;
+  int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
 };
 
 namespace {
@@ -301,6 +302,10 @@ ebic::SlabArgs make_slab_args(const ebic_ctx* ctx, const SlabCfg& cfg, const uin
   a.mask = d_mask;
   a.mask_wpc = ctx->ld / 32;
   a.err = ctx->d_err;
+  // L2 prefetch of the next slab: EBIC_PREFETCH=0/1 forces it, default on when
+  // the plane is larger than ~half of L2 (126 MB on B200)
+  const uint64_t plane_bytes = ctx->ld * ctx->n_cols * 4;
+  a.prefetch = ctx->prefetch >= 0 ? ctx->prefetch : (plane_bytes > (64ull << 20) ? 1 : 0);
   return a;
 }
 
@@ -576,6 +581,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
       ctx->smem_optin = (size_t)v;
     const char* e = std::getenv("EBIC_PATH");
     if (e) ctx->path = std::atoi(e);
+    const char* pf = std::getenv("EBIC_PREFETCH");
+    if (pf) ctx->prefetch = std::atoi(pf) ? 1 : 0;
   }
   *ctx_out = ctx;
   return EBIC_OK;

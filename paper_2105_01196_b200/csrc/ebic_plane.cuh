@@ -136,6 +136,7 @@ struct SlabArgs {
   uint32_t* mask;         // MASK: [cand][ld/32] words
   uint64_t mask_wpc;
   int* err;
+  int prefetch;           // warm L2 with the next unit's slab (plane larger than L2)
 };
 
 // One consecutive-pair test on RPL rows: forward needs c > thr(p), reversed p > thr(c).
@@ -258,7 +259,7 @@ __device__ __forceinline__ void sweep_class(const SlabArgs& a, uint32_t sa_rec, 
 // is swept (matters when the plane does not fit in L2, e.g. 200k x 2000).
 template <uint32_t RT>
 __device__ __forceinline__ void prefetch_next_slab(const SlabArgs& a, uint64_t u_next, uint64_t u_end) {
-  if (u_next >= u_end) return;
+  if (!a.prefetch || u_next >= u_end) return;
   const uint32_t row0 = (uint32_t)(u_next % a.n_slabs) * RT;
   constexpr uint32_t LINES = (RT * 4 + 127) / 128;
   for (uint32_t t = threadIdx.x; t < a.n_cols * LINES; t += blockDim.x) {
