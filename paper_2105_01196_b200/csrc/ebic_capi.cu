@@ -302,10 +302,13 @@ ebic::SlabArgs make_slab_args(const ebic_ctx* ctx, const SlabCfg& cfg, const uin
   a.mask = d_mask;
   a.mask_wpc = ctx->ld / 32;
   a.err = ctx->d_err;
-  // L2 prefetch of the next slab: EBIC_PREFETCH=0/1 forces it, default on when
-  // the plane is larger than ~half of L2 (126 MB on B200)
+  // L2 prefetch of the next slab (EBIC_PREFETCH=0/1 forces it).  Measured on
+  // B200 (profiles/r1_ab_prefetch.txt): +4% when the plane is L2-resident
+  // (20k x 1000, 80 MB), -5% when it streams from HBM (200k x 2000, 1.6 GB,
+  // where the extra requests compete with other chunks' reuse of the same
+  // slabs).  Default: on iff the plane fits comfortably in the 126 MB L2.
   const uint64_t plane_bytes = ctx->ld * ctx->n_cols * 4;
-  a.prefetch = ctx->prefetch >= 0 ? ctx->prefetch : (plane_bytes > (64ull << 20) ? 1 : 0);
+  a.prefetch = ctx->prefetch >= 0 ? ctx->prefetch : (plane_bytes <= (96ull << 20) ? 1 : 0);
   return a;
 }
 

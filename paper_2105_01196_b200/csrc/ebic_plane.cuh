@@ -256,7 +256,7 @@ __device__ __forceinline__ void sweep_class(const SlabArgs& a, uint32_t sa_rec, 
 }
 
 // Warm L2 with the plane rows of the CTA's NEXT work unit while the current one
-// is swept (matters when the plane does not fit in L2, e.g. 200k x 2000).
+// is swept (host policy in make_slab_args: only for L2-resident planes).
 template <uint32_t RT>
 __device__ __forceinline__ void prefetch_next_slab(const SlabArgs& a, uint64_t u_next, uint64_t u_end) {
   if (!a.prefetch || u_next >= u_end) return;
