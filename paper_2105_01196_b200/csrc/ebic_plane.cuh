@@ -371,14 +371,23 @@ slab_count_kernel(const SlabArgs a) {
     // stage the slab: rows [row0, row0+RT) of every column (RT*4 bytes contiguous per column)
     {
       constexpr uint32_t V4 = RT / 4;  // uint4 per column
+      constexpr int UNR = 4;           // all loads of a round in flight before any store
       const uint32_t total = a.n_cols * V4;
       const uint4* src = reinterpret_cast<const uint4*>(a.plane);
       uint4* dst = reinterpret_cast<uint4*>(s_slab);
       const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
-#pragma unroll 4
-      for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint32_t c = t / V4, q = t % V4;
-        dst[t] = __ldg(src + c * ld4 + r4 + q);
+      for (uint32_t t0 = threadIdx.x; t0 < total; t0 += UNR * blockDim.x) {
+        uint4 w[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const uint32_t t = t0 + k * blockDim.x;
+          if (t < total) w[k] = __ldg(src + (uint64_t)(t / V4) * ld4 + r4 + t % V4);
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const uint32_t t = t0 + k * blockDim.x;
+          if (t < total) dst[t] = w[k];
+        }
       }
     }
     __syncthreads();

@@ -218,19 +218,30 @@ slab_simd_kernel(const SlabArgs a) {
     // words) of one column and writes 2 pair-words to each 16-bit half-plane
     {
       constexpr uint32_t Q = RT / 4;  // uint4 per column
+      constexpr int UNR = 4;          // all loads of a round in flight before any use
       const uint32_t total = a.n_cols * Q;
       const uint4* src = reinterpret_cast<const uint4*>(a.plane);
       const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
-#pragma unroll 4
-      for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint32_t c = t / Q, q = t % Q;
-        const uint4 w = __ldg(src + c * ld4 + r4 + q);
-        const uint2 rg = make_uint2(__byte_perm(w.x, w.y, 0x7632) | 0x80008000u,
-                                    __byte_perm(w.z, w.w, 0x7632) | 0x80008000u);
-        const uint2 nt = make_uint2(0u - __byte_perm(w.x, w.y, 0x5410) - 0x00010001u,
-                                    0u - __byte_perm(w.z, w.w, 0x5410) - 0x00010001u);
-        *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + 2 * q) = rg;
-        *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + RT / 2 + 2 * q) = nt;
+      for (uint32_t t0 = threadIdx.x; t0 < total; t0 += UNR * blockDim.x) {
+        uint4 w[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const uint32_t t = t0 + k * blockDim.x;
+          if (t < total) w[k] = __ldg(src + (uint64_t)(t / Q) * ld4 + r4 + t % Q);
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const uint32_t t = t0 + k * blockDim.x;
+          if (t < total) {
+            const uint32_t c = t / Q, q = t % Q;
+            const uint2 rg = make_uint2(__byte_perm(w[k].x, w[k].y, 0x7632) | 0x80008000u,
+                                        __byte_perm(w[k].z, w[k].w, 0x7632) | 0x80008000u);
+            const uint2 nt = make_uint2(0u - __byte_perm(w[k].x, w[k].y, 0x5410) - 0x00010001u,
+                                        0u - __byte_perm(w[k].z, w[k].w, 0x5410) - 0x00010001u);
+            *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + 2 * q) = rg;
+            *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + RT / 2 + 2 * q) = nt;
+          }
+        }
       }
     }
     __syncthreads();
