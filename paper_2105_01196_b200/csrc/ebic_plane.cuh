@@ -274,7 +274,7 @@ __device__ __forceinline__ void prefetch_next_slab(const SlabArgs& a, uint64_t u
 // (slot = chunk, all columns 0).  Zeroes the chunk's shared counts.  Invalid
 // candidates (empty, or a column >= n_cols) raise the device error flag and
 // land in class 0, which is never swept (count 0).  Called by every thread.
-template <uint32_t STRIDE, int SUB = 1>
+template <uint32_t STRIDE>
 __device__ void pack_chunk(const SlabArgs& a, uint32_t c_begin, uint32_t c_n, uint4* s_rec, uint32_t* s_cnt,
                            uint32_t* s_hist, uint32_t* s_base, uint32_t* s_fill) {
   auto class_of = [&](uint32_t i, uint32_t& len, bool& bad) -> uint32_t {
@@ -316,15 +316,11 @@ __device__ void pack_chunk(const SlabArgs& a, uint32_t c_begin, uint32_t c_n, ui
     bool bad;
     const uint32_t cl = class_of(c_begin + j, len, bad);
     const uint32_t b = a.offs[c_begin + j];
-    const uint32_t slot = atomicAdd(&s_fill[cl], 1u);
-    const uint32_t pos = s_base[cl] + slot;
-    // slots swept by odd sub-groups of a packed-pair warp hold the columns
-    // reversed (see ebic_simd.cuh); only for fixed-length classes 2..7
-    const bool rev = SUB > 1 && (slot & 1u) && cl >= 2 && cl < 8;
+    const uint32_t pos = s_base[cl] + atomicAdd(&s_fill[cl], 1u);
     uint32_t h[8] = {j, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int k = 0; k < kRecCols; ++k)
-      if (!bad && (uint32_t)k < len) h[k + 1] = a.cols[b + (rev ? len - 1 - k : k)];
+      if (!bad && (uint32_t)k < len) h[k + 1] = a.cols[b + k];
     s_rec[pos] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
   }
 }

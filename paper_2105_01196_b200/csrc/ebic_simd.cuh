@@ -1,8 +1,7 @@
 // ebic_simd.cuh -- two rows per 32-bit word: the packed-rank slab kernel.
 //
 // Same rank-plane test as slab_count_kernel (R(y) > T(x) <=> v_y > thr(v_x),
-// see ebic_plane.cuh), but each slab column is restaged as one line of
-// 16-bit row PAIRS:
+// see ebic_plane.cuh), but each slab column is restaged as 16-bit row PAIRS:
 //   Rg[i] = (R(2i) | 0x8000) | (R(2i+1) | 0x8000) << 16        ("guarded" ranks)
 //   NT[i] = 0 - (T(2i) | T(2i+1) << 16) - 0x00010001            (negated thresholds)
 // For a consecutive pair (p, c) of a candidate, D = Rg[c] + NT[p] (mod 2^32)
@@ -11,24 +10,18 @@
 // interact (R, T <= C <= 8192 < 2^15).  One IADD tests two rows; AND-ing the
 // D's of all pairs and keeping bits 15/31 gives the verdict of both rows.
 //
-// Lane mapping: LPC = 32/SUB lanes per candidate, each lane owns P pair-words
+// Lane mapping: LPC = 32/SUB lanes per candidate, each lane owns P row pairs
 // (2P rows), so a slab holds RT = LPC * 2P rows:
 //   SUB=4, P=1: RT = 16  (C <= 2048)  four candidates per warp instruction
 //   SUB=2, P=1: RT = 32  (C <= 1024)  two candidates per warp instruction
 //   SUB=1, P=1: RT = 64  (C <= 512)
 //   SUB=1, P=2: RT = 128 (C <= 256)
-// Shared memory: one line per column, [RT/2 words Rg | RT/2 words NT] (4 B per
-// element, the same footprint as the u32 plane) while each lane does half the
-// instructions per row.
-//
-// Bank conflicts with several candidates per instruction: at SUB=2 a line is
-// 128 B, Rg in banks 0-15 and NT in banks 16-31 for EVERY column.  Because
-// D = Rg + NT is commutative, even sub-groups load (NT, Rg) and odd sub-groups
-// load (Rg, NT) for each column -- via per-lane base offsets, not branches --
-// and odd sub-groups get their candidate record with the columns REVERSED, so
-// the identical instruction sequence computes the same set of pair tests for
-// both.  Every LDS then has one half-warp in banks 0-15 and the other in 16-31:
-// conflict-free for any columns (at SUB=4 the same trick halves the conflicts).
+// Shared memory: one line per column with the row pairs interleaved,
+// [Rg_0 NT_0 Rg_1 NT_1 ...] (4 B per element, the same footprint as the u32
+// plane).  A lane fetches both words of its row pair(s) of a column with ONE
+// LDS.64 (P=1) / LDS.128 (P=2).  At SUB=2 each half-warp reads one whole,
+// aligned 128-B line per load: 2 wavefronts for 256 B, the minimum -- no bank
+// conflicts for any pair of columns.
 #pragma once
 #include <cstdint>
 
@@ -36,111 +29,94 @@
 
 namespace ebic {
 
+// Per-lane slab data: P row pairs x (Rg, NT) words; per-lane verdict: P words.
 template <int P> struct PairVec;
-template <> struct PairVec<1> { using V = uint32_t; };
-template <> struct PairVec<2> { using V = uint2; };
-template <> struct PairVec<4> { using V = uint4; };
-
-// D = Rg - T - 0x00010001 word-wise; keep the guard bits (15, 31)
-__device__ __forceinline__ uint32_t gt2(uint32_t rg, uint32_t t) { return (rg - t - 0x00010001u) & 0x80008000u; }
+template <> struct PairVec<1> { using V = uint2; using M = uint32_t; };
+template <> struct PairVec<2> { using V = uint4; using M = uint2; };
 
 __device__ __forceinline__ uint32_t& wref(uint32_t& v, int) { return v; }
 __device__ __forceinline__ uint32_t& wref(uint2& v, int q) { return q ? v.y : v.x; }
-__device__ __forceinline__ uint32_t& wref(uint4& v, int q) { return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w; }
 __device__ __forceinline__ uint32_t wget(const uint32_t& v, int) { return v; }
 __device__ __forceinline__ uint32_t wget(const uint2& v, int q) { return q ? v.y : v.x; }
 __device__ __forceinline__ uint32_t wget(const uint4& v, int q) { return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w; }
 
-template <int P, typename V>
-__device__ __forceinline__ void and_gt(V& acc, const V& rg, const V& t) {
+// D = Rg + NT (two rows at once); keep the guard bits 15/31
+__device__ __forceinline__ uint32_t sum2(uint32_t a, uint32_t b) { return (a + b) & 0x80008000u; }
+
+// acc[q] &= Rg_q(rg_src) + NT_q(nt_src)
+template <int P, typename M, typename V>
+__device__ __forceinline__ void and_pair(M& acc, const V& rg_src, const V& nt_src) {
 #pragma unroll
-  for (int q = 0; q < P; ++q) wref(acc, q) &= gt2(wget(rg, q), wget(t, q));
+  for (int q = 0; q < P; ++q) wref(acc, q) &= sum2(wget(rg_src, 2 * q), wget(nt_src, 2 * q + 1));
 }
 
-template <int P, typename V>
-__device__ __forceinline__ void or_into(V& acc, const V& x) {
+template <int P, typename M>
+__device__ __forceinline__ void or_into(M& acc, const M& x) {
 #pragma unroll
   for (int q = 0; q < P; ++q) wref(acc, q) |= wget(x, q);
 }
 
-template <int P, typename V>
-__device__ __forceinline__ uint32_t popc_words(const V& v) {
+template <int P, typename M>
+__device__ __forceinline__ uint32_t popc_words(const M& v) {
   uint32_t n = 0;
 #pragma unroll
   for (int q = 0; q < P; ++q) n += __popc(wget(v, q));
   return n;
 }
 
-// D = Rg + NT (two rows at once); keep the guard bits 15/31
-__device__ __forceinline__ uint32_t sum2(uint32_t a, uint32_t b) { return (a + b) & 0x80008000u; }
-
-template <int P, typename V>
-__device__ __forceinline__ void and_sum(V& acc, const V& x, const V& y) {
-#pragma unroll
-  for (int q = 0; q < P; ++q) wref(acc, q) &= sum2(wget(x, q), wget(y, q));
-}
-
-// Fixed-length body.  w1[k] / w2[k] are the two words of column rec[k] in this
-// sub-group's load order (even: NT then Rg; odd: Rg then NT, with the record
-// reversed).  Forward pair j is w1[j] + w2[j+1], reversed pair j is
-// w2[j] + w1[j+1] -- for both sub-groups.  Returns the guard bits of the lane's
-// row pairs that support the candidate.
+// Fixed-length body: L vector loads (both words of every column), then the
+// L-1 forward tests Rg(c_k) + NT(c_{k-1}) (and reversed Rg(c_{k-1}) + NT(c_k)).
+// Returns the guard bits of the lane's row pairs that support the candidate.
 template <int L, int P, bool NEG, uint32_t COLSHIFT>
-__device__ __forceinline__ typename PairVec<P>::V simd_eval(uint32_t base1, uint32_t base2, const uint4& rec,
-                                                          typename PairVec<P>::V vmask) {
+__device__ __forceinline__ typename PairVec<P>::M simd_eval(uint32_t lane_base, const uint4& rec,
+                                                          typename PairVec<P>::M vmask) {
   using V = typename PairVec<P>::V;
+  using M = typename PairVec<P>::M;
   const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
                                  hi16(rec.z), lo16(rec.w), hi16(rec.w)};
-  V w1[L], w2[L];
+  V w[L];
 #pragma unroll
-  for (int k = 0; k < L; ++k) {
-    const uint32_t off = cc[k] << COLSHIFT;
-    if (NEG || k + 1 < L) w1[k] = lds<V>(base1 + off);
-    if (NEG || k > 0) w2[k] = lds<V>(base2 + off);
-  }
-  V f = vmask;
+  for (int k = 0; k < L; ++k) w[k] = lds<V>(lane_base + (cc[k] << COLSHIFT));
+  M f = vmask;
 #pragma unroll
-  for (int k = 1; k < L; ++k) and_sum<P>(f, w1[k - 1], w2[k]);
+  for (int k = 1; k < L; ++k) and_pair<P>(f, w[k], w[k - 1]);
   if constexpr (NEG) {
-    V r = vmask;
+    M r = vmask;
 #pragma unroll
-    for (int k = 1; k < L; ++k) and_sum<P>(r, w2[k - 1], w1[k]);
+    for (int k = 1; k < L; ++k) and_pair<P>(r, w[k - 1], w[k]);
     or_into<P>(f, r);
   }
   return f;
 }
 
-template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT, uint32_t NTOFF>
-__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_line,
-                                                 uint32_t base1, uint32_t base2, uint32_t* s_cnt,
-                                                 uint32_t n_padded, uint32_t class_base, uint32_t c_begin,
-                                                 typename PairVec<P>::V vmask, int warp, int lane, int sub) {
+template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT>
+__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_base,
+                                                 uint32_t* s_cnt, uint32_t n_padded, uint32_t class_base,
+                                                 uint32_t c_begin, typename PairVec<P>::M vmask, int warp,
+                                                 int lane, int sub) {
   using V = typename PairVec<P>::V;
+  using M = typename PairVec<P>::M;
   constexpr int LPC = 32 / SUB;
   constexpr uint32_t stride = kSlabWarps * SUB;
   for (uint32_t t = warp * SUB + sub; t < n_padded; t += stride) {
     const uint4 rec = lds<uint4>(sa_rec + (class_base + t) * 16);
     const uint32_t j = lo16(rec.x);
-    V ok;
+    M ok;
     if constexpr (L == 1) {
       ok = vmask;  // no pair: every row supports (the trend.cpp:19 loop never runs)
     } else if constexpr (L < 8) {
-      ok = simd_eval<L, P, NEG, COLSHIFT>(base1, base2, rec, vmask);
+      ok = simd_eval<L, P, NEG, COLSHIFT>(lane_base, rec, vmask);
     } else {
-      // >= 8 columns (record not reversed): first 7 from the record, the tail
-      // from the CSR; fixed Rg/NT offsets (bank conflicts accepted on this rare path)
+      // >= 8 columns: first 7 from the record, the tail from the CSR
       const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
                                      hi16(rec.z), lo16(rec.w), hi16(rec.w)};
-      V f = vmask, r = NEG ? vmask : V{};
-      const uint32_t ap = lane_line + (cc[0] << COLSHIFT);
-      V rgp = NEG ? lds<V>(ap) : V{}, ntp = lds<V>(ap + NTOFF);
+      M f = vmask, r = NEG ? vmask : M{};
+      V wp = lds<V>(lane_base + (cc[0] << COLSHIFT));
       auto step = [&](uint32_t col) {
-        const uint32_t ac = lane_line + (col << COLSHIFT);
-        const V rgc = lds<V>(ac), ntc = lds<V>(ac + NTOFF);
-        and_sum<P>(f, rgc, ntp);
-        if (NEG) and_sum<P>(r, rgp, ntc);
-        rgp = rgc;
-        ntp = ntc;
+        const V wc = lds<V>(lane_base + (col << COLSHIFT));
+        and_pair<P>(f, wc, wp);
+        if (NEG) and_pair<P>(r, wp, wc);
+        wp = wc;
       };
 #pragma unroll
       for (int k = 1; k < kRecCols; ++k) step(cc[k]);
@@ -172,15 +148,14 @@ __device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_
 template <int P, int SUB, bool NEG>
 __global__ void __launch_bounds__(kSlabThreads, 1)
 slab_simd_kernel(const SlabArgs a) {
-  using V = typename PairVec<P>::V;
+  using M = typename PairVec<P>::M;
   constexpr int LPC = 32 / SUB;
   constexpr uint32_t RT = LPC * 2 * P;             // rows per slab
-  constexpr uint32_t CW = RT;                      // words per column line: RT/2 Rg + RT/2 NT
-  constexpr uint32_t NTOFF = RT * 2;                // bytes from a line's Rg words to its NT words
+  constexpr uint32_t CW = RT;                      // words per column line: RT/2 x (Rg, NT)
   constexpr uint32_t COLSHIFT = CW == 16 ? 6 : CW == 32 ? 7 : CW == 64 ? 8 : CW == 128 ? 9 : 10;  // log2(CW*4)
   static_assert((1u << COLSHIFT) == CW * 4, "column stride must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][Rg | NT]
+  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][RT/2 x (Rg, NT)]
   uint4* s_rec = reinterpret_cast<uint4*>(s_slab + (size_t)a.n_cols * CW);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rec + a.chunk + kClasses * kSlabWarps * SUB);
   __shared__ uint32_t s_hist[kClasses], s_base[kClasses], s_fill[kClasses];
@@ -189,10 +164,7 @@ slab_simd_kernel(const SlabArgs a) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / LPC, rl = lane % LPC;
-  const uint32_t lane_line = sa_slab + rl * P * 4;  // this lane's Rg words in column 0
-  // per-lane load order: even sub-groups (NT, Rg), odd sub-groups (Rg, NT)
-  const uint32_t base1 = lane_line + ((sub & 1) ? 0u : NTOFF);
-  const uint32_t base2 = lane_line + ((sub & 1) ? NTOFF : 0u);
+  const uint32_t lane_base = sa_slab + rl * P * 8;  // this lane's (Rg, NT) pair(s) in column 0
   const uint64_t U = (uint64_t)a.n_chunks * a.n_slabs;
   const uint64_t u_begin = blockIdx.x * U / gridDim.x, u_end = (blockIdx.x + 1) * U / gridDim.x;
   uint32_t cur_chunk = 0xffffffffu, c_begin = 0, c_n = 0;
@@ -212,13 +184,14 @@ slab_simd_kernel(const SlabArgs a) {
       cur_chunk = chunk;
       c_begin = chunk * a.chunk;
       c_n = min(a.chunk, a.n_cand - c_begin);
-      pack_chunk<kSlabWarps * SUB, SUB>(a, c_begin, c_n, s_rec, s_cnt, s_hist, s_base, s_fill);
+      pack_chunk<kSlabWarps * SUB>(a, c_begin, c_n, s_rec, s_cnt, s_hist, s_base, s_fill);
     }
     // stage + repack: each thread takes 4 consecutive rows (one uint4 of plane
-    // words) of one column and writes 2 pair-words to each 16-bit half-plane
+    // words) of one column -> 2 row pairs -> 4 words (Rg, NT, Rg, NT) of the line;
+    // a round of UNR loads is in flight before any store
     {
       constexpr uint32_t Q = RT / 4;  // uint4 per column
-      constexpr int UNR = 4;          // all loads of a round in flight before any use
+      constexpr int UNR = 4;
       const uint32_t total = a.n_cols * Q;
       const uint4* src = reinterpret_cast<const uint4*>(a.plane);
       const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
@@ -234,12 +207,11 @@ slab_simd_kernel(const SlabArgs a) {
           const uint32_t t = t0 + k * blockDim.x;
           if (t < total) {
             const uint32_t c = t / Q, q = t % Q;
-            const uint2 rg = make_uint2(__byte_perm(w[k].x, w[k].y, 0x7632) | 0x80008000u,
-                                        __byte_perm(w[k].z, w[k].w, 0x7632) | 0x80008000u);
-            const uint2 nt = make_uint2(0u - __byte_perm(w[k].x, w[k].y, 0x5410) - 0x00010001u,
-                                        0u - __byte_perm(w[k].z, w[k].w, 0x5410) - 0x00010001u);
-            *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + 2 * q) = rg;
-            *reinterpret_cast<uint2*>(s_slab + (size_t)c * CW + RT / 2 + 2 * q) = nt;
+            const uint4 v = make_uint4(__byte_perm(w[k].x, w[k].y, 0x7632) | 0x80008000u,
+                                       0u - __byte_perm(w[k].x, w[k].y, 0x5410) - 0x00010001u,
+                                       __byte_perm(w[k].z, w[k].w, 0x7632) | 0x80008000u,
+                                       0u - __byte_perm(w[k].z, w[k].w, 0x5410) - 0x00010001u);
+            *reinterpret_cast<uint4*>(s_slab + (size_t)c * CW + 4 * q) = v;
           }
         }
       }
@@ -249,16 +221,16 @@ slab_simd_kernel(const SlabArgs a) {
 
     // validity guard bits of this lane's row pairs (rows beyond n_rows never count)
     const uint32_t valid_rows = min(RT, a.n_rows - row0);
-    V vmask;
+    M vmask;
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       const uint32_t r = (rl * P + q) * 2;
       wref(vmask, q) = (r < valid_rows ? 0x8000u : 0u) | (r + 1 < valid_rows ? 0x80000000u : 0u);
     }
 
-#define EBIC_SIMD_SWEEP(L)                                                                                  \
-  simd_sweep_class<P, SUB, NEG, L, COLSHIFT, NTOFF>(a, sa_rec, lane_line, base1, base2, s_cnt, s_hist[L], \
-                                                    s_base[L], c_begin, vmask, warp, lane, sub)
+#define EBIC_SIMD_SWEEP(L)                                                                                      \
+  simd_sweep_class<P, SUB, NEG, L, COLSHIFT>(a, sa_rec, lane_base, s_cnt, s_hist[L], s_base[L], c_begin, vmask, \
+                                             warp, lane, sub)
     EBIC_SIMD_SWEEP(4);
     EBIC_SIMD_SWEEP(3);
     EBIC_SIMD_SWEEP(5);
