@@ -226,12 +226,24 @@ __device__ __forceinline__ void sweep_class(const SlabArgs& a, uint32_t sa_rec, 
         wp = wc;
       }
       if (j < a.chunk) {
+        // the tail in blocks of TB columns (independent index loads, then shared loads)
+        constexpr int TB = RPL == 1 ? 8 : RPL == 2 ? 4 : 2;  // register budget: 64 per thread
         const uint32_t b = a.offs[c_begin + j], e = a.offs[c_begin + j + 1];
-        for (uint32_t k = b + kRecCols; k < e; ++k) {
+        for (uint32_t k0 = b + kRecCols; k0 < e; k0 += TB) {
           if ((okf | okr) == 0u) break;  // this lane's rows are all decided
-          const V wc = lds<V>(lane_base + (__ldg(a.cols + k) << COLSHIFT));
-          pair_test<RPL, NEG>(wp, wc, okf, okr);
-          wp = wc;
+          uint32_t idx[TB];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) idx[i] = k0 + i < e ? __ldg(a.cols + k0 + i) : 0u;
+          V wv[TB];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) wv[i] = lds<V>(lane_base + (idx[i] << COLSHIFT));
+#pragma unroll
+          for (int i = 0; i < TB; ++i) {
+            if (k0 + i < e) {
+              pair_test<RPL, NEG>(wp, wv[i], okf, okr);
+              wp = wv[i];
+            }
+          }
         }
       }
       ok = okf | okr;

@@ -121,13 +121,29 @@ __device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_
 #pragma unroll
       for (int k = 1; k < kRecCols; ++k) step(cc[k]);
       if (j < a.chunk) {
+        // the tail in blocks of TB columns: TB independent index loads, then TB
+        // shared loads, then the pair tests (no load-to-load dependency chain)
+        constexpr int TB = P == 1 ? 8 : (NEG ? 2 : 4);  // register budget: 64 per thread
         const uint32_t b = a.offs[c_begin + j], e = a.offs[c_begin + j + 1];
-        for (uint32_t k = b + kRecCols; k < e; ++k) {
+        for (uint32_t k0 = b + kRecCols; k0 < e; k0 += TB) {
           uint32_t any = 0;
 #pragma unroll
           for (int q = 0; q < P; ++q) any |= wget(f, q) | wget(r, q);
           if (!any) break;  // this lane's rows are all decided
-          step(__ldg(a.cols + k));
+          uint32_t idx[TB];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) idx[i] = k0 + i < e ? __ldg(a.cols + k0 + i) : 0u;
+          V wv[TB];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) wv[i] = lds<V>(lane_base + (idx[i] << COLSHIFT));
+#pragma unroll
+          for (int i = 0; i < TB; ++i) {
+            if (k0 + i < e) {
+              and_pair<P>(f, wv[i], wp);
+              if (NEG) and_pair<P>(r, wp, wv[i]);
+              wp = wv[i];
+            }
+          }
         }
       }
       if (NEG) or_into<P>(f, r);
