@@ -25,4 +25,5 @@ done
 for c in c2 c4 c5; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_${c}_$TAG.json 2> $OUT/bench_${c}_$TAG.err
 done
+timeout 900 python scripts/run_e2e.py > $OUT/run_e2e_$TAG.txt 2>&1
 echo done

@@ -1,0 +1,41 @@
+"""End-to-end bicseek::run() -- the UNCHANGED reference evolution engine -- with
+the reference CPU evaluator (oracle/_ref/run_ref, WorkerPool of all cores) vs the
+B200 evaluator (oracle/_ref/run_device, the drop-in trend TU).  Reports run()
+wall time (its own steady_clock, evolution.cpp:308,330-331) and checks that the
+two produce identical biclusters, generation counts and termination."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+CASES = [
+    ("config1 default (tabu stop)", []),
+    ("config1 forced 200 gens", ["--tabu", "1000000000000"]),
+    ("10k x 500, P=4096, 20 gens", ["--rows", "10000", "--cols", "500", "--bic-rows", "500", "--bic-cols", "20",
+                                    "--pop", "4096", "--iters", "20", "--tabu", "1000000000000"]),
+    ("20k x 1000, P=4096, 10 gens", ["--rows", "20000", "--cols", "1000", "--bic-rows", "500", "--bic-cols", "20",
+                                     "--pop", "4096", "--iters", "10", "--tabu", "1000000000000"]),
+]
+
+
+def run(exe, args):
+    env = dict(os.environ, EBIC_SHIM_TRUST_POINTER="1")
+    out = subprocess.run([str(REPO / "oracle" / "_ref" / exe), *args], check=True, capture_output=True, text=True,
+                         env=env, timeout=1800).stdout
+    return json.loads(out)
+
+
+def main():
+    print(f"host: {os.cpu_count()} cores")
+    for label, args in CASES:
+        a, b = run("run_ref", args), run("run_device", args)
+        same = a["result"] == b["result"] and a["generations"] == b["generations"] and a["termination"] == b["termination"]
+        print(f"{label:32s} gens {a['generations']:4d} {a['termination']:9s} run() CPU {a['wall_s']:8.3f} s  "
+              f"B200 {b['wall_s']:8.3f} s  speed-up {a['wall_s'] / max(b['wall_s'], 1e-9):6.2f}x  identical={same}")
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()
