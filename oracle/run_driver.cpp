@@ -16,6 +16,7 @@
 
 #include "bicseek/datagen.hpp"
 #include "bicseek/evolution.hpp"
+#include "bicseek/trend.hpp"
 
 using namespace bicseek;
 
@@ -47,6 +48,7 @@ int main(int argc, char** argv) {
   EvolutionParams p;
   p.max_iterations = 200;
   bool quantize = true;
+  bool warm = false;
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i];
     const char* v = argv[i + 1];
@@ -65,6 +67,7 @@ int main(int argc, char** argv) {
     else if (k == "--approx") p.trend.approx = std::strtod(v, nullptr);
     else if (k == "--negative") p.trend.negative_trends = std::atoi(v) != 0;
     else if (k == "--quantize") quantize = std::atoi(v) != 0;
+    else if (k == "--warm") warm = std::atoi(v) != 0;
     else {
       std::fprintf(stderr, "unknown option %s\n", k.c_str());
       return 2;
@@ -76,6 +79,12 @@ int main(int argc, char** argv) {
     for (double& x : v) x = static_cast<double>(static_cast<float>(x));
   const ExpressionMatrix m(std::move(v), d.matrix.rows(), d.matrix.cols(), d.matrix.row_labels(),
                            d.matrix.col_labels());
+  if (warm) {
+    // one tiny evaluation before run(): takes one-time device/context start-up
+    // (CUDA context creation for the device build) out of run()'s own timer
+    const ExpressionMatrix w({1.0, 2.0, 2.0, 1.0}, 2, 2, default_labels('r', 2), default_labels('c', 2));
+    (void)evaluate_population(w, {Chromosome({0, 1})}, p.trend, nullptr);
+  }
   const RunResult r = run(m, p);
   std::printf("{\"result\":%s,\"generations\":%zu,\"termination\":\"%s\",\"wall_s\":%.6f}\n",
               bics_json(r.biclusters).c_str(), r.report.generations, r.report.termination.c_str(),

@@ -1,8 +1,9 @@
 """End-to-end bicseek::run() -- the UNCHANGED reference evolution engine -- with
 the reference CPU evaluator (oracle/_ref/run_ref, WorkerPool of all cores) vs the
 B200 evaluator (oracle/_ref/run_device, the drop-in trend TU).  Reports run()
-wall time (its own steady_clock, evolution.cpp:308,330-331) and checks that the
-two produce identical biclusters, generation counts and termination."""
+wall time (its own steady_clock, evolution.cpp:308,330-331; one tiny warm-up
+evaluation before run() keeps CUDA context creation out of it) and checks that
+the two produce identical biclusters, generation counts and termination."""
 import json
 import os
 import subprocess
@@ -22,7 +23,7 @@ CASES = [
 
 def run(exe, args):
     env = dict(os.environ, EBIC_SHIM_TRUST_POINTER="1")
-    out = subprocess.run([str(REPO / "oracle" / "_ref" / exe), *args], check=True, capture_output=True, text=True,
+    out = subprocess.run([str(REPO / "oracle" / "_ref" / exe), "--warm", "1", *args], check=True, capture_output=True, text=True,
                          env=env, timeout=1800).stdout
     return json.loads(out)
 
