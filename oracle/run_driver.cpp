@@ -5,7 +5,9 @@
 // it twice against the SAME unmodified evolution.cpp:
 //   oracle/_ref/run_ref     with the reference trend.cpp      (CPU evaluator)
 //   oracle/_ref/run_device  with bicseek_trend_device.cpp     (B200 evaluator)
-// and tests/test_run_parity.py requires byte-identical output.
+//   oracle/_ref/run_device_overlap  additionally --engine device: the
+//                   device-aware driver (csrc/bicseek_run_device.cpp)
+// and tests/test_gpu_reference_suite.py requires byte-identical output.
 //
 // Output (stdout, one JSON object): the canonical bicluster JSON of
 // io.cpp:131-150 (restated), generations, termination, evaluation count.
@@ -19,6 +21,13 @@
 #include "bicseek/trend.hpp"
 
 using namespace bicseek;
+
+#ifdef EBIC_DEVICE_RUN
+// paper_2105_01196_b200/csrc/bicseek_run_device.cpp: the device-aware driver
+namespace bicseek_device {
+RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device);
+}
+#endif
 
 static std::string bics_json(const BiclusterSet& set) {
   std::string out = "{\"biclusters\":[";
@@ -49,6 +58,7 @@ int main(int argc, char** argv) {
   p.max_iterations = 200;
   bool quantize = true;
   bool warm = false;
+  std::string engine = "reference";
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i];
     const char* v = argv[i + 1];
@@ -68,6 +78,7 @@ int main(int argc, char** argv) {
     else if (k == "--negative") p.trend.negative_trends = std::atoi(v) != 0;
     else if (k == "--quantize") quantize = std::atoi(v) != 0;
     else if (k == "--warm") warm = std::atoi(v) != 0;
+    else if (k == "--engine") engine = v;
     else {
       std::fprintf(stderr, "unknown option %s\n", k.c_str());
       return 2;
@@ -85,7 +96,17 @@ int main(int argc, char** argv) {
     const ExpressionMatrix w({1.0, 2.0, 2.0, 1.0}, 2, 2, default_labels('r', 2), default_labels('c', 2));
     (void)evaluate_population(w, {Chromosome({0, 1})}, p.trend, nullptr);
   }
-  const RunResult r = run(m, p);
+  RunResult r;
+  if (engine == "reference") {
+    r = run(m, p);
+  } else {
+#ifdef EBIC_DEVICE_RUN
+    r = bicseek_device::run(m, p, 0);
+#else
+    std::fprintf(stderr, "engine '%s' not built into this binary\n", engine.c_str());
+    return 2;
+#endif
+  }
   std::printf("{\"result\":%s,\"generations\":%zu,\"termination\":\"%s\",\"wall_s\":%.6f}\n",
               bics_json(r.biclusters).c_str(), r.report.generations, r.report.termination.c_str(),
               r.report.wall_time_seconds);

@@ -1,6 +1,7 @@
 """End-to-end bicseek::run() -- the UNCHANGED reference evolution engine -- with
 the reference CPU evaluator (oracle/_ref/run_ref, WorkerPool of all cores) vs the
-B200 evaluator (oracle/_ref/run_device, the drop-in trend TU).  Reports run()
+B200 evaluator (oracle/_ref/run_device, the drop-in trend TU) vs the
+device-aware driver (oracle/_ref/run_device_overlap --engine device).  Reports run()
 wall time (its own steady_clock, evolution.cpp:308,330-331; one tiny warm-up
 evaluation before run() keeps CUDA context creation out of it) and checks that
 the two produce identical biclusters, generation counts and termination."""
@@ -21,9 +22,9 @@ CASES = [
 ]
 
 
-def run(exe, args):
+def run(exe, args, extra=()):
     env = dict(os.environ, EBIC_SHIM_TRUST_POINTER="1")
-    out = subprocess.run([str(REPO / "oracle" / "_ref" / exe), "--warm", "1", *args], check=True, capture_output=True, text=True,
+    out = subprocess.run([str(REPO / "oracle" / "_ref" / exe), "--warm", "1", *extra, *args], check=True, capture_output=True, text=True,
                          env=env, timeout=1800).stdout
     return json.loads(out)
 
@@ -32,9 +33,13 @@ def main():
     print(f"host: {os.cpu_count()} cores")
     for label, args in CASES:
         a, b = run("run_ref", args), run("run_device", args)
-        same = a["result"] == b["result"] and a["generations"] == b["generations"] and a["termination"] == b["termination"]
-        print(f"{label:32s} gens {a['generations']:4d} {a['termination']:9s} run() CPU {a['wall_s']:8.3f} s  "
-              f"B200 {b['wall_s']:8.3f} s  speed-up {a['wall_s'] / max(b['wall_s'], 1e-9):6.2f}x  identical={same}")
+        c = run("run_device_overlap", args, ("--engine", "device"))
+        same = all(x["result"] == a["result"] and x["generations"] == a["generations"] and
+                   x["termination"] == a["termination"] for x in (b, c))
+        print(f"{label:30s} gens {a['generations']:4d} {a['termination']:9s} CPU ref {a['wall_s']:7.3f} s | "
+              f"B200 drop-in TU {b['wall_s']:7.3f} s ({a['wall_s'] / max(b['wall_s'], 1e-9):5.2f}x) | "
+              f"B200 device driver {c['wall_s']:7.3f} s ({a['wall_s'] / max(c['wall_s'], 1e-9):5.2f}x) | "
+              f"identical={same}")
         sys.stdout.flush()
 
 

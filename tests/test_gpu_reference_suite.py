@@ -44,3 +44,31 @@ def test_run_config1_byte_identical_to_reference(label):
     assert json.dumps(got["result"], sort_keys=True) == json.dumps(golden["result"], sort_keys=True)
     assert got["generations"] == golden["generations"]
     assert got["termination"] == golden["termination"]
+
+
+@pytest.mark.parametrize("label", ["default", "forced200", "neg_forced60"])
+def test_device_aware_driver_byte_identical_to_reference(label):
+    """The device-aware evolution driver (csrc/bicseek_run_device.cpp: one upload
+    per run, evaluation overlapped with breeding, batched archive row sets)
+    returns exactly the reference run()'s result on BASELINE config 1."""
+    exe = _need("run_device_overlap")
+    golden = json.loads((GOLDEN / "run_cfg1.json").read_text())[label]
+    out = subprocess.run([str(exe), "--engine", "device", *golden["args"]], check=True, capture_output=True,
+                         text=True, timeout=600).stdout
+    got = json.loads(out)
+    assert json.dumps(got["result"], sort_keys=True) == json.dumps(golden["result"], sort_keys=True)
+    assert got["generations"] == golden["generations"]
+    assert got["termination"] == golden["termination"]
+
+
+def test_device_aware_driver_matches_reference_at_scale():
+    """A larger run (10k x 500, P=1024, 15 generations, negatives on): the
+    driver's output equals the unchanged reference GA on the device TU."""
+    exe_a, exe_b = _need("run_device"), _need("run_device_overlap")
+    args = ["--rows", "10000", "--cols", "500", "--bic-rows", "500", "--bic-cols", "20", "--pop", "1024",
+            "--iters", "15", "--tabu", "1000000000000", "--negative", "1"]
+    a = json.loads(subprocess.run([str(exe_a), *args], check=True, capture_output=True, text=True,
+                                  timeout=600).stdout)
+    b = json.loads(subprocess.run([str(exe_b), "--engine", "device", *args], check=True, capture_output=True,
+                                  text=True, timeout=600).stdout)
+    assert a["result"] == b["result"] and a["generations"] == b["generations"]
