@@ -122,6 +122,8 @@ struct ebic_ctx {
   HostBuf<uint32_t> h_tmp_counts;
   Slot slots[EBIC_MARSHAL_SLOTS];
   uint64_t next_ticket = 1;
+  // tickets retired early (ring reuse / slot growth) whose device-side check failed
+  std::vector<uint64_t> failed_tickets;
   uint64_t launches = 0;
   uint32_t slab_rows = 0;  // 0 = auto (value path)
   // rank plane (per matrix x approx)
@@ -518,18 +520,30 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   return EBIC_OK;
 }
 
-int wait_slot(ebic_ctx* ctx, Slot& sl) {
+int bad_column_error(const ebic_ctx* ctx) {
+  return fail(EBIC_ERR_INVALID_ARGUMENT, "a candidate has a column index out of range (cols=%llu); its count is 0",
+              (unsigned long long)ctx->n_cols);
+}
+
+// Retire a slot: wait for its copies, hand the counts to the caller's buffer.
+// `early` = retired on behalf of another submission (ring reuse or growth): a
+// device-detected error is then remembered for that ticket's ebic_eval_wait
+// instead of being returned here.
+int wait_slot(ebic_ctx* ctx, Slot& sl, bool early = false) {
   if (!sl.ticket) return EBIC_OK;
   EBIC_CUDA(cudaEventSynchronize(sl.done));
   if (sl.user_counts) std::memcpy(sl.user_counts, sl.h_counts.p, sl.n_cand * sizeof(uint32_t));
   const int err = sl.h_err.p ? sl.h_err.p[0] : 0;
+  const uint64_t t = sl.ticket;
   sl.ticket = 0;
   sl.user_counts = nullptr;
-  (void)ctx;
-  if (err)
-    return fail(EBIC_ERR_INVALID_ARGUMENT,
-                "a candidate has a column index out of range (cols=%llu); its count is 0",
-                (unsigned long long)ctx->n_cols);
+  if (err) {
+    if (early) {
+      ctx->failed_tickets.push_back(t);
+      return EBIC_OK;
+    }
+    return bad_column_error(ctx);
+  }
   return EBIC_OK;
 }
 
@@ -703,11 +717,18 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
   EBIC_TRY(set_device(ctx));
   const uint64_t ticket = ctx->next_ticket++;
   Slot& sl = ctx->slots[ticket % EBIC_MARSHAL_SLOTS];
-  EBIC_TRY(wait_slot(ctx, sl));  // ring full: retire the oldest submission first
+  EBIC_TRY(wait_slot(ctx, sl, /*early=*/true));  // ring full: retire the oldest submission first
   const uint64_t n_idx = n_cand ? offsets[n_cand] : 0;
   // Grow every slot of the ring together (cudaMallocHost costs milliseconds):
   // after the first submission of a given size, no later submission allocates.
+  // A slot still in flight is retired first -- its pending copies target the
+  // buffers that growing would free.
   for (Slot& any : ctx->slots) {
+    const bool grow = any.h_cols.n < n_idx || any.h_offs.n < n_cand + 1 || any.h_counts.n < n_cand ||
+                      !any.h_cols.p || !any.h_offs.p || !any.h_counts.p || !any.h_err.p ||
+                      any.d_cols.n < n_idx || any.d_offs.n < n_cand + 1 || any.d_counts.n < n_cand;
+    if (!grow) continue;
+    if (&any != &sl) EBIC_TRY(wait_slot(ctx, any, /*early=*/true));
     EBIC_TRY(ensure(any.h_cols, n_idx));
     EBIC_TRY(ensure(any.h_offs, n_cand + 1));
     EBIC_TRY(ensure(any.h_counts, n_cand));
@@ -750,7 +771,13 @@ int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket) {
   if (sl.ticket != ticket) {
     if (ticket == 0 || ticket >= ctx->next_ticket)
       return fail(EBIC_ERR_INVALID_ARGUMENT, "unknown ticket %llu", (unsigned long long)ticket);
-    return EBIC_OK;  // already retired (its slot was reused)
+    // already retired (its slot was reused): report its device-side error, once
+    auto it = std::find(ctx->failed_tickets.begin(), ctx->failed_tickets.end(), ticket);
+    if (it != ctx->failed_tickets.end()) {
+      ctx->failed_tickets.erase(it);
+      return bad_column_error(ctx);
+    }
+    return EBIC_OK;
   }
   EBIC_TRY(set_device(ctx));
   return wait_slot(ctx, sl);

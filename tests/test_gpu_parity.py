@@ -280,13 +280,26 @@ def test_marshaller_ring(evaluator):
     rng = np.random.default_rng(4)
     m = rng.standard_normal((4000, 50)).astype(np.float32)
     evaluator.upload(m)
-    pops = [synth.random_population(int(rng.integers(1, 900)), 50, seed=i) for i in range(7)]
+    # growing sizes force the ring's pinned buffers to grow while earlier
+    # submissions are still in flight; more submissions than EBIC_MARSHAL_SLOTS
+    sizes = [300, 700, 1500, 1400, 3000, 6000, 200, 9000, 50]
+    pops = [synth.random_population(n, 50, seed=i) for i, n in enumerate(sizes)]
     outs = [np.zeros(len(p), dtype=np.uint32) for p in pops]
-    tickets = [evaluator.submit(p, o) for p, o in zip(pops, outs)]  # more than EBIC_MARSHAL_SLOTS in flight
+    tickets = [evaluator.submit(p, o) for p, o in zip(pops, outs)]
     for t in tickets:
         evaluator.wait(t)
     for p, o in zip(pops, outs):
         np.testing.assert_array_equal(o, oracle.evaluate_population(m, p.cols, p.offsets, 0.03, False))
+    # a bad column in an early submission is reported by ITS wait, not by a later submit
+    bad = Population(np.array([0, 99], np.uint32), np.array([0, 2], np.uint32))
+    ob = np.zeros(1, dtype=np.uint32)
+    tb = evaluator.submit(bad, ob)
+    later = [evaluator.submit(p, o) for p, o in zip(pops[:5], outs[:5])]
+    for t in later:
+        evaluator.wait(t)
+    with pytest.raises(EbicError, match="out of range"):
+        evaluator.wait(tb)
+    evaluator.wait(tb)  # reported once
 
 
 def test_errors_are_reported_not_undefined(evaluator):
