@@ -390,7 +390,9 @@ int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
       return launch_slab<false, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
     }
   }
-  if (ctx->path == EBIC_PATH_PLANE || ctx->path == EBIC_PATH_PLANE_U32)
+  // (row masks for supporting_rows may always fall back to the value kernel:
+  // the path knob is about the counting kernels)
+  if (!MASK && (ctx->path == EBIC_PATH_PLANE || ctx->path == EBIC_PATH_PLANE_U32))
     return fail(EBIC_ERR_INVALID_ARGUMENT, "rank-plane path unavailable for a %llu-column matrix",
                 (unsigned long long)ctx->n_cols);
   const ebic::TrendArgs ta = make_args(approx, neg);
