@@ -134,6 +134,7 @@ struct ebic_ctx {
   int n_sms = 148;
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
+  int plane_builder = 0;  // 0 auto, 1 force the block-sort builder (EBIC_PLANE_BUILDER=1, cross-checks)
 };
 
 namespace {
@@ -197,7 +198,19 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   const size_t esz = ctx->store == EBIC_STORE_F32 ? sizeof(float) : sizeof(double);
   const size_t smem = pow2 * esz;
   const unsigned grid = (unsigned)std::min<uint64_t>(ctx->n_rows, (uint64_t)ctx->n_sms * 8);
-  if (ctx->store == EBIC_STORE_F32) {
+  if (ctx->store == EBIC_STORE_F32 && ctx->n_cols <= 1024 && ctx->plane_builder != 1) {
+    // warp-per-row register sort (no block barriers)
+    const unsigned g = (unsigned)std::min<uint64_t>((ctx->n_rows + ebic::kPlaneWarps - 1) / ebic::kPlaneWarps,
+                                                    (uint64_t)ctx->n_sms * 8);
+    const float* st = (const float*)ctx->d_mat;
+    const uint32_t R = (uint32_t)ctx->n_rows, C = (uint32_t)ctx->n_cols;
+    const unsigned bs = ebic::kPlaneWarps * 32;
+    if (C <= 64) ebic::build_plane_warp_kernel<2><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
+    else if (C <= 128) ebic::build_plane_warp_kernel<4><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
+    else if (C <= 256) ebic::build_plane_warp_kernel<8><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
+    else if (C <= 512) ebic::build_plane_warp_kernel<16><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
+    else ebic::build_plane_warp_kernel<32><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
+  } else if (ctx->store == EBIC_STORE_F32) {
     EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ebic::build_plane_kernel<float><<<grid, 256, smem, s>>>((const float*)ctx->d_mat, ctx->ld, (uint32_t)ctx->n_rows,
                                                            (uint32_t)ctx->n_cols, pow2, approx, ctx->d_plane);
@@ -600,6 +613,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
       ctx->smem_optin = (size_t)v;
     const char* e = std::getenv("EBIC_PATH");
     if (e) ctx->path = std::atoi(e);
+    const char* pb = std::getenv("EBIC_PLANE_BUILDER");
+    if (pb) ctx->plane_builder = std::atoi(pb);
     const char* pf = std::getenv("EBIC_PREFETCH");
     if (pf) ctx->prefetch = std::atoi(pf) ? 1 : 0;
   }

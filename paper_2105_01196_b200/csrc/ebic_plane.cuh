@@ -181,6 +181,96 @@ __device__ __forceinline__ uint32_t eval_fixed(uint32_t lane_base, const uint4& 
 }
 
 // ---------------------------------------------------------------------------
+// plane builder, fast path: float32 store, C <= 32*E.  One WARP per row: the
+// row is sorted in registers (E consecutive elements per lane, bitonic network
+// -- in-lane stages on registers, cross-lane stages with __shfl_xor_sync, no
+// block barriers), written once to a per-warp shared buffer, then R and T come
+// from two binary searches per element exactly as in build_plane_kernel.
+// Sort keys are the order-preserving unsigned images of the floats; the
+// searches compare the floats themselves (so -0.0 == +0.0 as in the reference).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t f2key(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+constexpr int kPlaneWarps = 8;
+
+template <int E>
+__global__ void __launch_bounds__(kPlaneWarps * 32)
+build_plane_warp_kernel(const float* __restrict__ store, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
+                        double approx, uint32_t* __restrict__ plane) {
+  __shared__ float s_sorted[kPlaneWarps][32 * E];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* srt = s_sorted[warp];
+  for (uint32_t row = blockIdx.x * kPlaneWarps + warp; row < n_rows; row += gridDim.x * kPlaneWarps) {
+    uint32_t k[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const uint32_t c = lane * E + j;
+      k[j] = c < n_cols ? f2key(store[(uint64_t)c * ld + row]) : 0xFFFFFFFFu;
+    }
+    // bitonic sort of N = 32E keys; element g = lane*E + j
+#pragma unroll
+    for (int kk = 2; kk <= 32 * E; kk <<= 1) {
+#pragma unroll
+      for (int d = kk >> 1; d > 0; d >>= 1) {
+        if (d < E) {
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            if ((j & d) == 0) {
+              const uint32_t g = lane * E + j;
+              const bool up = (g & kk) == 0;
+              const uint32_t a = k[j], b = k[j ^ d];
+              const uint32_t lo = min(a, b), hi = max(a, b);
+              k[j] = up ? lo : hi;
+              k[j ^ d] = up ? hi : lo;
+            }
+          }
+        } else {
+          const int lx = d / E;
+          const bool lower = (lane & lx) == 0;
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            const uint32_t g = lane * E + j;
+            const bool up = (g & kk) == 0;
+            const uint32_t o = __shfl_xor_sync(kFull, k[j], lx);
+            k[j] = (lower == up) ? min(k[j], o) : max(k[j], o);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const uint32_t c = lane * E + j;
+      if (c < n_cols) srt[c] = key2f(k[j]);
+    }
+    __syncwarp();
+    for (uint32_t c = lane; c < n_cols; c += 32) {
+      const float v = store[(uint64_t)c * ld + row];
+      uint32_t lo = 0, hi = n_cols;  // lower_bound: #values < v
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (srt[mid] < v) lo = mid + 1; else hi = mid;
+      }
+      const uint32_t rank1 = lo + 1;
+      const double t = thr64((double)v, approx);  // upper_bound: #values <= thr(v)
+      lo = 0;
+      hi = n_cols;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((double)srt[mid] <= t) lo = mid + 1; else hi = mid;
+      }
+      plane[(uint64_t)c * ld + row] = (rank1 << 16) | lo;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // slab kernel
 //   RPL : consecutive rows per lane (1, 2, 4)   -> LDS.32 / .64 / .128
 //   SUB : candidates per warp (1, 2, 4)          -> 32/SUB lanes per candidate

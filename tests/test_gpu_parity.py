@@ -383,3 +383,30 @@ def test_wide_matrices_every_slab_variant(path_evaluator, n_cols):
         want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
         got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
         np.testing.assert_array_equal(got, want, err_msg=f"C={n_cols} approx={approx} neg={neg}")
+
+
+@pytest.mark.parametrize("n_cols", [2, 33, 64, 65, 200, 511, 1000, 1024])
+def test_warp_plane_builder_equals_block_builder(n_cols, monkeypatch):
+    """The warp-per-row register-sort plane builder (f32, C <= 1024) gives the
+    same counts as the block bitonic builder, on rows full of ties, signed
+    zeros, subnormals and huge values."""
+    from paper_2105_01196_b200 import Evaluator
+
+    rng = np.random.default_rng(n_cols)
+    vals = np.array([0.0, -0.0, 1e-45, -1e-45, 1.0, 1.0, -1.0, 3.4e38, -3.4e38, 0.97, 1.03], dtype=np.float32)
+    m = np.where(rng.random((777, n_cols)) < 0.5, rng.choice(vals, size=(777, n_cols)),
+                 rng.standard_normal((777, n_cols)).astype(np.float32)).astype(np.float32)
+    seqs = [rng.choice(n_cols, size=int(rng.integers(1, min(n_cols, 7) + 1)), replace=False) for _ in range(400)]
+    pop = Population.from_sequences(seqs)
+    results = []
+    for builder in ("0", "1"):
+        monkeypatch.setenv("EBIC_PLANE_BUILDER", builder)
+        with Evaluator(0) as ev:
+            ev.upload(m)
+            ev.set_path(EBIC_PATH_PLANE)
+            results.append([ev.evaluate_population(pop, TrendParams(a, neg)) for a, neg in
+                            ((0.0, True), (0.03, False), (0.5, True))])
+    for got_warp, got_block, (a, neg) in zip(results[0], results[1], ((0.0, True), (0.03, False), (0.5, True))):
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, a, neg)
+        np.testing.assert_array_equal(got_warp, want)
+        np.testing.assert_array_equal(got_block, want)
