@@ -134,7 +134,7 @@ struct ebic_ctx {
   int n_sms = 148;
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
-  int plane_builder = 0;  // 0 auto, 1 force the block-sort builder (EBIC_PLANE_BUILDER=1, cross-checks)
+  int plane_builder = 0;  // 0 auto (row-tile builder), 1 force the per-row block-sort builder (EBIC_PLANE_BUILDER=1)
 };
 
 namespace {
@@ -198,18 +198,25 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   const size_t esz = ctx->store == EBIC_STORE_F32 ? sizeof(float) : sizeof(double);
   const size_t smem = pow2 * esz;
   const unsigned grid = (unsigned)std::min<uint64_t>(ctx->n_rows, (uint64_t)ctx->n_sms * 8);
-  if (ctx->store == EBIC_STORE_F32 && ctx->n_cols <= 1024 && ctx->plane_builder != 1) {
-    // warp-per-row register sort (no block barriers)
-    const unsigned g = (unsigned)std::min<uint64_t>((ctx->n_rows + ebic::kPlaneWarps - 1) / ebic::kPlaneWarps,
-                                                    (uint64_t)ctx->n_sms * 8);
-    const float* st = (const float*)ctx->d_mat;
-    const uint32_t R = (uint32_t)ctx->n_rows, C = (uint32_t)ctx->n_cols;
-    const unsigned bs = ebic::kPlaneWarps * 32;
-    if (C <= 64) ebic::build_plane_warp_kernel<2><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
-    else if (C <= 128) ebic::build_plane_warp_kernel<4><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
-    else if (C <= 256) ebic::build_plane_warp_kernel<8><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
-    else if (C <= 512) ebic::build_plane_warp_kernel<16><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
-    else ebic::build_plane_warp_kernel<32><<<g, bs, 0, s>>>(st, ctx->ld, R, C, approx, ctx->d_plane);
+  // row-tile builder: RG rows per CTA (8 when they fit in ~96 KB of shared memory)
+  uint32_t rg = 8;
+  while (rg > 1 && (size_t)rg * ((ctx->n_cols + 1) + pow2) * esz > 96 * 1024) rg >>= 1;
+  const size_t tile_smem = (size_t)rg * ((ctx->n_cols + 1) + pow2) * esz;
+  if (ctx->plane_builder != 1 && tile_smem <= 200 * 1024) {
+    const unsigned g = (unsigned)std::min<uint64_t>((ctx->n_rows + rg - 1) / rg, (uint64_t)ctx->n_sms * 16);
+    if (ctx->store == EBIC_STORE_F32) {
+      EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_tile_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_smem));
+      ebic::build_plane_tile_kernel<float><<<g, 256, tile_smem, s>>>((const float*)ctx->d_mat, ctx->ld,
+                                                                     (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols,
+                                                                     pow2, rg, approx, ctx->d_plane);
+    } else {
+      EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_tile_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tile_smem));
+      ebic::build_plane_tile_kernel<double><<<g, 256, tile_smem, s>>>((const double*)ctx->d_mat, ctx->ld,
+                                                                      (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols,
+                                                                      pow2, rg, approx, ctx->d_plane);
+    }
   } else if (ctx->store == EBIC_STORE_F32) {
     EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ebic::build_plane_kernel<float><<<grid, 256, smem, s>>>((const float*)ctx->d_mat, ctx->ld, (uint32_t)ctx->n_rows,

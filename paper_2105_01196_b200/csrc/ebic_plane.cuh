@@ -181,92 +181,80 @@ __device__ __forceinline__ uint32_t eval_fixed(uint32_t lane_base, const uint4& 
 }
 
 // ---------------------------------------------------------------------------
-// plane builder, fast path: float32 store, C <= 32*E.  One WARP per row: the
-// row is sorted in registers (E consecutive elements per lane, bitonic network
-// -- in-lane stages on registers, cross-lane stages with __shfl_xor_sync, no
-// block barriers), written once to a per-warp shared buffer, then R and T come
-// from two binary searches per element exactly as in build_plane_kernel.
-// Sort keys are the order-preserving unsigned images of the floats; the
-// searches compare the floats themselves (so -0.0 == +0.0 as in the reference).
+// plane builder, row-tile version (the default): a CTA owns RG consecutive rows
+// (one warp per row).  The tile is read from the column-major store with RG
+// consecutive rows per column -- one full 32-B sector per column at RG = 8, f32
+// (a warp reading a single row would touch one sector per ELEMENT) -- sorted
+// per row with a warp-level bitonic network in shared memory (__syncwarp only),
+// searched exactly like build_plane_kernel, and written back the same way.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t f2key(float f) {
-  const uint32_t b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float key2f(uint32_t k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
-}
-
-constexpr int kPlaneWarps = 8;
-
-template <int E>
-__global__ void __launch_bounds__(kPlaneWarps * 32)
-build_plane_warp_kernel(const float* __restrict__ store, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
-                        double approx, uint32_t* __restrict__ plane) {
-  __shared__ float s_sorted[kPlaneWarps][32 * E];
+template <typename T>
+__global__ void __launch_bounds__(256)
+build_plane_tile_kernel(const T* __restrict__ store, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
+                        uint32_t pow2, uint32_t rg, double approx, uint32_t* __restrict__ plane) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t cp = n_cols + 1;                              // padded tile row (bank spread)
+  T* s_val = reinterpret_cast<T*>(smem_raw);                   // [rg][cp] values, then plane words
+  T* s_srt = s_val + (size_t)rg * cp;                          // [rg][pow2] sorted values
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* srt = s_sorted[warp];
-  for (uint32_t row = blockIdx.x * kPlaneWarps + warp; row < n_rows; row += gridDim.x * kPlaneWarps) {
-    uint32_t k[E];
-#pragma unroll
-    for (int j = 0; j < E; ++j) {
-      const uint32_t c = lane * E + j;
-      k[j] = c < n_cols ? f2key(store[(uint64_t)c * ld + row]) : 0xFFFFFFFFu;
+  const uint32_t n_groups = (n_rows + rg - 1) / rg;
+  for (uint32_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const uint32_t row0 = grp * rg;
+    // 1. tile load: consecutive threads read consecutive rows of a column
+    for (uint32_t t = threadIdx.x; t < rg * n_cols; t += blockDim.x) {
+      const uint32_t c = t / rg, r = t % rg;
+      s_val[r * cp + c] = row0 + r < n_rows ? store[(uint64_t)c * ld + row0 + r] : (T)0;
     }
-    // bitonic sort of N = 32E keys; element g = lane*E + j
-#pragma unroll
-    for (int kk = 2; kk <= 32 * E; kk <<= 1) {
-#pragma unroll
-      for (int d = kk >> 1; d > 0; d >>= 1) {
-        if (d < E) {
-#pragma unroll
-          for (int j = 0; j < E; ++j) {
-            if ((j & d) == 0) {
-              const uint32_t g = lane * E + j;
-              const bool up = (g & kk) == 0;
-              const uint32_t a = k[j], b = k[j ^ d];
-              const uint32_t lo = min(a, b), hi = max(a, b);
-              k[j] = up ? lo : hi;
-              k[j ^ d] = up ? hi : lo;
+    __syncthreads();
+    for (uint32_t w = warp; w < rg; w += blockDim.x / 32) {
+      T* v = s_val + (size_t)w * cp;
+      T* srt = s_srt + (size_t)w * pow2;
+      // 2. warp bitonic sort (ascending), padding +inf
+      for (uint32_t j = lane; j < pow2; j += 32) srt[j] = j < n_cols ? v[j] : (T)INFINITY;
+      __syncwarp();
+      for (uint32_t k = 2; k <= pow2; k <<= 1) {
+        for (uint32_t d = k >> 1; d > 0; d >>= 1) {
+          for (uint32_t i = lane; i < pow2 / 2; i += 32) {
+            const uint32_t a = ((i & ~(d - 1)) << 1) | (i & (d - 1));  // lower index of the i-th pair
+            const uint32_t b = a | d;
+            const T x = srt[a], y = srt[b];
+            if ((x > y) == ((a & k) == 0)) {
+              srt[a] = y;
+              srt[b] = x;
             }
           }
-        } else {
-          const int lx = d / E;
-          const bool lower = (lane & lx) == 0;
-#pragma unroll
-          for (int j = 0; j < E; ++j) {
-            const uint32_t g = lane * E + j;
-            const bool up = (g & kk) == 0;
-            const uint32_t o = __shfl_xor_sync(kFull, k[j], lx);
-            k[j] = (lower == up) ? min(k[j], o) : max(k[j], o);
-          }
+          __syncwarp();
         }
       }
-    }
-#pragma unroll
-    for (int j = 0; j < E; ++j) {
-      const uint32_t c = lane * E + j;
-      if (c < n_cols) srt[c] = key2f(k[j]);
-    }
-    __syncwarp();
-    for (uint32_t c = lane; c < n_cols; c += 32) {
-      const float v = store[(uint64_t)c * ld + row];
-      uint32_t lo = 0, hi = n_cols;  // lower_bound: #values < v
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (srt[mid] < v) lo = mid + 1; else hi = mid;
+      // 3. exact ranks: R = 1 + lower_bound(v), T = upper_bound(thr64(v))
+      for (uint32_t c = lane; c < n_cols; c += 32) {
+        const T x = v[c];
+        uint32_t lo = 0, hi = n_cols;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (srt[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        const uint32_t rank1 = lo + 1;
+        const double t = thr64((double)x, approx);
+        lo = 0;
+        hi = n_cols;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if ((double)srt[mid] <= t) lo = mid + 1; else hi = mid;
+        }
+        // the plane word replaces the value in place (low 32 bits of the element;
+        // each element is read, then overwritten, by the same lane)
+        *reinterpret_cast<uint32_t*>(&v[c]) = (rank1 << 16) | lo;
       }
-      const uint32_t rank1 = lo + 1;
-      const double t = thr64((double)v, approx);  // upper_bound: #values <= thr(v)
-      lo = 0;
-      hi = n_cols;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if ((double)srt[mid] <= t) lo = mid + 1; else hi = mid;
-      }
-      plane[(uint64_t)c * ld + row] = (rank1 << 16) | lo;
     }
-    __syncwarp();
+    __syncthreads();
+    // 4. coalesced write-back of the plane words
+    for (uint32_t t = threadIdx.x; t < rg * n_cols; t += blockDim.x) {
+      const uint32_t c = t / rg, r = t % rg;
+      if (row0 + r < n_rows)
+        plane[(uint64_t)c * ld + row0 + r] = *reinterpret_cast<const uint32_t*>(&s_val[(size_t)r * cp + c]);
+    }
+    __syncthreads();
   }
 }
 

@@ -385,28 +385,31 @@ def test_wide_matrices_every_slab_variant(path_evaluator, n_cols):
         np.testing.assert_array_equal(got, want, err_msg=f"C={n_cols} approx={approx} neg={neg}")
 
 
-@pytest.mark.parametrize("n_cols", [2, 33, 64, 65, 200, 511, 1000, 1024])
-def test_warp_plane_builder_equals_block_builder(n_cols, monkeypatch):
-    """The warp-per-row register-sort plane builder (f32, C <= 1024) gives the
-    same counts as the block bitonic builder, on rows full of ties, signed
-    zeros, subnormals and huge values."""
+@pytest.mark.parametrize("n_cols", [2, 33, 64, 65, 200, 511, 1000, 1024, 2000, 3000])
+@pytest.mark.parametrize("f64", [False, True])
+def test_plane_builders_agree(n_cols, f64, monkeypatch):
+    """The row-tile plane builder (default) and the per-row block-sort builder
+    give identical counts -- on rows full of ties, signed zeros, subnormals and
+    huge values, for f32 and f64 stores."""
     from paper_2105_01196_b200 import Evaluator
 
     rng = np.random.default_rng(n_cols)
     vals = np.array([0.0, -0.0, 1e-45, -1e-45, 1.0, 1.0, -1.0, 3.4e38, -3.4e38, 0.97, 1.03], dtype=np.float32)
     m = np.where(rng.random((777, n_cols)) < 0.5, rng.choice(vals, size=(777, n_cols)),
-                 rng.standard_normal((777, n_cols)).astype(np.float32)).astype(np.float32)
+                 rng.standard_normal((777, n_cols)).astype(np.float32)).astype(np.float64)
+    if f64:
+        m = m + rng.standard_normal(m.shape) * 1e-9  # not float32-representable: f64 store
     seqs = [rng.choice(n_cols, size=int(rng.integers(1, min(n_cols, 7) + 1)), replace=False) for _ in range(400)]
     pop = Population.from_sequences(seqs)
+    settings = ((0.0, True), (0.03, False), (0.5, True))
     results = []
     for builder in ("0", "1"):
         monkeypatch.setenv("EBIC_PLANE_BUILDER", builder)
         with Evaluator(0) as ev:
-            ev.upload(m)
+            assert ev.upload(m) == (EBIC_STORE_F64 if f64 else EBIC_STORE_F32)
             ev.set_path(EBIC_PATH_PLANE)
-            results.append([ev.evaluate_population(pop, TrendParams(a, neg)) for a, neg in
-                            ((0.0, True), (0.03, False), (0.5, True))])
-    for got_warp, got_block, (a, neg) in zip(results[0], results[1], ((0.0, True), (0.03, False), (0.5, True))):
+            results.append([ev.evaluate_population(pop, TrendParams(a, neg)) for a, neg in settings])
+    for got_tile, got_block, (a, neg) in zip(results[0], results[1], settings):
         want = oracle.evaluate_population(m, pop.cols, pop.offsets, a, neg)
-        np.testing.assert_array_equal(got_warp, want)
+        np.testing.assert_array_equal(got_tile, want)
         np.testing.assert_array_equal(got_block, want)
