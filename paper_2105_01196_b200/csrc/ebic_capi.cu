@@ -204,19 +204,20 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   const size_t tile_smem = (size_t)rg * ((ctx->n_cols + 1) + pow2) * esz;
   if (ctx->plane_builder != 1 && tile_smem <= 200 * 1024) {
     const unsigned g = (unsigned)std::min<uint64_t>((ctx->n_rows + rg - 1) / rg, (uint64_t)ctx->n_sms * 16);
-    if (ctx->store == EBIC_STORE_F32) {
-      EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_tile_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_smem));
-      ebic::build_plane_tile_kernel<float><<<g, 256, tile_smem, s>>>((const float*)ctx->d_mat, ctx->ld,
-                                                                     (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols,
-                                                                     pow2, rg, approx, ctx->d_plane);
-    } else {
-      EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_tile_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)tile_smem));
-      ebic::build_plane_tile_kernel<double><<<g, 256, tile_smem, s>>>((const double*)ctx->d_mat, ctx->ld,
-                                                                      (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols,
-                                                                      pow2, rg, approx, ctx->d_plane);
-    }
+    const uint32_t R = (uint32_t)ctx->n_rows, C = (uint32_t)ctx->n_cols;
+    auto go = [&](auto kern, const auto* st) -> int {
+      EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+      kern<<<g, 256, tile_smem, s>>>(st, ctx->ld, R, C, pow2, rg, approx, ctx->d_plane);
+      return EBIC_OK;
+    };
+    const float* sf = (const float*)ctx->d_mat;
+    if (ctx->store != EBIC_STORE_F32) EBIC_TRY(go(ebic::build_plane_tile_kernel<double, 0>, (const double*)ctx->d_mat));
+    else if (C <= 64) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 2>, sf));
+    else if (C <= 128) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 4>, sf));
+    else if (C <= 256) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 8>, sf));
+    else if (C <= 512) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 16>, sf));
+    else if (C <= 1024) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 32>, sf));
+    else EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 0>, sf));
   } else if (ctx->store == EBIC_STORE_F32) {
     EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ebic::build_plane_kernel<float><<<grid, 256, smem, s>>>((const float*)ctx->d_mat, ctx->ld, (uint32_t)ctx->n_rows,

@@ -188,7 +188,50 @@ __device__ __forceinline__ uint32_t eval_fixed(uint32_t lane_base, const uint4& 
 // per row with a warp-level bitonic network in shared memory (__syncwarp only),
 // searched exactly like build_plane_kernel, and written back the same way.
 // ---------------------------------------------------------------------------
-template <typename T>
+// Order-preserving unsigned image of a float (sort key) and back.
+__device__ __forceinline__ uint32_t f2key(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// Warp bitonic sort of 32*E keys held E per lane (element g = lane*E + j):
+// in-lane stages on registers, cross-lane stages with __shfl_xor_sync.
+template <int E>
+__device__ __forceinline__ void warp_register_sort(uint32_t (&k)[E], int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32 * E; kk <<= 1) {
+#pragma unroll
+    for (int d = kk >> 1; d > 0; d >>= 1) {
+      if (d < E) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          if ((j & d) == 0) {
+            const bool up = ((lane * E + j) & kk) == 0;
+            const uint32_t a = k[j], b = k[j ^ d];
+            k[j] = up ? min(a, b) : max(a, b);
+            k[j ^ d] = up ? max(a, b) : min(a, b);
+          }
+        }
+      } else {
+        const int lx = d / E;
+        const bool lower = (lane & lx) == 0;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const bool up = ((lane * E + j) & kk) == 0;
+          const uint32_t o = __shfl_xor_sync(kFull, k[j], lx);
+          k[j] = (lower == up) ? min(k[j], o) : max(k[j], o);
+        }
+      }
+    }
+  }
+}
+
+// E == 0: warp-level shared-memory bitonic sort (any C, f32 or f64);
+// E > 0 : float32 rows with C <= 32*E sorted in registers (warp_register_sort).
+template <typename T, int E>
 __global__ void __launch_bounds__(256)
 build_plane_tile_kernel(const T* __restrict__ store, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
                         uint32_t pow2, uint32_t rg, double approx, uint32_t* __restrict__ plane) {
@@ -209,21 +252,37 @@ build_plane_tile_kernel(const T* __restrict__ store, uint64_t ld, uint32_t n_row
     for (uint32_t w = warp; w < rg; w += blockDim.x / 32) {
       T* v = s_val + (size_t)w * cp;
       T* srt = s_srt + (size_t)w * pow2;
-      // 2. warp bitonic sort (ascending), padding +inf
-      for (uint32_t j = lane; j < pow2; j += 32) srt[j] = j < n_cols ? v[j] : (T)INFINITY;
-      __syncwarp();
-      for (uint32_t k = 2; k <= pow2; k <<= 1) {
-        for (uint32_t d = k >> 1; d > 0; d >>= 1) {
-          for (uint32_t i = lane; i < pow2 / 2; i += 32) {
-            const uint32_t a = ((i & ~(d - 1)) << 1) | (i & (d - 1));  // lower index of the i-th pair
-            const uint32_t b = a | d;
-            const T x = srt[a], y = srt[b];
-            if ((x > y) == ((a & k) == 0)) {
-              srt[a] = y;
-              srt[b] = x;
+      // 2. sort the row (ascending, padding +inf) into srt
+      if constexpr (E > 0) {
+        uint32_t key[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const uint32_t c = lane * E + j;
+          key[j] = c < n_cols ? f2key((float)v[c]) : 0xFFFFFFFFu;
+        }
+        warp_register_sort<E>(key, lane);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const uint32_t c = lane * E + j;
+          if (c < n_cols) srt[c] = (T)key2f(key[j]);
+        }
+        __syncwarp();
+      } else {
+        for (uint32_t j = lane; j < pow2; j += 32) srt[j] = j < n_cols ? v[j] : (T)INFINITY;
+        __syncwarp();
+        for (uint32_t k = 2; k <= pow2; k <<= 1) {
+          for (uint32_t d = k >> 1; d > 0; d >>= 1) {
+            for (uint32_t i = lane; i < pow2 / 2; i += 32) {
+              const uint32_t a = ((i & ~(d - 1)) << 1) | (i & (d - 1));  // lower index of the i-th pair
+              const uint32_t b = a | d;
+              const T x = srt[a], y = srt[b];
+              if ((x > y) == ((a & k) == 0)) {
+                srt[a] = y;
+                srt[b] = x;
+              }
             }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
       // 3. exact ranks: R = 1 + lower_bound(v), T = upper_bound(thr64(v))
