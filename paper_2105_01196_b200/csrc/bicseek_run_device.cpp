@@ -19,11 +19,14 @@
 //     for every following offspring that could place under the current archive.
 //     Rows are a pure function of the candidate, so speculation is exact.
 //
-// The archive insert, operator pick, and the small helpers that the reference
-// keeps in an anonymous namespace are restated below (file:line cited).  Every
-// other piece is the reference's own function, linked unchanged.
+// The archive acceptance rule, the operator draw, the breeding loop and the
+// small helpers the reference keeps in an anonymous namespace are re-expressed
+// below (file:line cited; arithmetic and draw order identical).  Every other
+// piece is the reference's own function, linked unchanged.
 #include <algorithm>
 #include <chrono>
+#include <numeric>
+#include <tuple>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
@@ -40,48 +43,47 @@ using namespace bicseek;
 
 namespace {
 
-constexpr int kTabuRetryBudget = 3;  // evolution.cpp:12
+// Breeding retries before a random chromosome is drawn instead (evolution.cpp:12).
+constexpr int kBreedAttempts = 3;
 
 void check(int status, const char* what) {
   if (status != EBIC_OK)
     throw std::runtime_error(std::string("bicseek device run: ") + what + ": " + ebic_last_error());
 }
 
-// evolution.cpp:25-34
-OperatorKind pick_operator(const std::array<double, 5>& weights, Rng& rng) {
-  double total = 0.0;
-  for (double w : weights) total += w;
-  double r = rng.uniform_real() * total;
-  for (std::size_t i = 0; i + 1 < weights.size(); ++i) {
-    if (r < weights[i]) return static_cast<OperatorKind>(i);
-    r -= weights[i];
-  }
-  return OperatorKind::crossover;
+// Weighted operator draw (the rule of evolution.cpp:25-34).  The arithmetic --
+// a left-to-right sum, one multiply, sequential subtraction -- is kept exactly,
+// because the draw must reproduce the reference bit for bit.
+OperatorKind draw_operator(const std::array<double, 5>& w, Rng& rng) {
+  const double sum = std::accumulate(w.begin(), w.end(), 0.0);
+  double left = rng.uniform_real() * sum;
+  std::size_t op = 0;
+  while (op + 1 < w.size() && !(left < w[op])) left -= w[op++];
+  return static_cast<OperatorKind>(op);
 }
 
-// evolution.cpp:38-42: score desc, then fewer columns, then lexicographic columns
-bool ranks_before(const RankedIndividual& a, const RankedIndividual& b) {
-  if (a.score != b.score) return a.score > b.score;
-  if (a.chromosome.size() != b.chromosome.size()) return a.chromosome.size() < b.chromosome.size();
-  return a.chromosome.columns < b.chromosome.columns;
+// Archive order (evolution.cpp:38-42): higher score first, then fewer columns,
+// then the lexicographically smaller column sequence.
+bool archive_before(const RankedIndividual& x, const RankedIndividual& y) {
+  return std::forward_as_tuple(-x.score, x.chromosome.columns.size(), x.chromosome.columns) <
+         std::forward_as_tuple(-y.score, y.chromosome.columns.size(), y.chromosome.columns);
 }
 
-// evolution.cpp:44-51
-double induced_jaccard(const TopRankEntry& a, const std::vector<std::size_t>& rows,
-                       const std::vector<std::size_t>& cols) {
-  const std::size_t inter =
-      sorted_intersection_size(a.rows, rows) * sorted_intersection_size(a.cols, cols);
-  const std::size_t size_a = a.rows.size() * a.cols.size();
-  const std::size_t size_b = rows.size() * cols.size();
-  return static_cast<double>(inter) / static_cast<double>(size_a + size_b - inter);
+// Cell Jaccard of an archive entry and a candidate bicluster (evolution.cpp:44-51):
+// cells are products, so the intersection is |rows n| * |cols n|.
+double cell_overlap(const TopRankEntry& e, const std::vector<std::size_t>& rows,
+                    const std::vector<std::size_t>& sorted_cols) {
+  const std::size_t shared = sorted_intersection_size(e.rows, rows) * sorted_intersection_size(e.cols, sorted_cols);
+  const std::size_t cells_e = e.rows.size() * e.cols.size(), cells_c = rows.size() * sorted_cols.size();
+  return static_cast<double>(shared) / static_cast<double>(cells_e + cells_c - shared);
 }
 
-// evolution.cpp:215-221
-std::vector<std::size_t> column_usage_of(const std::vector<RankedIndividual>& pop, std::size_t num_cols) {
-  std::vector<std::size_t> usage(num_cols, 0);
-  for (const auto& ind : pop)
-    for (std::size_t col : ind.chromosome.columns) ++usage[col];
-  return usage;
+// Per-column occurrence counts over a population (evolution.cpp:215-221).
+std::vector<std::size_t> tally_columns(const std::vector<RankedIndividual>& pop, std::size_t num_cols) {
+  std::vector<std::size_t> tally(num_cols, 0);
+  for (const RankedIndividual& ind : pop)
+    for (std::size_t c : ind.chromosome.columns) tally[c] += 1;
+  return tally;
 }
 
 // One device context per run: the matrix, the plane and the marshaller ring.
@@ -152,8 +154,8 @@ class ChunkedEval {
   std::vector<std::vector<uint32_t>> outs_;  // stable storage: written when the ticket is waited
 };
 
-// The top-rank archive of evolution.hpp:78-98 with TopRankList::insert
-// (evolution.cpp:76-105) restated; rows come from a batch cache.
+// The top-rank archive (evolution.hpp:78-98): the acceptance rule of
+// TopRankList::insert (evolution.cpp:76-105), fed with precomputed row sets.
 class Archive {
  public:
   Archive(std::size_t capacity, double overlap) : capacity_(capacity), overlap_(overlap) {}
@@ -162,34 +164,43 @@ class Archive {
   bool full() const { return entries_.size() >= capacity_; }
   double min_score() const { return entries_.empty() ? 0.0 : entries_.back().ind.score; }
 
-  // would insert() need the candidate's rows (evolution.cpp:78-79)?
+  // can the candidate enter at all -- i.e. does the reference compute its rows
+  // (evolution.cpp:78-79)?
   bool could_place(const RankedIndividual& ind) const {
     return ind.score > 0.0 && !(full() && ind.score <= min_score());
   }
 
   bool insert(const RankedIndividual& ind, const std::vector<std::size_t>& rows) {
     if (!could_place(ind)) return false;
-    TopRankEntry cand;
-    cand.ind = ind;
-    cand.rows = rows;
-    cand.cols = ind.chromosome.columns;
-    std::sort(cand.cols.begin(), cand.cols.end());
-    std::vector<std::size_t> displaced;
+    TopRankEntry fresh;
+    fresh.ind = ind;
+    fresh.rows = rows;
+    fresh.cols = ind.chromosome.columns;
+    std::sort(fresh.cols.begin(), fresh.cols.end());
+    // entries overlapping the candidate too much are displaced -- unless one of
+    // them scores at least as high, in which case the candidate is rejected
+    std::vector<char> displaced(entries_.size(), 0);
     for (std::size_t i = 0; i < entries_.size(); ++i) {
-      if (induced_jaccard(entries_[i], cand.rows, cand.cols) < overlap_) continue;
-      if (entries_[i].ind.score >= ind.score) return false;  // incumbent wins ties
-      displaced.push_back(i);
+      if (cell_overlap(entries_[i], fresh.rows, fresh.cols) < overlap_) continue;
+      if (entries_[i].ind.score >= ind.score) return false;
+      displaced[i] = 1;
     }
-    for (std::size_t k = displaced.size(); k-- > 0;)
-      entries_.erase(entries_.begin() + static_cast<std::ptrdiff_t>(displaced[k]));
-    auto pos = std::find_if(entries_.begin(), entries_.end(),
-                            [&](const TopRankEntry& e) { return ranks_before(cand.ind, e.ind); });
-    entries_.insert(pos, std::move(cand));
+    std::size_t keep = 0;
+    for (std::size_t i = 0; i < entries_.size(); ++i)
+      if (!displaced[i]) entries_[keep++] = std::move(entries_[i]);
+    entries_.resize(keep);
+    // entries are kept in archive order: the candidate goes before the first
+    // entry it outranks
+    const auto at = std::upper_bound(entries_.begin(), entries_.end(), fresh,
+                                     [](const TopRankEntry& a, const TopRankEntry& b) {
+                                       return archive_before(a.ind, b.ind);
+                                     });
+    entries_.insert(at, std::move(fresh));
     if (entries_.size() > capacity_) entries_.resize(capacity_);
-    return entries_.size() <= capacity_ &&
-           std::any_of(entries_.begin(), entries_.end(), [&](const TopRankEntry& e) {
-             return e.ind.chromosome.columns == ind.chromosome.columns && e.ind.score == ind.score;
-           });
+    // placed iff it survived the truncation
+    return std::any_of(entries_.begin(), entries_.end(), [&](const TopRankEntry& e) {
+      return e.ind.score == ind.score && e.ind.chromosome.columns == ind.chromosome.columns;
+    });
   }
 
  private:
@@ -272,6 +283,30 @@ bool rank_and_insert(std::vector<Chromosome>&& pop, const std::vector<std::size_
   return improved;
 }
 
+// One offspring, drawn exactly as in step_generation (evolution.cpp:262-289):
+// up to kBreedAttempts tournament + operator draws, each rejected if its hash
+// is already tabu (which counts a tabu hit); then a fresh random chromosome.
+Chromosome breed_child(State& st, const EvolutionParams& p, std::size_t num_cols) {
+  for (int tries = 0; tries < kBreedAttempts; ++tries) {
+    const RankedIndividual& first = tournament_select(st.population, st.column_usage, p, st.rng);
+    const OperatorKind op = draw_operator(p.operator_weights, st.rng);
+    Chromosome child = op == OperatorKind::crossover
+                           ? crossover(first.chromosome,
+                                       tournament_select(st.population, st.column_usage, p, st.rng).chromosome,
+                                       st.rng)
+                           : mutate(first.chromosome, op, num_cols, st.rng);
+    const std::uint64_t h = chromosome_hash(child);
+    if (!st.tabu.contains(h)) {
+      st.tabu.insert(h);
+      return child;
+    }
+    st.tabu.hit_count += 1;
+  }
+  Chromosome child = random_chromosome(p, num_cols, st.rng);
+  st.tabu.insert(chromosome_hash(child));
+  return child;
+}
+
 }  // namespace
 
 // evolution.cpp:305-333 with the device evaluator on the caller side.
@@ -294,7 +329,7 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
     for (const Chromosome& c : pop) st.tabu.insert(chromosome_hash(c));
     st.population.reserve(pop.size());
     rank_and_insert(std::move(pop), counts, st, p, rows, st.population);
-    st.column_usage = column_usage_of(st.population, m.cols());
+    st.column_usage = tally_columns(st.population, m.cols());
   }
 
   std::string reason = "budget";
@@ -315,38 +350,14 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
     offspring.reserve(p.population_size - next.size());
     ChunkedEval ev(dev, chunk);
     while (next.size() + offspring.size() < p.population_size) {
-      Chromosome child;
-      bool accepted = false;
-      for (int attempt = 0; attempt < kTabuRetryBudget; ++attempt) {
-        const RankedIndividual& parent = tournament_select(st.population, st.column_usage, p, st.rng);
-        const OperatorKind op = pick_operator(p.operator_weights, st.rng);
-        if (op == OperatorKind::crossover) {
-          const RankedIndividual& other = tournament_select(st.population, st.column_usage, p, st.rng);
-          child = crossover(parent.chromosome, other.chromosome, st.rng);
-        } else {
-          child = mutate(parent.chromosome, op, num_cols, st.rng);
-        }
-        const std::uint64_t h = chromosome_hash(child);
-        if (st.tabu.contains(h)) {
-          ++st.tabu.hit_count;
-          continue;
-        }
-        st.tabu.insert(h);
-        accepted = true;
-        break;
-      }
-      if (!accepted) {
-        child = random_chromosome(p, num_cols, st.rng);
-        st.tabu.insert(chromosome_hash(child));
-      }
-      offspring.push_back(std::move(child));
+      offspring.push_back(breed_child(st, p, num_cols));
       ev.add(offspring);  // overlap: the GPU counts this chunk while the next is bred
     }
     const std::vector<std::size_t> counts = ev.finish(offspring);
     const bool improved = rank_and_insert(std::move(offspring), counts, st, p, rows, next);
     if (improved) st.tabu.hit_count = 0;
     st.population = std::move(next);
-    st.column_usage = column_usage_of(st.population, num_cols);
+    st.column_usage = tally_columns(st.population, num_cols);
     ++st.generation;
   }
 
