@@ -186,8 +186,11 @@ class Archive {
       displaced[i] = 1;
     }
     std::size_t keep = 0;
-    for (std::size_t i = 0; i < entries_.size(); ++i)
-      if (!displaced[i]) entries_[keep++] = std::move(entries_[i]);
+    for (std::size_t i = 0; i < entries_.size(); ++i) {
+      if (displaced[i]) continue;
+      if (keep != i) entries_[keep] = std::move(entries_[i]);  // (no self-move)
+      ++keep;
+    }
     entries_.resize(keep);
     // entries are kept in archive order: the candidate goes before the first
     // entry it outranks
