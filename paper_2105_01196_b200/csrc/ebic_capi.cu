@@ -217,6 +217,7 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
     else if (C <= 256) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 8>, sf));
     else if (C <= 512) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 16>, sf));
     else if (C <= 1024) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 32>, sf));
+    else if (C <= 2048) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 64>, sf));
     else EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 0>, sf));
   } else if (ctx->store == EBIC_STORE_F32) {
     EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
