@@ -134,7 +134,7 @@ struct ebic_ctx {
   int n_sms = 148;
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
-  int plane_builder = 0;  // 0 auto (row-tile builder), 1 force the per-row block-sort builder (EBIC_PLANE_BUILDER=1)
+  int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
 };
 
 namespace {
@@ -198,11 +198,15 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   const size_t esz = ctx->store == EBIC_STORE_F32 ? sizeof(float) : sizeof(double);
   const size_t smem = pow2 * esz;
   const unsigned grid = (unsigned)std::min<uint64_t>(ctx->n_rows, (uint64_t)ctx->n_sms * 8);
-  // row-tile builder: RG rows per CTA (8 when they fit in ~96 KB of shared memory)
+  // Row-tile builder (RG rows per CTA, register sort) for f32 rows of <= 1024
+  // columns; otherwise the per-row block builder -- measured faster than the
+  // warp-level shared-memory sort for wide or f64 rows (C4: 22.7 vs 26.8 ms).
   uint32_t rg = 8;
   while (rg > 1 && (size_t)rg * ((ctx->n_cols + 1) + pow2) * esz > 96 * 1024) rg >>= 1;
   const size_t tile_smem = (size_t)rg * ((ctx->n_cols + 1) + pow2) * esz;
-  if (ctx->plane_builder != 1 && tile_smem <= 200 * 1024) {
+  const bool tile = ctx->plane_builder == 2 || (ctx->plane_builder == 0 && ctx->store == EBIC_STORE_F32 &&
+                                                ctx->n_cols <= 1024);
+  if (tile && tile_smem <= 200 * 1024) {
     const unsigned g = (unsigned)std::min<uint64_t>((ctx->n_rows + rg - 1) / rg, (uint64_t)ctx->n_sms * 16);
     const uint32_t R = (uint32_t)ctx->n_rows, C = (uint32_t)ctx->n_cols;
     auto go = [&](auto kern, const auto* st) -> int {
@@ -217,7 +221,6 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
     else if (C <= 256) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 8>, sf));
     else if (C <= 512) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 16>, sf));
     else if (C <= 1024) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 32>, sf));
-    else if (C <= 2048) EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 64>, sf));
     else EBIC_TRY(go(ebic::build_plane_tile_kernel<float, 0>, sf));
   } else if (ctx->store == EBIC_STORE_F32) {
     EBIC_CUDA(cudaFuncSetAttribute(ebic::build_plane_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

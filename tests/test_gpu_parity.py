@@ -388,9 +388,9 @@ def test_wide_matrices_every_slab_variant(path_evaluator, n_cols):
 @pytest.mark.parametrize("n_cols", [2, 33, 64, 65, 200, 511, 1000, 1024, 2000, 3000])
 @pytest.mark.parametrize("f64", [False, True])
 def test_plane_builders_agree(n_cols, f64, monkeypatch):
-    """The row-tile plane builder (default) and the per-row block-sort builder
-    give identical counts -- on rows full of ties, signed zeros, subnormals and
-    huge values, for f32 and f64 stores."""
+    """The row-tile plane builder (register or warp shared-memory sort) and the
+    per-row block-sort builder give identical counts -- on rows full of ties,
+    signed zeros, subnormals and huge values, for f32 and f64 stores."""
     from paper_2105_01196_b200 import Evaluator
 
     rng = np.random.default_rng(n_cols)
@@ -403,7 +403,7 @@ def test_plane_builders_agree(n_cols, f64, monkeypatch):
     pop = Population.from_sequences(seqs)
     settings = ((0.0, True), (0.03, False), (0.5, True))
     results = []
-    for builder in ("0", "1"):
+    for builder in ("2", "1"):
         monkeypatch.setenv("EBIC_PLANE_BUILDER", builder)
         with Evaluator(0) as ev:
             assert ev.upload(m) == (EBIC_STORE_F64 if f64 else EBIC_STORE_F32)
