@@ -98,8 +98,11 @@ int ebic_matrix_free(ebic_ctx* ctx);
 /* ---- fitness counts (reference: evaluate_population, trend.cpp:56-72) ---- */
 
 /* Host pointers, synchronous.  counts_out[i] = number of rows r of the
- * resident matrix (shard) with row_supports(r, candidate i).  Validates every
- * column index and candidate length (>= 1) on the host before launching. */
+ * resident matrix (shard) with row_supports(r, candidate i).  Offsets are
+ * validated on the host, column indices on the device (an out-of-range column
+ * returns EBIC_ERR_INVALID_ARGUMENT; that candidate's count is 0).  If all
+ * three arrays are page-locked (cudaHostAlloc / cudaHostRegister / torch
+ * pin_memory) they are DMA'd directly, with no staging copy. */
 int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
                      uint64_t n_cand, double approx, int negative_trends, uint32_t* counts_out);
 

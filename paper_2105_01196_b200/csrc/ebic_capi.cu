@@ -812,8 +812,48 @@ int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket) {
   return wait_slot(ctx, sl);
 }
 
+namespace {
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
 int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
                      double approx, int negative_trends, uint32_t* counts_out) {
+  // Zero-copy when the caller's arrays are already page-locked (cudaHostAlloc /
+  // cudaHostRegister / torch pin_memory): DMA straight from and into them.
+  // Otherwise go through the marshaller's pinned staging slots.
+  if (n_cand && ctx && ctx->d_mat && cols && offsets && counts_out && is_pinned(cols) && is_pinned(offsets) &&
+      is_pinned(counts_out)) {
+    EBIC_TRY(check_approx(approx));
+    EBIC_TRY(validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false));
+    EBIC_TRY(set_device(ctx));
+    const uint64_t n_idx = offsets[n_cand];
+    EBIC_TRY(ensure(ctx->d_tmp_cols, n_idx));
+    EBIC_TRY(ensure(ctx->d_tmp_offs, n_cand + 1));
+    EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
+    cudaStream_t s = ctx->stream;
+    EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
+    EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, cols, n_idx * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    EBIC_CUDA(cudaMemsetAsync(ctx->d_tmp_counts.p, 0, n_cand * sizeof(uint32_t), s));
+    EBIC_TRY(launch_count<false>(ctx, ctx->d_tmp_cols.p, ctx->d_tmp_offs.p, n_cand, approx, negative_trends,
+                                 ctx->d_tmp_counts.p, nullptr, s));
+    EBIC_CUDA(cudaMemcpyAsync(counts_out, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    int err = 0;
+    EBIC_CUDA(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EBIC_CUDA(cudaStreamSynchronize(s));
+    if (err) {
+      EBIC_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)));
+      return bad_column_error(ctx);
+    }
+    return EBIC_OK;
+  }
   uint64_t t = 0;
   EBIC_TRY(ebic_eval_submit(ctx, cols, offsets, n_cand, approx, negative_trends, counts_out, &t));
   return ebic_eval_wait(ctx, t);

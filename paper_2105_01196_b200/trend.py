@@ -190,11 +190,18 @@ class Evaluator:
         return {"rows": r.value, "cols": c.value, "ld": ld.value, "store": st.value, "row_base": rb.value}
 
     # -- evaluation --------------------------------------------------------
-    def evaluate_population(self, pop, params: TrendParams | None = None) -> np.ndarray:
-        """trend.cpp:56-72: uint32 support count per candidate (host arrays, synchronous)."""
+    def evaluate_population(self, pop, params: TrendParams | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        """trend.cpp:56-72: uint32 support count per candidate (host arrays, synchronous).
+
+        If the population arrays and `out` are page-locked (e.g. numpy views of
+        torch pin_memory tensors), the library DMAs them directly (no staging copy).
+        """
         p = params or TrendParams()
         pop = _as_population(pop)
-        out = np.zeros(len(pop), dtype=np.uint32)
+        if out is None:
+            out = np.zeros(len(pop), dtype=np.uint32)
+        elif out.dtype != np.uint32 or not out.flags.c_contiguous or out.size < len(pop):
+            raise ValueError("out must be a contiguous uint32 array of at least len(pop) elements")
         if len(pop) == 0:
             return out
         check(self._L.ebic_eval_counts(self._h, _ptr(pop.cols), _ptr(pop.offsets), len(pop),
