@@ -168,6 +168,15 @@ int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
 #define EBIC_PATH_PLANE_U32 3
 int ebic_ctx_set_path(ebic_ctx* ctx, int path);
 
+/* Packed-pair layout of the hot kernel: `rows_per_lane_pairs` (1 or 2) 16-bit
+ * row pairs per lane and `cands_per_warp` (1, 2 or 4) candidates per warp
+ * instruction; (0, 0) = auto ((2,1) for <= 256 columns, (1,2) for <= 1024,
+ * (1,4) for <= 2048: the fastest measured on B200).  A forced layout whose
+ * slab does not fit in shared memory falls back to the 32-bit-word plane
+ * kernel.  Every layout is bit-exact; the knob exists for cross-checking and
+ * benchmarking. */
+int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_per_warp);
+
 /* Build (or reuse) the rank plane of the resident matrix for `approx` now,
  * instead of lazily on the first evaluation with that approx.  The plane is a
  * per-(matrix, approx) index: a GA run uses one approx for all generations. */

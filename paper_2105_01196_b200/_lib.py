@@ -50,6 +50,7 @@ SIGNATURES = {
     "ebic_ctx_launch_count": (C.c_int, [_vp, _u64p]),
     "ebic_ctx_set_slab_rows": (C.c_int, [_vp, C.c_uint32]),
     "ebic_ctx_set_path": (C.c_int, [_vp, C.c_int]),
+    "ebic_ctx_set_pair_layout": (C.c_int, [_vp, C.c_int, C.c_int]),
     "ebic_matrix_prepare": (C.c_int, [_vp, C.c_double]),
 }
 

@@ -40,7 +40,7 @@ def _nvcc() -> str:
 
 
 def _sources():
-    return [CSRC / "ebic_capi.cu", CSRC / "ebic_kernels.cuh", REPO / "include" / "ebic.h"]
+    return [CSRC / "ebic_capi.cu", *sorted(CSRC.glob("*.cuh")), REPO / "include" / "ebic.h"]
 
 
 def needs_rebuild() -> bool:

@@ -20,6 +20,7 @@
 #include "ebic_kernels.cuh"
 #include "ebic_plane.cuh"
 #include "ebic_simd.cuh"
+#include "ebic_pair.cuh"
 
 namespace {
 
@@ -135,6 +136,9 @@ struct ebic_ctx {
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
+  int chunk_groups = 1;   // EBIC_CHUNK_GROUPS: slab_pair_kernel CTAs in per-chunk groups (1) or linear units (0)
+  int pair_kernel = 1;    // EBIC_PAIR_KERNEL: 1 position-indexed counts (slab_pair_kernel), 0 slab_simd_kernel (A/B)
+  int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
 };
 
 namespace {
@@ -240,6 +244,7 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
 
 struct SlabCfg {
   bool simd = false;  // packed 16-bit rank pairs (slab_simd_kernel); p = pair-words per lane
+  bool v2 = false;    // ... with position-indexed counts (slab_pair_kernel)
   int p = 1;
   int rpl = 1, sub = 1;
   uint32_t rt = 32;
@@ -258,11 +263,15 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
   const size_t kSlabCap = 128 * 1024;
   bool found = false;
   if (!mask && ctx->path != EBIC_PATH_PLANE_U32) {
-    // packed pairs: the largest slab (most rows per lane) that fits
-    struct Opt { int p, sub; uint32_t rt; };
+    // packed pairs: the first layout (in measured order of speed on B200, see
+    // profiles/r1_layout_ab.txt) whose slab fits in 128 KB.  The other
+    // layouts are reachable through ebic_ctx_set_pair_layout.
     // (P = 4 would need > 64 registers per thread at 1024 threads: spills)
-    const Opt opts[4] = {{2, 1, 128}, {1, 1, 64}, {1, 2, 32}, {1, 4, 16}};
-    for (const Opt& o : opts) {
+    struct Opt { int p, sub; uint32_t rt; };
+    const Opt opts[6] = {{2, 1, 128}, {1, 2, 32}, {1, 4, 16}, {2, 4, 32}, {2, 2, 64}, {1, 1, 64}};
+    for (int k = 0; k < 6; ++k) {
+      const Opt& o = opts[k];
+      if (ctx->simd_force ? ctx->simd_force != o.p * 16 + o.sub : k >= 3) continue;
       if (C * o.rt * 4 <= kSlabCap) {
         c.simd = true;
         c.p = o.p;
@@ -272,6 +281,20 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
         break;
       }
     }
+  }
+  if (found && ctx->pair_kernel) {
+    // slab_pair_kernel: per position a record (<= 16 B), a count and a slot; the
+    // (kClasses - 1) swept classes are each padded to the sweep stride
+    const size_t slab = C * c.rt * 4;
+    const size_t stride = (size_t)ebic::kSlabWarps * c.sub;
+    const size_t fixed = slab + (size_t)(ebic::kClasses - 1) * stride * ebic::kPairPosBytes + 16;
+    const uint64_t cmax = std::min<uint64_t>((budget - fixed) / ebic::kPairPosBytes, 16384);
+    const uint64_t n_chunks = (n_cand + cmax - 1) / cmax;
+    c.chunk = (uint32_t)((n_cand + n_chunks - 1) / n_chunks);
+    c.smem = fixed + (size_t)c.chunk * ebic::kPairPosBytes;
+    c.v2 = true;
+    c.ok = true;
+    return c;
   }
   if (found) {
     const size_t slab = C * c.rt * 4;
@@ -336,6 +359,7 @@ ebic::SlabArgs make_slab_args(const ebic_ctx* ctx, const SlabCfg& cfg, const uin
   // slabs).  Default: on iff the plane fits comfortably in the 126 MB L2.
   const uint64_t plane_bytes = ctx->ld * ctx->n_cols * 4;
   a.prefetch = ctx->prefetch >= 0 ? ctx->prefetch : (plane_bytes <= (96ull << 20) ? 1 : 0);
+  a.group = 0;
   return a;
 }
 
@@ -362,16 +386,21 @@ int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, con
 template <int P, int SUB, bool NEG>
 int launch_simd_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
                   uint64_t n_cand, uint32_t* d_counts, cudaStream_t s) {
-  auto kern = ebic::slab_simd_kernel<P, SUB, NEG>;
-  static std::atomic<uint64_t> attr_done{0};
+  auto kern = cfg.v2 ? ebic::slab_pair_kernel<P, SUB, NEG> : ebic::slab_simd_kernel<P, SUB, NEG>;
+  static std::atomic<uint64_t> attr_done[2] = {{0}, {0}};
   const uint64_t bit = 1ull << (ctx->device & 63);
-  if (!(attr_done.load(std::memory_order_relaxed) & bit)) {
+  if (!(attr_done[cfg.v2].load(std::memory_order_relaxed) & bit)) {
     EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ctx->smem_optin - 1024)));
-    attr_done.fetch_or(bit);
+    attr_done[cfg.v2].fetch_or(bit);
   }
   ebic::SlabArgs a = make_slab_args(ctx, cfg, d_cols, d_offs, n_cand, d_counts, nullptr);
   const uint64_t units = (uint64_t)a.n_chunks * a.n_slabs;
-  const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
+  unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
+  if (cfg.v2 && ctx->chunk_groups && a.n_chunks <= (uint32_t)ctx->n_sms) {
+    // chunk groups in step (a CTA per SM, up to n_sms % n_chunks SMs idle)
+    a.group = std::min<uint32_t>((uint32_t)ctx->n_sms / a.n_chunks, a.n_slabs);
+    grid = a.group * a.n_chunks;
+  }
   kern<<<grid, ebic::kSlabThreads, cfg.smem, s>>>(a);
   ctx->launches++;
   EBIC_CUDA(cudaGetLastError());
@@ -383,7 +412,11 @@ int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const
                 uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
   if constexpr (!MASK) {
     if (cfg.simd) {
-      if (cfg.p == 2) return launch_simd_t<2, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      if (cfg.p == 2) {
+        if (cfg.sub == 1) return launch_simd_t<2, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+        if (cfg.sub == 2) return launch_simd_t<2, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+        return launch_simd_t<2, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      }
       if (cfg.sub == 1) return launch_simd_t<1, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
       if (cfg.sub == 2) return launch_simd_t<1, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
       return launch_simd_t<1, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
@@ -629,6 +662,13 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (pb) ctx->plane_builder = std::atoi(pb);
     const char* pf = std::getenv("EBIC_PREFETCH");
     if (pf) ctx->prefetch = std::atoi(pf) ? 1 : 0;
+    const char* cg = std::getenv("EBIC_CHUNK_GROUPS");
+    if (cg) ctx->chunk_groups = std::atoi(cg) ? 1 : 0;
+    const char* pk = std::getenv("EBIC_PAIR_KERNEL");
+    if (pk) ctx->pair_kernel = std::atoi(pk) ? 1 : 0;
+    const char* sc = std::getenv("EBIC_PAIR_LAYOUT");
+    int fp = 0, fs = 0;
+    if (sc && std::sscanf(sc, "%d,%d", &fp, &fs) == 2) ctx->simd_force = fp * 16 + fs;
   }
   *ctx_out = ctx;
   return EBIC_OK;
@@ -965,6 +1005,20 @@ int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows) {
   if (slab_rows % ebic::kRowAlign)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "slab_rows must be a multiple of %u", ebic::kRowAlign);
   ctx->slab_rows = slab_rows;
+  return EBIC_OK;
+}
+
+int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_per_warp) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (rows_per_lane_pairs == 0 && cands_per_warp == 0) {
+    ctx->simd_force = 0;
+    return EBIC_OK;
+  }
+  const bool ok_p = rows_per_lane_pairs == 1 || rows_per_lane_pairs == 2;
+  const bool ok_s = cands_per_warp == 1 || cands_per_warp == 2 || cands_per_warp == 4;
+  if (!ok_p || !ok_s)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "bad packed-pair layout (%d, %d)", rows_per_lane_pairs, cands_per_warp);
+  ctx->simd_force = rows_per_lane_pairs * 16 + cands_per_warp;
   return EBIC_OK;
 }
 

@@ -137,6 +137,8 @@ struct SlabArgs {
   uint64_t mask_wpc;
   int* err;
   int prefetch;           // warm L2 with the next unit's slab (plane larger than L2)
+  uint32_t group;         // > 0: CTAs per chunk; CTA b sweeps one slab range of chunk b / group
+                          // (all chunk groups walk the plane in step: one DRAM pass); 0: linear units
 };
 
 // One consecutive-pair test on RPL rows: forward needs c > thr(p), reversed p > thr(c).

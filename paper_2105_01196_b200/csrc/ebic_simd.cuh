@@ -17,7 +17,8 @@
 //   SUB=1, P=1: RT = 64  (C <= 512)
 //   SUB=1, P=2: RT = 128 (C <= 256)
 // Shared memory: one line per column with the row pairs interleaved,
-// [Rg_0 NT_0 Rg_1 NT_1 ...] (4 B per element, the same footprint as the u32
+// [Rg_0 NT_0 Rg_1 NT_1 ...] at P=1, [Rg_0 Rg_1 NT_0 NT_1 ...] per lane at P=2
+// (see stage_pairs; 4 B per element, the same footprint as the u32
 // plane).  A lane fetches both words of its row pair(s) of a column with ONE
 // LDS.64 (P=1) / LDS.128 (P=2).  At SUB=2 each half-warp reads one whole,
 // aligned 128-B line per load: 2 wavefronts for 256 B, the minimum -- no bank
@@ -43,11 +44,27 @@ __device__ __forceinline__ uint32_t wget(const uint4& v, int q) { return q == 0 
 // D = Rg + NT (two rows at once); keep the guard bits 15/31
 __device__ __forceinline__ uint32_t sum2(uint32_t a, uint32_t b) { return (a + b) & 0x80008000u; }
 
+// A lane's slab words for one column: P = 1: (Rg, NT); P = 2: (Rg_0, Rg_1,
+// NT_0, NT_1) -- same-kind words adjacent, so that the first column of a
+// candidate (NT only) and the last (Rg only) are one aligned 8-byte LDS each
+// when ptxas narrows the 16-byte load, not two strided 4-byte ones (which
+// would cost twice the shared-memory wavefronts).
 // acc[q] &= Rg_q(rg_src) + NT_q(nt_src)
 template <int P, typename M, typename V>
 __device__ __forceinline__ void and_pair(M& acc, const V& rg_src, const V& nt_src) {
 #pragma unroll
-  for (int q = 0; q < P; ++q) wref(acc, q) &= sum2(wget(rg_src, 2 * q), wget(nt_src, 2 * q + 1));
+  for (int q = 0; q < P; ++q) wref(acc, q) &= sum2(wget(rg_src, q), wget(nt_src, P + q));
+}
+
+// Stage one uint4 of plane words (4 consecutive rows of a column) as slab
+// words: two row pairs (Rg, NT) per pair for P = 1, (Rg, Rg, NT, NT) for P = 2.
+template <int P>
+__device__ __forceinline__ uint4 stage_pairs(const uint4& w) {
+  const uint32_t rg0 = __byte_perm(w.x, w.y, 0x7632) | 0x80008000u;
+  const uint32_t nt0 = 0u - __byte_perm(w.x, w.y, 0x5410) - 0x00010001u;
+  const uint32_t rg1 = __byte_perm(w.z, w.w, 0x7632) | 0x80008000u;
+  const uint32_t nt1 = 0u - __byte_perm(w.z, w.w, 0x5410) - 0x00010001u;
+  return P == 1 ? make_uint4(rg0, nt0, rg1, nt1) : make_uint4(rg0, rg1, nt0, nt1);
 }
 
 template <int P, typename M>
@@ -223,11 +240,7 @@ slab_simd_kernel(const SlabArgs a) {
           const uint32_t t = t0 + k * blockDim.x;
           if (t < total) {
             const uint32_t c = t / Q, q = t % Q;
-            const uint4 v = make_uint4(__byte_perm(w[k].x, w[k].y, 0x7632) | 0x80008000u,
-                                       0u - __byte_perm(w[k].x, w[k].y, 0x5410) - 0x00010001u,
-                                       __byte_perm(w[k].z, w[k].w, 0x7632) | 0x80008000u,
-                                       0u - __byte_perm(w[k].z, w[k].w, 0x5410) - 0x00010001u);
-            *reinterpret_cast<uint4*>(s_slab + (size_t)c * CW + 4 * q) = v;
+            *reinterpret_cast<uint4*>(s_slab + (size_t)c * CW + 4 * q) = stage_pairs<P>(w[k]);
           }
         }
       }

@@ -153,6 +153,10 @@ class Evaluator:
         """EBIC_PATH_AUTO (rank-plane slab kernel when C <= 8192) / _VALUE / _PLANE."""
         check(self._L.ebic_ctx_set_path(self._h, int(path)))
 
+    def set_pair_layout(self, pairs_per_lane: int = 0, cands_per_warp: int = 0) -> None:
+        """Force one packed-pair layout of the hot kernel ((0, 0) = auto)."""
+        check(self._L.ebic_ctx_set_pair_layout(self._h, int(pairs_per_lane), int(cands_per_warp)))
+
     def prepare(self, approx: float) -> None:
         """Build the rank plane for `approx` now (otherwise built on first use)."""
         check(self._L.ebic_matrix_prepare(self._h, float(approx)))

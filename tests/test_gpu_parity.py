@@ -413,3 +413,34 @@ def test_plane_builders_agree(n_cols, f64, monkeypatch):
         want = oracle.evaluate_population(m, pop.cols, pop.offsets, a, neg)
         np.testing.assert_array_equal(got_tile, want)
         np.testing.assert_array_equal(got_block, want)
+
+
+PAIR_LAYOUTS = [(2, 1), (2, 2), (2, 4), (1, 1), (1, 2), (1, 4)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", PAIR_LAYOUTS, ids=[f"p{p}s{s}" for p, s in PAIR_LAYOUTS])
+@pytest.mark.parametrize("n_cols", [40, 250, 500, 1000, 2000])
+def test_every_pair_layout(evaluator, layout, n_cols):
+    """Each packed-pair layout of the hot kernel (row pairs per lane x
+    candidates per warp instruction), forced, against the C oracle: short and
+    long candidates (record tail from the CSR), negatives, ragged last slab.
+    Layouts whose slab does not fit run on the 32-bit-word kernel instead."""
+    rng = np.random.default_rng(1000 + n_cols)
+    R = 1000 + 37
+    m = rng.standard_normal((R, n_cols)).astype(np.float32)
+    m[: R // 4] = np.sort(m[: R // 4], axis=1)
+    m[R // 4: R // 2] = -np.sort(m[R // 4: R // 2], axis=1)
+    m[rng.random(m.shape) < 0.02] = 0.0
+    seqs = [rng.choice(n_cols, size=int(rng.integers(1, 11)), replace=False) for _ in range(900)]
+    seqs += [np.sort(rng.choice(n_cols, size=min(L, n_cols), replace=False)) for L in (8, 12, 30)]
+    pop = Population.from_sequences(seqs)
+    evaluator.upload(m)
+    evaluator.set_pair_layout(*layout)
+    try:
+        for approx, neg in ((0.03, False), (0.0, True), (0.3, True)):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+            np.testing.assert_array_equal(got, want, err_msg=f"C={n_cols} layout={layout} approx={approx} neg={neg}")
+    finally:
+        evaluator.set_pair_layout(0, 0)
