@@ -400,7 +400,13 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
             v[:] = a
             return v
 
-        pops = [Population(pinned(pp.cols), pinned(pp.offsets)) for pp in pops]
+        def pinned_csr(pp):
+            # one page-locked block [offsets | cols]: the library DMAs it in one copy
+            buf = pinned(np.concatenate([pp.offsets, pp.cols]))
+            n1 = pp.offsets.size
+            return Population(buf[n1:], buf[:n1])
+
+        pops = [pinned_csr(pp) for pp in pops]
         out_pinned = pinned(np.zeros(P, dtype=np.uint32))
 
         def call(pop, params):

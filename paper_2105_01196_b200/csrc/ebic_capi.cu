@@ -94,6 +94,27 @@ int ensure(HostBuf<T>& b, size_t n) {
   return EBIC_OK;
 }
 
+// ensure() for buffers whose contents must be zero when first used
+template <typename T>
+int ensure_zero(DevBuf<T>& b, size_t n, cudaStream_t s) {
+  if (b.n >= n && b.p) return EBIC_OK;
+  EBIC_TRY(ensure(b, n));
+  EBIC_CUDA(cudaMemsetAsync(b.p, 0, b.n * sizeof(T), s));
+  return EBIC_OK;
+}
+
+// Device alias of page-locked host memory (nullptr if the memory is not
+// page-locked or not mapped into the device's address space).
+void* dev_alias(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return static_cast<char*>(a.devicePointer) + 0;
+}
+
 struct Slot {
   HostBuf<uint32_t> h_cols, h_offs, h_counts;
   HostBuf<int> h_err;  // device-detected argument errors of this submission
@@ -121,6 +142,10 @@ struct ebic_ctx {
   DevBuf<uint32_t> d_mask, d_rows, d_tmp_cols, d_tmp_offs, d_tmp_counts;
   DevBuf<uint64_t> d_row_offsets;
   HostBuf<uint32_t> h_tmp_counts;
+  // slab_pair_kernel: per-candidate partial-count accumulators and per-chunk
+  // arrival counters, both zero between launches (the kernel re-zeroes them)
+  DevBuf<uint32_t> d_acc, d_done;
+  HostBuf<int> h_err1;  // page-locked, device-mapped: error flag of the zero-copy host path
   Slot slots[EBIC_MARSHAL_SLOTS];
   uint64_t next_ticket = 1;
   // tickets retired early (ring reuse / slot growth) whose device-side check failed
@@ -383,9 +408,14 @@ int launch_slab_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, con
   return EBIC_OK;
 }
 
+struct PairOut {       // where slab_pair_kernel publishes its results
+  uint32_t* out;       // final counts (device-accessible)
+  int* err_out;        // device error flag forwarded here (nullptr: kept in ctx->d_err)
+};
+
 template <int P, int SUB, bool NEG>
 int launch_simd_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
-                  uint64_t n_cand, uint32_t* d_counts, cudaStream_t s) {
+                  uint64_t n_cand, uint32_t* d_counts, const PairOut* po, cudaStream_t s) {
   auto kern = cfg.v2 ? ebic::slab_pair_kernel<P, SUB, NEG> : ebic::slab_simd_kernel<P, SUB, NEG>;
   static std::atomic<uint64_t> attr_done[2] = {{0}, {0}};
   const uint64_t bit = 1ull << (ctx->device & 63);
@@ -396,10 +426,20 @@ int launch_simd_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, con
   ebic::SlabArgs a = make_slab_args(ctx, cfg, d_cols, d_offs, n_cand, d_counts, nullptr);
   const uint64_t units = (uint64_t)a.n_chunks * a.n_slabs;
   unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
-  if (cfg.v2 && ctx->chunk_groups && a.n_chunks <= (uint32_t)ctx->n_sms) {
-    // chunk groups in step (a CTA per SM, up to n_sms % n_chunks SMs idle)
-    a.group = std::min<uint32_t>((uint32_t)ctx->n_sms / a.n_chunks, a.n_slabs);
-    grid = a.group * a.n_chunks;
+  if (cfg.v2) {
+    if (!po || !po->out) return fail(EBIC_ERR_INVALID_ARGUMENT, "internal: pair kernel without an output");
+    // chunk groups of `group` CTAs (a CTA per SM; up to n_sms % n_chunks SMs idle):
+    // the groups walk the plane in step, and every CTA packs its chunk once
+    const uint32_t n_sms = (uint32_t)ctx->n_sms;
+    a.group = std::max<uint32_t>(1, std::min<uint32_t>(n_sms / std::min<uint32_t>(a.n_chunks, n_sms), a.n_slabs));
+    const uint32_t n_groups = std::min<uint32_t>(a.n_chunks, n_sms / a.group);
+    grid = a.group * n_groups;
+    EBIC_TRY(ensure_zero(ctx->d_acc, n_cand, s));
+    EBIC_TRY(ensure_zero(ctx->d_done, (size_t)a.n_chunks + 1, s));
+    a.counts = ctx->d_acc.p;
+    a.out = po->out;
+    a.done = ctx->d_done.p;
+    a.err_out = po->err_out ? po->err_out : ctx->d_err;
   }
   kern<<<grid, ebic::kSlabThreads, cfg.smem, s>>>(a);
   ctx->launches++;
@@ -409,17 +449,17 @@ int launch_simd_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, con
 
 template <bool NEG, bool MASK>
 int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
-                uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+                uint64_t n_cand, uint32_t* d_counts, uint32_t* d_mask, const PairOut* po, cudaStream_t s) {
   if constexpr (!MASK) {
     if (cfg.simd) {
       if (cfg.p == 2) {
-        if (cfg.sub == 1) return launch_simd_t<2, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
-        if (cfg.sub == 2) return launch_simd_t<2, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
-        return launch_simd_t<2, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+        if (cfg.sub == 1) return launch_simd_t<2, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, po, s);
+        if (cfg.sub == 2) return launch_simd_t<2, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, po, s);
+        return launch_simd_t<2, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, po, s);
       }
-      if (cfg.sub == 1) return launch_simd_t<1, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
-      if (cfg.sub == 2) return launch_simd_t<1, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
-      return launch_simd_t<1, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, s);
+      if (cfg.sub == 1) return launch_simd_t<1, 1, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, po, s);
+      if (cfg.sub == 2) return launch_simd_t<1, 2, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, po, s);
+      return launch_simd_t<1, 4, NEG>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, po, s);
     }
   }
   if constexpr (MASK) {
@@ -435,17 +475,20 @@ int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const
   }
 }
 
+// Counting launch.  d_counts must be zero: the kernels ADD into it -- except
+// slab_pair_kernel, which writes final counts to po->out (see count_into).
 template <bool MASK>
 int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand,
-                 double approx, int neg, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s) {
+                 double approx, int neg, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s,
+                 const PairOut* po = nullptr) {
   if (n_cand == 0) return EBIC_OK;
   if (n_cand > 0xffffffffull / 2) return fail(EBIC_ERR_INVALID_ARGUMENT, "too many candidates");
   if (ctx->path != EBIC_PATH_VALUE && plane_fits(ctx)) {
     const SlabCfg cfg = choose_slab(ctx, n_cand, MASK);
     if (cfg.ok) {
       EBIC_TRY(ensure_plane(ctx, approx, s));
-      if (neg) return launch_slab<true, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
-      return launch_slab<false, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, s);
+      if (neg) return launch_slab<true, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, po, s);
+      return launch_slab<false, MASK>(ctx, cfg, d_cols, d_offs, n_cand, d_counts, d_mask, po, s);
     }
   }
   // (row masks for supporting_rows may always fall back to the value kernel:
@@ -473,6 +516,36 @@ int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     }
   }
   EBIC_CUDA(cudaGetLastError());
+  return EBIC_OK;
+}
+
+// Does a counting launch of n_cand candidates run slab_pair_kernel?  That
+// kernel writes final counts to any device-accessible pointer -- including
+// the device alias of page-locked host memory -- with no memset before and no
+// copy after; the other kernels add into zeroed device memory.
+bool pair_path(const ebic_ctx* ctx, uint64_t n_cand) {
+  if (n_cand == 0 || ctx->path == EBIC_PATH_VALUE || !plane_fits(ctx)) return false;
+  const SlabCfg cfg = choose_slab(ctx, n_cand, false);
+  return cfg.ok && cfg.simd && cfg.v2;
+}
+
+// Evaluate and leave the FINAL counts in `out` and the device error flag in
+// `err_out` (nullptr: ctx->d_err, read by ebic_ctx_sync).  `out` may be host
+// memory (device alias) only when pair_path(ctx, n_cand); `err_out` may be
+// host memory (device alias) always.
+int count_into(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand, double approx,
+               int neg, uint32_t* out, int* err_out, cudaStream_t s) {
+  if (n_cand == 0) return EBIC_OK;
+  if (pair_path(ctx, n_cand)) {
+    const PairOut po{out, err_out};
+    return launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, nullptr, nullptr, s, &po);
+  }
+  EBIC_CUDA(cudaMemsetAsync(out, 0, n_cand * sizeof(uint32_t), s));
+  EBIC_TRY(launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, out, nullptr, s));
+  if (err_out && err_out != ctx->d_err) {
+    EBIC_CUDA(cudaMemcpyAsync(err_out, ctx->d_err, sizeof(int), cudaMemcpyDefault, s));
+    EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
+  }
   return EBIC_OK;
 }
 
@@ -770,9 +843,7 @@ int ebic_eval_counts_device(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_
   EBIC_TRY(set_device(ctx));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   if (n_cand == 0) return EBIC_OK;
-  EBIC_CUDA(cudaMemsetAsync(d_counts, 0, n_cand * sizeof(uint32_t), s));
-  return launch_count<false>(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, d_counts,
-                             nullptr, s);
+  return count_into(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, d_counts, nullptr, s);
 }
 
 int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
@@ -816,13 +887,21 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
                               cudaMemcpyHostToDevice, s));
     EBIC_CUDA(cudaMemcpyAsync(sl.d_offs.p, sl.h_offs.p, (n_cand + 1) * sizeof(uint32_t),
                               cudaMemcpyHostToDevice, s));
-    EBIC_CUDA(cudaMemsetAsync(sl.d_counts.p, 0, n_cand * sizeof(uint32_t), s));
-    EBIC_TRY(launch_count<false>(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends,
-                                 sl.d_counts.p, nullptr, s));
-    EBIC_CUDA(cudaMemcpyAsync(sl.h_counts.p, sl.d_counts.p, n_cand * sizeof(uint32_t),
-                              cudaMemcpyDeviceToHost, s));
-    EBIC_CUDA(cudaMemcpyAsync(sl.h_err.p, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
+    // the pair kernel writes the counts and the error flag straight into the
+    // slot's page-locked buffers; otherwise device counts + a D2H copy
+    uint32_t* h_counts_dev = static_cast<uint32_t*>(dev_alias(sl.h_counts.p));
+    int* h_err_dev = static_cast<int*>(dev_alias(sl.h_err.p));
+    if (h_counts_dev && h_err_dev && pair_path(ctx, n_cand)) {
+      EBIC_TRY(count_into(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends, h_counts_dev,
+                          h_err_dev, s));
+    } else {
+      EBIC_TRY(count_into(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends, sl.d_counts.p,
+                          nullptr, s));
+      EBIC_CUDA(cudaMemcpyAsync(sl.h_counts.p, sl.d_counts.p, n_cand * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, s));
+      EBIC_CUDA(cudaMemcpyAsync(sl.h_err.p, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+      EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
+    }
   } else {
     sl.h_err.p[0] = 0;
   }
@@ -852,46 +931,54 @@ int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket) {
   return wait_slot(ctx, sl);
 }
 
-namespace {
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-}  // namespace
 
 int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
                      double approx, int negative_trends, uint32_t* counts_out) {
   // Zero-copy when the caller's arrays are already page-locked (cudaHostAlloc /
-  // cudaHostRegister / torch pin_memory): DMA straight from and into them.
-  // Otherwise go through the marshaller's pinned staging slots.
-  if (n_cand && ctx && ctx->d_mat && cols && offsets && counts_out && is_pinned(cols) && is_pinned(offsets) &&
-      is_pinned(counts_out)) {
+  // cudaHostRegister / torch pin_memory): the inputs are DMA'd straight from
+  // them (ONE copy when the offsets are immediately followed by the columns in
+  // memory) and the pair kernel writes the counts straight into counts_out
+  // over the bus.  Otherwise go through the marshaller's pinned staging slots.
+  uint32_t* out_dev = (n_cand && ctx && ctx->d_mat && cols && offsets && counts_out && dev_alias(cols) &&
+                       dev_alias(offsets))
+                          ? static_cast<uint32_t*>(dev_alias(counts_out))
+                          : nullptr;
+  if (out_dev) {
     EBIC_TRY(check_approx(approx));
     EBIC_TRY(validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false));
     EBIC_TRY(set_device(ctx));
-    const uint64_t n_idx = offsets[n_cand];
-    EBIC_TRY(ensure(ctx->d_tmp_cols, n_idx));
-    EBIC_TRY(ensure(ctx->d_tmp_offs, n_cand + 1));
-    EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
     cudaStream_t s = ctx->stream;
-    EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
-    EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, cols, n_idx * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    EBIC_CUDA(cudaMemsetAsync(ctx->d_tmp_counts.p, 0, n_cand * sizeof(uint32_t), s));
-    EBIC_TRY(launch_count<false>(ctx, ctx->d_tmp_cols.p, ctx->d_tmp_offs.p, n_cand, approx, negative_trends,
-                                 ctx->d_tmp_counts.p, nullptr, s));
-    EBIC_CUDA(cudaMemcpyAsync(counts_out, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    int err = 0;
-    EBIC_CUDA(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    EBIC_CUDA(cudaStreamSynchronize(s));
-    if (err) {
-      EBIC_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)));
-      return bad_column_error(ctx);
+    const uint64_t n_idx = offsets[n_cand];
+    const bool one_copy = offsets + (n_cand + 1) == cols;
+    const uint32_t *d_cols, *d_offs;
+    if (one_copy) {
+      EBIC_TRY(ensure(ctx->d_tmp_cols, n_cand + 1 + n_idx));
+      EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, offsets, (n_cand + 1 + n_idx) * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, s));
+      d_offs = ctx->d_tmp_cols.p;
+      d_cols = ctx->d_tmp_cols.p + n_cand + 1;
+    } else {
+      EBIC_TRY(ensure(ctx->d_tmp_cols, n_idx));
+      EBIC_TRY(ensure(ctx->d_tmp_offs, n_cand + 1));
+      EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, cols, n_idx * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, s));
+      d_offs = ctx->d_tmp_offs.p;
+      d_cols = ctx->d_tmp_cols.p;
     }
+    EBIC_TRY(ensure(ctx->h_err1, 1));
+    int* err_dev = static_cast<int*>(dev_alias(ctx->h_err1.p));
+    if (!err_dev) return fail(EBIC_ERR_CUDA, "page-locked error flag is not device-mapped");
+    ctx->h_err1.p[0] = 0;
+    if (pair_path(ctx, n_cand)) {
+      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, out_dev, err_dev, s));
+    } else {
+      EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
+      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, ctx->d_tmp_counts.p, err_dev, s));
+      EBIC_CUDA(cudaMemcpyAsync(counts_out, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    }
+    EBIC_CUDA(cudaStreamSynchronize(s));
+    if (*(volatile int*)ctx->h_err1.p) return bad_column_error(ctx);
     return EBIC_OK;
   }
   uint64_t t = 0;

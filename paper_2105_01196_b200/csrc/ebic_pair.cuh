@@ -273,23 +273,76 @@ slab_pair_kernel(const SlabArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / LPC, rl = lane % LPC;
   const uint32_t lane_base = sa_slab + rl * P * 8;  // this lane's (Rg, NT) pair(s) in column 0
-  uint64_t u_begin, u_end;  // work units u = chunk * n_slabs + slab
-  if (a.group) {
-    // one chunk per CTA; CTA i of every chunk group sweeps the same slab range,
-    // so the groups read each slab of the plane at about the same time
-    const uint32_t ch = blockIdx.x / a.group, i = blockIdx.x % a.group;
-    u_begin = (uint64_t)ch * a.n_slabs + (uint64_t)i * a.n_slabs / a.group;
-    u_end = (uint64_t)ch * a.n_slabs + (uint64_t)(i + 1) * a.n_slabs / a.group;
-  } else {
-    const uint64_t U = (uint64_t)a.n_chunks * a.n_slabs;
-    u_begin = blockIdx.x * U / gridDim.x;
-    u_end = (blockIdx.x + 1) * U / gridDim.x;
-  }
-  uint32_t cur_chunk = 0xffffffffu, c_begin = 0, c_n = 0;
+  // Work: chunk groups of a.group CTAs.  CTA b sweeps slab range b % group of
+  // chunks b / group, b / group + n_groups, ...; CTA i of every group sweeps
+  // the same slab range, so the groups read each slab of the plane at about
+  // the same time (one pass over the plane from DRAM when it exceeds L2).
+  const uint32_t n_groups = gridDim.x / a.group, gi = blockIdx.x % a.group;
+  const uint32_t s_begin = (uint32_t)((uint64_t)gi * a.n_slabs / a.group);
+  const uint32_t s_end = (uint32_t)((uint64_t)(gi + 1) * a.n_slabs / a.group);
+  __shared__ uint32_t s_last;
 
-  // position-indexed accumulators -> global counts (once per CTA and chunk)
-  auto flush = [&]() {
-    if (cur_chunk == 0xffffffffu) return;
+  for (uint32_t chunk = blockIdx.x / a.group; chunk < a.n_chunks; chunk += n_groups) {
+    const uint32_t c_begin = chunk * a.chunk, c_n = min(a.chunk, a.n_cand - c_begin);
+    __syncthreads();  // the previous chunk's records / bookkeeping are no longer read
+    pack_chunk_pos<STRIDE>(a, c_begin, c_n, s_rec, s_acc, s_perm, bk);
+    for (uint32_t slab = s_begin; slab < s_end; ++slab) {
+      const uint32_t row0 = slab * RT;
+      __syncthreads();  // previous slab fully consumed (and the pack done)
+      // stage + repack: each thread takes 4 consecutive rows (one uint4 of plane
+      // words) of one column -> 2 row pairs -> 4 words (Rg, NT, Rg, NT) of the line;
+      // a round of UNR loads is in flight before any store
+      {
+        constexpr uint32_t Q = RT / 4;  // uint4 per column
+        constexpr int UNR = 4;
+        const uint32_t total = a.n_cols * Q;
+        const uint4* src = reinterpret_cast<const uint4*>(a.plane);
+        const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
+        for (uint32_t t0 = threadIdx.x; t0 < total; t0 += UNR * blockDim.x) {
+          uint4 w[UNR];
+#pragma unroll
+          for (int k = 0; k < UNR; ++k) {
+            const uint32_t t = t0 + k * blockDim.x;
+            if (t < total) w[k] = __ldg(src + (uint64_t)(t / Q) * ld4 + r4 + t % Q);
+          }
+#pragma unroll
+          for (int k = 0; k < UNR; ++k) {
+            const uint32_t t = t0 + k * blockDim.x;
+            if (t < total) {
+              const uint32_t c = t / Q, q = t % Q;
+              *reinterpret_cast<uint4*>(s_slab + (size_t)c * CW + 4 * q) = stage_pairs<P>(w[k]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      prefetch_next_slab<RT>(a, (uint64_t)chunk * a.n_slabs + slab + 1, (uint64_t)chunk * a.n_slabs + s_end);
+
+      const uint32_t valid_rows = min(RT, a.n_rows - row0);
+      M vmask;
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const uint32_t r = (rl * P + q) * 2;
+        wref(vmask, q) = (r < valid_rows ? 0x8000u : 0u) | (r + 1 < valid_rows ? 0x80000000u : 0u);
+      }
+      uint32_t g = 0, pending = 0;
+      uint32_t* acc_w = s_acc + (size_t)warp * bk.K * SUB;
+#define EBIC_PAIR_SWEEP(L)                                                                                   \
+    pair_sweep_class<P, SUB, NEG, L, COLSHIFT>(a, sa_rec + bk.rbyte[L], lane_base, bk.npad[L] / STRIDE, c_begin, \
+                                               vmask, warp, lane, sub, g, pending, acc_w)
+      EBIC_PAIR_SWEEP(4);
+      EBIC_PAIR_SWEEP(3);
+      EBIC_PAIR_SWEEP(5);
+      EBIC_PAIR_SWEEP(2);
+      EBIC_PAIR_SWEEP(6);
+      EBIC_PAIR_SWEEP(7);
+      EBIC_PAIR_SWEEP(8);
+      EBIC_PAIR_SWEEP(1);
+#undef EBIC_PAIR_SWEEP
+      park_flush_tail<SUB>(g, pending, acc_w, lane);
+    }  // slabs
+    __syncthreads();
+    // position-indexed accumulators -> the chunk's global partial counts
     for (uint32_t p = threadIdx.x; p < bk.npos; p += blockDim.x) {
       const uint32_t slot = s_perm[p];
       if (slot >= c_n) continue;
@@ -302,74 +355,35 @@ slab_pair_kernel(const SlabArgs a) {
       const uint32_t cnt = s_acc[(w * bk.K + g) * SUB + s];
       if (cnt) atomicAdd(&a.counts[c_begin + slot], cnt);
     }
-  };
-
-  for (uint64_t u = u_begin; u < u_end; ++u) {
-    const uint32_t chunk = (uint32_t)(u / a.n_slabs), slab = (uint32_t)(u % a.n_slabs);
-    const uint32_t row0 = slab * RT;
+    // the last CTA of the chunk group publishes the chunk's counts to a.out
+    // (device memory, or page-locked host memory written over the bus: no
+    // separate D2H copy) and re-zeroes the accumulators for the next launch
+    __threadfence();
     __syncthreads();
-    if (chunk != cur_chunk) {
-      flush();
+    if (threadIdx.x == 0) s_last = atomicAdd(&a.done[chunk], 1u) == a.group - 1;
+    __syncthreads();
+    if (s_last) {
+      // (writes to page-locked host memory are visible to the host once the
+      // kernel has completed: no system-scope fence needed here)
+      __threadfence();
+      for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x) {
+        a.out[c_begin + j] = __ldcg(&a.counts[c_begin + j]);
+        a.counts[c_begin + j] = 0;
+      }
       __syncthreads();
-      cur_chunk = chunk;
-      c_begin = chunk * a.chunk;
-      c_n = min(a.chunk, a.n_cand - c_begin);
-      pack_chunk_pos<STRIDE>(a, c_begin, c_n, s_rec, s_acc, s_perm, bk);
-    }
-    // stage + repack: each thread takes 4 consecutive rows (one uint4 of plane
-    // words) of one column -> 2 row pairs -> 4 words (Rg, NT, Rg, NT) of the line;
-    // a round of UNR loads is in flight before any store
-    {
-      constexpr uint32_t Q = RT / 4;  // uint4 per column
-      constexpr int UNR = 4;
-      const uint32_t total = a.n_cols * Q;
-      const uint4* src = reinterpret_cast<const uint4*>(a.plane);
-      const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
-      for (uint32_t t0 = threadIdx.x; t0 < total; t0 += UNR * blockDim.x) {
-        uint4 w[UNR];
-#pragma unroll
-        for (int k = 0; k < UNR; ++k) {
-          const uint32_t t = t0 + k * blockDim.x;
-          if (t < total) w[k] = __ldg(src + (uint64_t)(t / Q) * ld4 + r4 + t % Q);
-        }
-#pragma unroll
-        for (int k = 0; k < UNR; ++k) {
-          const uint32_t t = t0 + k * blockDim.x;
-          if (t < total) {
-            const uint32_t c = t / Q, q = t % Q;
-            *reinterpret_cast<uint4*>(s_slab + (size_t)c * CW + 4 * q) = stage_pairs<P>(w[k]);
+      if (threadIdx.x == 0) {
+        a.done[chunk] = 0;
+        // the last chunk to be published forwards the device error flag
+        if (atomicAdd(&a.done[a.n_chunks], 1u) == a.n_chunks - 1) {
+          if (a.err_out != a.err) {
+            *a.err_out = *(volatile int*)a.err;
+            *a.err = 0;
           }
+          a.done[a.n_chunks] = 0;
         }
       }
     }
-    __syncthreads();
-    prefetch_next_slab<RT>(a, u + 1, u_end);
-
-    const uint32_t valid_rows = min(RT, a.n_rows - row0);
-    M vmask;
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const uint32_t r = (rl * P + q) * 2;
-      wref(vmask, q) = (r < valid_rows ? 0x8000u : 0u) | (r + 1 < valid_rows ? 0x80000000u : 0u);
-    }
-    uint32_t g = 0, pending = 0;
-    uint32_t* acc_w = s_acc + (size_t)warp * bk.K * SUB;
-#define EBIC_PAIR_SWEEP(L)                                                                                   \
-  pair_sweep_class<P, SUB, NEG, L, COLSHIFT>(a, sa_rec + bk.rbyte[L], lane_base, bk.npad[L] / STRIDE, c_begin, \
-                                             vmask, warp, lane, sub, g, pending, acc_w)
-    EBIC_PAIR_SWEEP(4);
-    EBIC_PAIR_SWEEP(3);
-    EBIC_PAIR_SWEEP(5);
-    EBIC_PAIR_SWEEP(2);
-    EBIC_PAIR_SWEEP(6);
-    EBIC_PAIR_SWEEP(7);
-    EBIC_PAIR_SWEEP(8);
-    EBIC_PAIR_SWEEP(1);
-#undef EBIC_PAIR_SWEEP
-    park_flush_tail<SUB>(g, pending, acc_w, lane);
-  }
-  __syncthreads();
-  flush();
+  }  // chunks
 }
 
 }  // namespace ebic

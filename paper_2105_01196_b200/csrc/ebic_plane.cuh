@@ -137,8 +137,10 @@ struct SlabArgs {
   uint64_t mask_wpc;
   int* err;
   int prefetch;           // warm L2 with the next unit's slab (plane larger than L2)
-  uint32_t group;         // > 0: CTAs per chunk; CTA b sweeps one slab range of chunk b / group
-                          // (all chunk groups walk the plane in step: one DRAM pass); 0: linear units
+  uint32_t group;         // slab_pair_kernel: CTAs per chunk group (see the kernel)
+  uint32_t* out;          // slab_pair_kernel: final counts (written, not added; device-accessible)
+  uint32_t* done;         // slab_pair_kernel: [n_chunks + 1] arrival counters, zero between launches
+  int* err_out;           // slab_pair_kernel: where the device error flag is forwarded (== err: kept)
 };
 
 // One consecutive-pair test on RPL rows: forward needs c > thr(p), reversed p > thr(c).

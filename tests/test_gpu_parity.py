@@ -444,3 +444,57 @@ def test_every_pair_layout(evaluator, layout, n_cols):
             np.testing.assert_array_equal(got, want, err_msg=f"C={n_cols} layout={layout} approx={approx} neg={neg}")
     finally:
         evaluator.set_pair_layout(0, 0)
+
+
+def _pinned_u32(a):
+    import torch
+
+    t = torch.empty(max(a.size, 1), dtype=torch.int32, pin_memory=True)
+    v = t.numpy().view(np.uint32)[: a.size]
+    v[:] = a
+    return t, v
+
+
+@pytest.mark.parametrize("layout", ["separate", "one_block"])
+@pytest.mark.parametrize("path", [EBIC_PATH_AUTO, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE], ids=["pair", "u32", "value"])
+def test_zero_copy_host_path(evaluator, layout, path):
+    """Page-locked host arrays: inputs DMA'd directly (one copy for an
+    [offsets | cols] block), counts written by the kernel straight into the
+    page-locked output (pair kernel) or copied back (other kernels); a bad
+    column is reported and the next call is clean."""
+    rng = np.random.default_rng(77)
+    m = rng.standard_normal((3000, 700)).astype(np.float32)
+    m[:500] = np.sort(m[:500], axis=1)
+    pop = Population.from_sequences(rng.choice(700, size=int(rng.integers(2, 10)), replace=False)
+                                    for _ in range(5000))
+    evaluator.upload(m)
+    evaluator.set_path(path)
+    keep = []
+    try:
+        if layout == "one_block":
+            t, buf = _pinned_u32(np.concatenate([pop.offsets, pop.cols]))
+            keep.append(t)
+            ppop = Population(buf[pop.offsets.size:], buf[: pop.offsets.size])
+        else:
+            (t1, c), (t2, o) = _pinned_u32(pop.cols), _pinned_u32(pop.offsets)
+            keep += [t1, t2]
+            ppop = Population(c, o)
+        t3, out = _pinned_u32(np.full(len(pop), 0xDEADBEEF, np.uint32))
+        keep.append(t3)
+        for approx, neg in ((0.03, False), (0.0, True)):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(ppop, TrendParams(approx=approx, negative_trends=neg), out=out)
+            np.testing.assert_array_equal(got, want)
+        # a bad column: reported, and the following call is clean again
+        bad = ppop.cols.copy()
+        bad_pop = Population(bad, ppop.offsets.copy())
+        bad[3] = 700
+        t4, bc = _pinned_u32(bad)
+        keep.append(t4)
+        with pytest.raises(EbicError):
+            evaluator.evaluate_population(Population(bc, ppop.offsets), TrendParams(), out=out)
+        del bad_pop
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
+        np.testing.assert_array_equal(evaluator.evaluate_population(ppop, TrendParams(), out=out), want)
+    finally:
+        evaluator.set_path(EBIC_PATH_AUTO)
