@@ -945,9 +945,12 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
                           : nullptr;
   if (out_dev) {
     EBIC_TRY(check_approx(approx));
-    EBIC_TRY(validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false));
+    if (offsets[0] != 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "offsets[0] must be 0");
     EBIC_TRY(set_device(ctx));
     cudaStream_t s = ctx->stream;
+    // the input DMA is issued first; the offsets are checked on the host while
+    // it is in flight (the copy reads exactly [0, offsets[n_cand]) of cols, the
+    // size the caller declares), and the kernel is launched only if they pass
     const uint64_t n_idx = offsets[n_cand];
     const bool one_copy = offsets + (n_cand + 1) == cols;
     const uint32_t *d_cols, *d_offs;
@@ -965,6 +968,11 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
                                 cudaMemcpyHostToDevice, s));
       d_offs = ctx->d_tmp_offs.p;
       d_cols = ctx->d_tmp_cols.p;
+    }
+    if (validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false) != EBIC_OK) {
+      const std::string msg = g_last_error;
+      cudaStreamSynchronize(s);  // the scratch buffers may be reused by the next call
+      return fail(EBIC_ERR_INVALID_ARGUMENT, "%s", msg.c_str());
     }
     EBIC_TRY(ensure(ctx->h_err1, 1));
     int* err_dev = static_cast<int*>(dev_alias(ctx->h_err1.p));

@@ -84,8 +84,10 @@ def _as_population(pop) -> Population:
     return Population.from_sequences(pop)
 
 
-def _ptr(a: np.ndarray):
-    return a.ctypes.data_as(C.c_void_p)
+def _ptr(a: np.ndarray) -> int:
+    # the buffer address as a plain int (the bindings declare c_void_p); cheaper
+    # than ndarray.ctypes.data_as on the per-call path
+    return a.__array_interface__["data"][0]
 
 
 def device_count() -> int:

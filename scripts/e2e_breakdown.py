@@ -81,3 +81,18 @@ def dev():
 
 
 timeit("device API + sync (kernel + launch)", dev)
+
+# the same zero-copy call straight through ctypes (no Python-side checks)
+import ctypes as C  # noqa: E402
+
+L, h = ev._L, ev._h
+pc, po, pout = C.c_void_p(bpop.cols.ctypes.data), C.c_void_p(bpop.offsets.ctypes.data), C.c_void_p(vout.ctypes.data)
+timeit("raw ctypes ebic_eval_counts, pinned block", lambda: L.ebic_eval_counts(h, pc, po, 16384, 0.03, 0, pout))
+timeit("raw ctypes, 1 candidate (fixed overhead)",
+       lambda: L.ebic_eval_counts(h, C.c_void_p(tiny.cols.ctypes.data), C.c_void_p(tiny.offsets.ctypes.data), 1,
+                                  0.03, 0, pout))
+# host-side validation cost: offsets scan only (ebic_eval_counts with an invalid approx fails after nothing)
+t0 = time.perf_counter()
+for _ in range(1000):
+    np.all(np.diff(bpop.offsets.astype(np.int64)) > 0)
+print(f"{'numpy offsets scan (reference point)':60s} {(time.perf_counter() - t0) / 1000 * 1e6:9.1f} us")
