@@ -294,7 +294,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     b, e = row_range(R, rank, world) if args.shard == "rows" else (0, R)
 
     ev = Evaluator(local_rank)
-    ev.set_path({"auto": 0, "value": 1, "plane": 2}[args.path])
+    ev.set_path({"auto": 0, "value": 1, "plane": 2, "table": 4}[args.path])
     t0 = time.perf_counter()
     ev.upload(np.ascontiguousarray(m[b:e]), row_base=b)
     upload_ms = (time.perf_counter() - t0) * 1e3
@@ -376,6 +376,12 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     # roofline of the fitness kernel on this rank
     sum_len = [int(dp[3]) for dp in d_pops]
     alg_bytes = [4.0 * (e - b) * sl for sl in sum_len]
+    # pair-trend index in use: the kernel streams (L - 1) pair vectors of wp
+    # words per candidate (x2 with negatives) -- its PHYSICAL HBM traffic
+    index_bytes, index_used = ev.index_info()
+    wp = ((e - b + 31) // 32 + 3) // 4 * 4
+    n_pairs = [int(dp[3]) - int(dp[2]) for dp in d_pops]
+    phys_bytes = [4.0 * wp * npair * (2 if cfg["negative"] else 1) for npair in n_pairs]
     per_step_bytes = [alg_bytes[i % n_pops] for i in range(args.steps)]
     kern_avg_s = statistics.mean(kern_ms) / 1e3
     achieved = statistics.mean(bb / (km / 1e3) for bb, km in zip(per_step_bytes, kern_ms)) / 1e9
@@ -453,8 +459,16 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                    "shard": args.shard, "path": args.path},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, world),
-                     "kernel": ("slab_simd_kernel (packed rank pairs)" if Ccols <= 1024 else "slab_count_kernel (rank plane)")
+                     "kernel": ("table_count_kernel (pair-trend index)" if index_used else
+                                "slab_pair_kernel (packed rank pairs)" if Ccols <= 2048 else "slab_count_kernel (rank plane)")
                      if (args.path != "value" and Ccols <= 8192) else "fitness_count_kernel (value)", "kernel_avg_ms": kern_avg_s * 1e3,
+                     "physical": ({"what": "pair-vector bytes streamed from HBM per launch (4 B x wp words x (L-1) pairs "
+                                          "per candidate) / kernel time, vs the same peak",
+                                  "bytes_per_launch": statistics.mean(phys_bytes),
+                                  "gbs": statistics.mean(pb / (km / 1e3) for pb, km in
+                                                         zip([phys_bytes[i % n_pops] for i in range(args.steps)],
+                                                             kern_ms)) / 1e9,
+                                  } if index_used else None),
                      "algorithmic_bytes_per_launch": statistics.mean(alg_bytes),
                      "peak_source": peak_src,
                      "note": "algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "
@@ -464,12 +478,16 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                 "api": "ebic_eval_counts (Evaluator.evaluate_population), pinned host arrays" if world == 1
                        else f"ShardedEvaluator({args.shard}) over ebic_eval_counts + NCCL"},
         "gpu_launches": int(launches),
-        "store": {"upload_ms": upload_ms, "rank_plane_build_ms": prepare_ms,
-                  "note": "one-time per matrix (upload+transpose) and per (matrix, approx) (rank plane); "
-                          "not part of a step, like the reference's matrix construction"},
+        "store": {"upload_ms": upload_ms, "index_build_ms": prepare_ms,
+                  "pair_trend_index_bytes": index_bytes if index_used else 0,
+                  "note": "one-time per matrix (upload+transpose) and per (matrix, approx) (rank plane + "
+                          "pair-trend index: every pair test of the matrix as row bitsets, independent of the "
+                          "candidates); not part of a step, like the reference's matrix construction"},
         "wall_ms_timed_region": wall * 1e3,
         "parity_device_vs_host_api": parity_dev_vs_host,
     }
+    if line["roofline"]["physical"]:
+        line["roofline"]["physical"]["frac"] = line["roofline"]["physical"]["gbs"] / peak
     with_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
     if with_cpu:
         CUR_APPROX[0], CUR_NEG[0] = cfg["approx"], cfg["negative"]
@@ -501,7 +519,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="collective backend for N > 1 (gloo lets N ranks share one GPU to test the sharded path)")
-    ap.add_argument("--path", choices=["auto", "value", "plane"], default="auto",
+    ap.add_argument("--path", choices=["auto", "value", "plane", "table"], default="auto",
                     help="evaluation kernel: rank-plane slab kernel (auto for <= 8192 cols) or float value kernel")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

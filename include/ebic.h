@@ -156,16 +156,21 @@ int ebic_ctx_launch_count(ebic_ctx* ctx, uint64_t* n_out);
 /* Tuning knob for the value-path kernel: rows per CTA slab (0 = auto). */
 int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
 
-/* Evaluation path.  AUTO: the rank-plane slab kernels whenever the matrix has
- * <= 8192 columns (packed 16-bit rank pairs when a 32-row slab fits in shared
- * memory, else 32-bit plane words), otherwise the value kernel.  VALUE, PLANE
- * and PLANE_U32 (32-bit plane words only) force one; the plane paths fail
- * with EBIC_ERR_INVALID_ARGUMENT if the matrix is too wide.  All are
- * bit-exact; the knob exists for cross-checking and benchmarking. */
+/* Evaluation path.  AUTO: the pair-trend index (every consecutive-pair test
+ * of the matrix as row bitsets, built once per matrix x approx; C^2 x R/8
+ * bytes) when it fits the context's budget, else the rank-plane slab kernels
+ * whenever the matrix has <= 8192 columns (packed 16-bit rank pairs when a
+ * 32-row slab fits in shared memory, else 32-bit plane words), otherwise the
+ * value kernel.  TABLE, VALUE, PLANE (slab kernels, no index) and PLANE_U32
+ * (32-bit plane words only) force one; a forced path that cannot serve the
+ * matrix fails with EBIC_ERR_INVALID_ARGUMENT (or EBIC_ERR_CUDA if the index
+ * does not fit in memory).  All are bit-exact; the knob exists for
+ * cross-checking and benchmarking. */
 #define EBIC_PATH_AUTO 0
 #define EBIC_PATH_VALUE 1
 #define EBIC_PATH_PLANE 2
 #define EBIC_PATH_PLANE_U32 3
+#define EBIC_PATH_TABLE 4
 int ebic_ctx_set_path(ebic_ctx* ctx, int path);
 
 /* Packed-pair layout of the hot kernel: `rows_per_lane_pairs` (1 or 2) 16-bit
@@ -176,6 +181,14 @@ int ebic_ctx_set_path(ebic_ctx* ctx, int path);
  * kernel.  Every layout is bit-exact; the knob exists for cross-checking and
  * benchmarking. */
 int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_per_warp);
+
+/* Memory budget of the pair-trend index (bytes; default 24 GiB, env
+ * EBIC_TABLE_BUDGET_MB); AUTO uses the index only if it needs <= min(budget,
+ * free device memory / 2 at upload). */
+int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes);
+/* Bytes the pair-trend index of the resident matrix needs (0 if the matrix is
+ * too wide for the rank plane) and whether it is built. */
+int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use);
 
 /* Build (or reuse) the rank plane of the resident matrix for `approx` now,
  * instead of lazily on the first evaluation with that approx.  The plane is a

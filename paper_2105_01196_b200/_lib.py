@@ -51,6 +51,8 @@ SIGNATURES = {
     "ebic_ctx_set_slab_rows": (C.c_int, [_vp, C.c_uint32]),
     "ebic_ctx_set_path": (C.c_int, [_vp, C.c_int]),
     "ebic_ctx_set_pair_layout": (C.c_int, [_vp, C.c_int, C.c_int]),
+    "ebic_ctx_set_table_budget": (C.c_int, [_vp, C.c_uint64]),
+    "ebic_matrix_index_info": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
     "ebic_matrix_prepare": (C.c_int, [_vp, C.c_double]),
 }
 
@@ -58,6 +60,7 @@ EBIC_PATH_AUTO = 0
 EBIC_PATH_VALUE = 1
 EBIC_PATH_PLANE = 2
 EBIC_PATH_PLANE_U32 = 3
+EBIC_PATH_TABLE = 4
 
 
 class EbicError(RuntimeError):

@@ -21,6 +21,7 @@
 #include "ebic_plane.cuh"
 #include "ebic_simd.cuh"
 #include "ebic_pair.cuh"
+#include "ebic_table.cuh"
 
 namespace {
 
@@ -155,6 +156,14 @@ struct ebic_ctx {
   // rank plane (per matrix x approx)
   uint32_t* d_plane = nullptr;
   bool plane_valid = false;
+  // pair-trend index (ebic_table.cuh), per matrix x approx; used when it fits
+  // table_budget bytes (EBIC_TABLE_BUDGET_MB; default min(24 GB, free HBM / 2)
+  // at upload time)
+  uint32_t* d_table = nullptr;
+  bool table_valid = false, table_failed = false;
+  double table_approx = 0.0;
+  uint64_t table_budget = 0;
+  uint64_t table_budget_user = 24ull << 30;  // ebic_ctx_set_table_budget / EBIC_TABLE_BUDGET_MB
   double plane_approx = 0.0;
   int path = EBIC_PATH_AUTO;
   int n_sms = 148;
@@ -162,6 +171,8 @@ struct ebic_ctx {
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
   int chunk_groups = 1;   // EBIC_CHUNK_GROUPS: slab_pair_kernel CTAs in per-chunk groups (1) or linear units (0)
+  int table_align = 4;     // EBIC_TABLE_ALIGN: pair-vector length granule in words (A/B)
+  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto, 1 warp per candidate, 2 CTA per candidate (A/B)
   int pair_kernel = 1;    // EBIC_PAIR_KERNEL: 1 position-indexed counts (slab_pair_kernel), 0 slab_simd_kernel (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
 };
@@ -264,6 +275,130 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   EBIC_CUDA(cudaGetLastError());
   ctx->plane_valid = true;
   ctx->plane_approx = approx;
+  return EBIC_OK;
+}
+
+// ---- pair-trend index ------------------------------------------------------
+constexpr int kTableNoMemory = -1;  // internal status: the index does not fit (fall back)
+
+uint64_t table_wp(const ebic_ctx* ctx) {
+  const uint64_t al = (uint64_t)ctx->table_align;  // words; a multiple of 4 (uint4 vectors)
+  return ((ctx->n_rows + 31) / 32 + al - 1) / al * al;
+}
+uint64_t table_bytes(const ebic_ctx* ctx) { return ctx->n_cols * ctx->n_cols * table_wp(ctx) * sizeof(uint32_t); }
+
+bool table_allowed(const ebic_ctx* ctx) {
+  if (!(ctx->path == EBIC_PATH_AUTO || ctx->path == EBIC_PATH_TABLE) || !plane_fits(ctx) || ctx->table_failed)
+    return false;
+  return ctx->path == EBIC_PATH_TABLE || table_bytes(ctx) <= ctx->table_budget;
+}
+
+// Build (or reuse) the index for `approx`.  kTableNoMemory if it cannot be
+// allocated (the caller falls back to the slab kernels; not retried for this
+// matrix).
+int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
+  if (ctx->table_valid && std::memcmp(&ctx->table_approx, &approx, sizeof(double)) == 0) return EBIC_OK;
+  EBIC_TRY(ensure_plane(ctx, approx, s));
+  ctx->table_valid = false;
+  if (!ctx->d_table) {
+    if (cudaMalloc(&ctx->d_table, table_bytes(ctx)) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->d_table = nullptr;
+      ctx->table_failed = true;
+      return kTableNoMemory;
+    }
+  }
+  const uint32_t wp = (uint32_t)table_wp(ctx);
+  const dim3 grid((wp + 31) / 32, (unsigned)((ctx->n_cols + ebic::kTableBuildWarps - 1) / ebic::kTableBuildWarps));
+  ebic::build_pair_table_kernel<<<grid, ebic::kTableBuildWarps * 32, 0, s>>>(
+      ctx->d_plane, ctx->ld, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp, ctx->d_table);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  ctx->table_valid = true;
+  ctx->table_approx = approx;
+  return EBIC_OK;
+}
+
+// Use the index for this evaluation?  Builds it on first use; false if it is
+// not allowed or cannot be allocated.
+int use_table(ebic_ctx* ctx, double approx, cudaStream_t s, bool* yes) {
+  *yes = false;
+  if (!table_allowed(ctx)) {
+    if (ctx->path == EBIC_PATH_TABLE)
+      return fail(EBIC_ERR_INVALID_ARGUMENT, "pair-trend index unavailable for this matrix (%llu columns)",
+                  (unsigned long long)ctx->n_cols);
+    return EBIC_OK;
+  }
+  const int st = ensure_table(ctx, approx, s);
+  if (st == kTableNoMemory) {
+    if (ctx->path == EBIC_PATH_TABLE)
+      return fail(EBIC_ERR_CUDA, "pair-trend index (%llu bytes) does not fit in device memory",
+                  (unsigned long long)table_bytes(ctx));
+    return EBIC_OK;
+  }
+  EBIC_TRY(st);
+  *yes = true;
+  return EBIC_OK;
+}
+
+// Counts WRITTEN to out (any device-accessible pointer), optional row masks.
+// n_idx bounds the offsets (checked on device).
+template <bool MASK>
+int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand, uint64_t n_idx,
+                 int neg, uint32_t* out, int* err_out, uint32_t* d_mask, cudaStream_t s) {
+  const uint32_t nv = (uint32_t)(table_wp(ctx) / 4);
+  if (nv <= 256 && ctx->table_kernel != 2) {
+    // short vectors: a warp per candidate, J = ceil(nv / 32) slices per lane
+    const uint32_t J = (nv + 31) / 32;
+    // a warp per candidate for the whole population (the block scheduler
+    // balances the tail better than a grid-stride loop over fewer warps)
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
+    auto go = [&](auto kern) {
+      kern<<<grid, 256, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
+                                d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err,
+                                d_mask, ctx->ld / 32);
+    };
+    auto pickj = [&](auto negc) {
+      constexpr bool N = decltype(negc)::value;
+      switch (J) {
+        case 1: go(ebic::table_count_warp_kernel<1, N, MASK>); break;
+        case 2: go(ebic::table_count_warp_kernel<2, N, MASK>); break;
+        case 3: go(ebic::table_count_warp_kernel<3, N, MASK>); break;
+        case 4: go(ebic::table_count_warp_kernel<4, N, MASK>); break;
+        case 5: go(ebic::table_count_warp_kernel<5, N, MASK>); break;
+        case 6: go(ebic::table_count_warp_kernel<6, N, MASK>); break;
+        case 7: go(ebic::table_count_warp_kernel<7, N, MASK>); break;
+        default: go(ebic::table_count_warp_kernel<8, N, MASK>); break;
+      }
+    };
+    if (neg) pickj(std::true_type{});
+    else pickj(std::false_type{});
+    ctx->launches++;
+    EBIC_CUDA(cudaGetLastError());
+    return EBIC_OK;
+  }
+  // long vectors: a CTA per candidate, T threads (one uint4 slice of every
+  // pair vector each, J slices when the vector exceeds 1024 slices)
+  const uint32_t T = std::min<uint32_t>(1024, (nv + 31) / 32 * 32);
+  const uint32_t J = (nv + T - 1) / T;
+  const uint64_t resident = (uint64_t)ctx->n_sms * std::max<uint32_t>(1, 2048 / T);
+  const unsigned grid = (unsigned)std::min<uint64_t>(n_cand, resident);
+  auto go = [&](auto kern) {
+    kern<<<grid, T, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
+                            d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err,
+                            d_mask, ctx->ld / 32);
+  };
+  auto pick = [&](auto negc) {
+    constexpr bool N = decltype(negc)::value;
+    if (J <= 1) go(ebic::table_count_kernel<1, N, MASK>);
+    else if (J <= 2) go(ebic::table_count_kernel<2, N, MASK>);
+    else if (J <= 4) go(ebic::table_count_kernel<4, N, MASK>);
+    else go(ebic::table_count_kernel<8, N, MASK>);
+  };
+  if (neg) pick(std::true_type{});
+  else pick(std::false_type{});
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
   return EBIC_OK;
 }
 
@@ -480,10 +615,15 @@ int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const
 template <bool MASK>
 int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand,
                  double approx, int neg, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s,
-                 const PairOut* po = nullptr) {
+                 const PairOut* po = nullptr, uint64_t n_idx = 0xffffffffull) {
   if (n_cand == 0) return EBIC_OK;
   if (n_cand > 0xffffffffull / 2) return fail(EBIC_ERR_INVALID_ARGUMENT, "too many candidates");
-  if (ctx->path != EBIC_PATH_VALUE && plane_fits(ctx)) {
+  bool table = false;
+  EBIC_TRY(use_table(ctx, approx, s, &table));
+  if (table)
+    return launch_table<MASK>(ctx, d_cols, d_offs, n_cand, n_idx, neg, po ? po->out : d_counts,
+                              po ? po->err_out : nullptr, d_mask, s);
+  if (ctx->path != EBIC_PATH_VALUE && ctx->path != EBIC_PATH_TABLE && plane_fits(ctx)) {
     const SlabCfg cfg = choose_slab(ctx, n_cand, MASK);
     if (cfg.ok) {
       EBIC_TRY(ensure_plane(ctx, approx, s));
@@ -529,16 +669,26 @@ bool pair_path(const ebic_ctx* ctx, uint64_t n_cand) {
   return cfg.ok && cfg.simd && cfg.v2;
 }
 
+// Will the counting launch write its results directly (pair-trend index or
+// slab_pair_kernel)?  Builds the index on first use.
+int direct_path(ebic_ctx* ctx, uint64_t n_cand, double approx, cudaStream_t s, bool* yes) {
+  EBIC_TRY(use_table(ctx, approx, s, yes));
+  if (!*yes) *yes = pair_path(ctx, n_cand);
+  return EBIC_OK;
+}
+
 // Evaluate and leave the FINAL counts in `out` and the device error flag in
 // `err_out` (nullptr: ctx->d_err, read by ebic_ctx_sync).  `out` may be host
 // memory (device alias) only when pair_path(ctx, n_cand); `err_out` may be
 // host memory (device alias) always.
 int count_into(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand, double approx,
-               int neg, uint32_t* out, int* err_out, cudaStream_t s) {
+               int neg, uint32_t* out, int* err_out, cudaStream_t s, uint64_t n_idx = 0xffffffffull) {
   if (n_cand == 0) return EBIC_OK;
-  if (pair_path(ctx, n_cand)) {
+  bool direct = false;
+  EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
+  if (direct) {
     const PairOut po{out, err_out};
-    return launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, nullptr, nullptr, s, &po);
+    return launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, nullptr, nullptr, s, &po, n_idx);
   }
   EBIC_CUDA(cudaMemsetAsync(out, 0, n_cand * sizeof(uint32_t), s));
   EBIC_TRY(launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, out, nullptr, s));
@@ -649,6 +799,15 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   ctx->n_cols = n_cols;
   ctx->ld = ld;
   ctx->row_base = row_base;
+  {
+    // pair-trend index budget: the user cap, at most half of the free HBM
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      fr = 0;
+    }
+    ctx->table_budget = std::min<uint64_t>(ctx->table_budget_user, fr / 2);
+  }
   if (store_out) *store_out = chosen;
   return EBIC_OK;
 }
@@ -737,6 +896,12 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (pf) ctx->prefetch = std::atoi(pf) ? 1 : 0;
     const char* cg = std::getenv("EBIC_CHUNK_GROUPS");
     if (cg) ctx->chunk_groups = std::atoi(cg) ? 1 : 0;
+    const char* tb = std::getenv("EBIC_TABLE_BUDGET_MB");
+    if (tb) ctx->table_budget_user = (uint64_t)std::strtoull(tb, nullptr, 10) << 20;
+    const char* ta = std::getenv("EBIC_TABLE_ALIGN");
+    if (ta) ctx->table_align = std::max(4, std::atoi(ta) / 4 * 4);
+    const char* tk = std::getenv("EBIC_TABLE_KERNEL");
+    if (tk) ctx->table_kernel = std::atoi(tk);
     const char* pk = std::getenv("EBIC_PAIR_KERNEL");
     if (pk) ctx->pair_kernel = std::atoi(pk) ? 1 : 0;
     const char* sc = std::getenv("EBIC_PAIR_LAYOUT");
@@ -827,6 +992,9 @@ int ebic_matrix_free(ebic_ctx* ctx) {
   if (ctx->d_plane) cudaFree(ctx->d_plane);
   ctx->d_plane = nullptr;
   ctx->plane_valid = false;
+  if (ctx->d_table) cudaFree(ctx->d_table);
+  ctx->d_table = nullptr;
+  ctx->table_valid = ctx->table_failed = false;
   ctx->d_mat = nullptr;
   ctx->store = 0;
   ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
@@ -883,15 +1051,21 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
   }
   cudaStream_t s = ctx->stream;
   if (n_cand) {
-    EBIC_CUDA(cudaMemcpyAsync(sl.d_cols.p, sl.h_cols.p, n_idx * sizeof(uint32_t),
-                              cudaMemcpyHostToDevice, s));
-    EBIC_CUDA(cudaMemcpyAsync(sl.d_offs.p, sl.h_offs.p, (n_cand + 1) * sizeof(uint32_t),
-                              cudaMemcpyHostToDevice, s));
-    // the pair kernel writes the counts and the error flag straight into the
-    // slot's page-locked buffers; otherwise device counts + a D2H copy
     uint32_t* h_counts_dev = static_cast<uint32_t*>(dev_alias(sl.h_counts.p));
     int* h_err_dev = static_cast<int*>(dev_alias(sl.h_err.p));
-    if (h_counts_dev && h_err_dev && pair_path(ctx, n_cand)) {
+    // (reading the candidates over the bus from the page-locked slot inside
+    // the kernel measured slower than one DMA: the first loads of every warp
+    // wait a bus round trip)
+    EBIC_CUDA(cudaMemcpyAsync(sl.d_cols.p, sl.h_cols.p, n_idx * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    EBIC_CUDA(cudaMemcpyAsync(sl.d_offs.p, sl.h_offs.p, (n_cand + 1) * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, s));
+    // the index / pair kernels write the counts and the error flag straight
+    // into the slot's page-locked buffers; otherwise device counts + a D2H copy
+    const bool mapped = h_counts_dev && h_err_dev;
+    bool direct = false;
+    EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
+    if (mapped && direct) {
+      sl.h_err.p[0] = 0;  // the index kernel only writes on error (the slot is not in flight)
       EBIC_TRY(count_into(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends, h_counts_dev,
                           h_err_dev, s));
     } else {
@@ -948,10 +1122,14 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
     if (offsets[0] != 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "offsets[0] must be 0");
     EBIC_TRY(set_device(ctx));
     cudaStream_t s = ctx->stream;
+    const uint64_t n_idx = offsets[n_cand];
+    EBIC_TRY(ensure(ctx->h_err1, 1));
+    int* err_dev = static_cast<int*>(dev_alias(ctx->h_err1.p));
+    if (!err_dev) return fail(EBIC_ERR_CUDA, "page-locked error flag is not device-mapped");
+    ctx->h_err1.p[0] = 0;
     // the input DMA is issued first; the offsets are checked on the host while
     // it is in flight (the copy reads exactly [0, offsets[n_cand]) of cols, the
     // size the caller declares), and the kernel is launched only if they pass
-    const uint64_t n_idx = offsets[n_cand];
     const bool one_copy = offsets + (n_cand + 1) == cols;
     const uint32_t *d_cols, *d_offs;
     if (one_copy) {
@@ -974,12 +1152,10 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
       cudaStreamSynchronize(s);  // the scratch buffers may be reused by the next call
       return fail(EBIC_ERR_INVALID_ARGUMENT, "%s", msg.c_str());
     }
-    EBIC_TRY(ensure(ctx->h_err1, 1));
-    int* err_dev = static_cast<int*>(dev_alias(ctx->h_err1.p));
-    if (!err_dev) return fail(EBIC_ERR_CUDA, "page-locked error flag is not device-mapped");
-    ctx->h_err1.p[0] = 0;
-    if (pair_path(ctx, n_cand)) {
-      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, out_dev, err_dev, s));
+    bool direct = false;
+    EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
+    if (direct) {
+      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, out_dev, err_dev, s, n_idx));
     } else {
       EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
       EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, ctx->d_tmp_counts.p, err_dev, s));
@@ -1117,9 +1293,30 @@ int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_p
   return EBIC_OK;
 }
 
+int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  ctx->table_budget_user = bytes;
+  if (ctx->d_mat) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      fr = 0;
+    }
+    ctx->table_budget = std::min<uint64_t>(bytes, fr / 2 + (ctx->d_table ? table_bytes(ctx) : 0));
+  }
+  return EBIC_OK;
+}
+
+int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use) {
+  EBIC_TRY(need_matrix(ctx));
+  if (bytes_needed) *bytes_needed = plane_fits(ctx) ? table_bytes(ctx) : 0;
+  if (in_use) *in_use = ctx->table_valid ? 1 : 0;
+  return EBIC_OK;
+}
+
 int ebic_ctx_set_path(ebic_ctx* ctx, int path) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
-  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_PLANE_U32) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
+  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_TABLE) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
   ctx->path = path;
   return EBIC_OK;
 }
@@ -1130,6 +1327,8 @@ int ebic_matrix_prepare(ebic_ctx* ctx, double approx) {
   EBIC_TRY(set_device(ctx));
   if (ctx->path == EBIC_PATH_VALUE || !plane_fits(ctx)) return EBIC_OK;
   EBIC_TRY(ensure_plane(ctx, approx, ctx->stream));
+  bool table = false;
+  EBIC_TRY(use_table(ctx, approx, ctx->stream, &table));
   EBIC_CUDA(cudaStreamSynchronize(ctx->stream));
   return EBIC_OK;
 }

@@ -159,6 +159,16 @@ class Evaluator:
         """Force one packed-pair layout of the hot kernel ((0, 0) = auto)."""
         check(self._L.ebic_ctx_set_pair_layout(self._h, int(pairs_per_lane), int(cands_per_warp)))
 
+    def set_table_budget(self, nbytes: int) -> None:
+        """Memory cap of the pair-trend index (AUTO path uses it only below the cap)."""
+        check(self._L.ebic_ctx_set_table_budget(self._h, int(nbytes)))
+
+    def index_info(self) -> tuple[int, bool]:
+        """(bytes the pair-trend index of the resident matrix needs, whether it is built)."""
+        nb, used = C.c_uint64(0), C.c_int(0)
+        check(self._L.ebic_matrix_index_info(self._h, C.byref(nb), C.byref(used)))
+        return int(nb.value), bool(used.value)
+
     def prepare(self, approx: float) -> None:
         """Build the rank plane for `approx` now (otherwise built on first use)."""
         check(self._L.ebic_matrix_prepare(self._h, float(approx)))

@@ -10,16 +10,19 @@ from conftest import golden_cases, load_golden
 from paper_2105_01196_b200 import (EBIC_STORE_AUTO, EBIC_STORE_F32, EBIC_STORE_F64, EbicError, Population,
                                    TrendParams)
 from paper_2105_01196_b200 import synth
-from paper_2105_01196_b200._lib import EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE
+from paper_2105_01196_b200._lib import (EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32, EBIC_PATH_TABLE,
+                                        EBIC_PATH_VALUE)
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=[EBIC_PATH_AUTO, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE], ids=["plane", "plane_u32", "value"])
+@pytest.fixture(params=[EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE],
+                ids=["table", "plane", "plane_u32", "value"])
 def path_evaluator(evaluator, request):
-    """The same checks on every exact evaluation path: the default rank-plane
-    kernels (packed 16-bit rank pairs where the slab fits), the 32-bit-word
-    plane kernel, and the float value kernel."""
+    """The same checks on every exact evaluation path: the default (the
+    pair-trend index where it fits), the rank-plane slab kernels (packed 16-bit
+    rank pairs where the slab fits), the 32-bit-word plane kernel, and the
+    float value kernel."""
     evaluator.set_path(request.param)
     yield evaluator
     evaluator.set_path(EBIC_PATH_AUTO)
@@ -436,6 +439,7 @@ def test_every_pair_layout(evaluator, layout, n_cols):
     seqs += [np.sort(rng.choice(n_cols, size=min(L, n_cols), replace=False)) for L in (8, 12, 30)]
     pop = Population.from_sequences(seqs)
     evaluator.upload(m)
+    evaluator.set_path(EBIC_PATH_PLANE)
     evaluator.set_pair_layout(*layout)
     try:
         for approx, neg in ((0.03, False), (0.0, True), (0.3, True)):
@@ -444,6 +448,7 @@ def test_every_pair_layout(evaluator, layout, n_cols):
             np.testing.assert_array_equal(got, want, err_msg=f"C={n_cols} layout={layout} approx={approx} neg={neg}")
     finally:
         evaluator.set_pair_layout(0, 0)
+        evaluator.set_path(EBIC_PATH_AUTO)
 
 
 def _pinned_u32(a):
@@ -498,3 +503,63 @@ def test_zero_copy_host_path(evaluator, layout, path):
         np.testing.assert_array_equal(evaluator.evaluate_population(ppop, TrendParams(), out=out), want)
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
+
+
+
+@pytest.mark.parametrize("R", [1, 31, 32, 33, 127, 1000, 1037, 4099])
+@pytest.mark.parametrize("n_cols", [2, 37, 300])
+def test_pair_trend_index_vs_oracle(evaluator, R, n_cols):
+    """The pair-trend index (forced) against the C oracle: ragged row counts
+    (partial words and pair vectors), tiny and mid widths, duplicate columns,
+    length-1 and long candidates, negatives, several approx values; row masks
+    (supporting_rows) from the same index."""
+    rng = np.random.default_rng(R * 1000 + n_cols)
+    m = rng.standard_normal((R, n_cols)).astype(np.float32)
+    m[: R // 3] = np.sort(m[: R // 3], axis=1)
+    m[rng.random(m.shape) < 0.05] = 0.0
+    seqs = [rng.choice(n_cols, size=int(rng.integers(1, min(n_cols, 9) + 1)), replace=False) for _ in range(600)]
+    seqs += [rng.integers(0, n_cols, size=int(rng.integers(2, 6))) for _ in range(50)]  # duplicates allowed
+    seqs += [np.sort(rng.choice(n_cols, size=min(n_cols, 40), replace=False))]
+    pop = Population.from_sequences(seqs)
+    evaluator.upload(m)
+    evaluator.set_path(EBIC_PATH_TABLE)
+    try:
+        for approx, neg in ((0.03, False), (0.0, True), (0.25, True), (0.03, True)):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(pop, TrendParams(approx=approx, negative_trends=neg))
+            np.testing.assert_array_equal(got, want, err_msg=f"R={R} C={n_cols} approx={approx} neg={neg}")
+        for j in (0, 7, len(pop) - 1):
+            for approx, neg in ((0.03, False), (0.1, True)):
+                rows = evaluator.supporting_rows(pop.sequence(j), TrendParams(approx, neg))
+                np.testing.assert_array_equal(rows, oracle.supporting_rows(m, pop.sequence(j), approx, neg))
+        assert evaluator.index_info()[1]
+    finally:
+        evaluator.set_path(EBIC_PATH_AUTO)
+
+
+def test_pair_trend_index_budget_and_fallback(evaluator):
+    """AUTO builds the index only within the budget; below it the slab kernels
+    run (same counts); the index is rebuilt per approx and per matrix."""
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((2000, 120)).astype(np.float32)
+    pop = synth.random_population(800, 120, seed=9)
+    evaluator.upload(m)
+    need, built = evaluator.index_info()
+    assert need == 120 * 120 * 64 * 4 and not built  # wp = round_up(ceil(2000/32), 4) = 64 words
+    try:
+        evaluator.set_table_budget(need - 1)
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams()), want)
+        assert not evaluator.index_info()[1]
+        evaluator.set_table_budget(1 << 40)
+        for approx in (0.03, 0.2, 0.0, 0.03):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, True)
+            np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, True)), want)
+            assert evaluator.index_info()[1]
+        m2 = m[:, ::-1].copy()
+        evaluator.upload(m2)
+        assert not evaluator.index_info()[1]
+        want = oracle.evaluate_population(m2, pop.cols, pop.offsets, 0.03, False)
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams()), want)
+    finally:
+        evaluator.set_table_budget(24 << 30)
