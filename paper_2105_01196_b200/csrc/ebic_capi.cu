@@ -172,7 +172,7 @@ struct ebic_ctx {
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
   int chunk_groups = 1;   // EBIC_CHUNK_GROUPS: slab_pair_kernel CTAs in per-chunk groups (1) or linear units (0)
   int table_align = 4;     // EBIC_TABLE_ALIGN: pair-vector length granule in words (A/B)
-  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto, 1 warp per candidate, 2 CTA per candidate (A/B)
+  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (warp per candidate up to 256 slices), 2 CTA per candidate (A/B)
   int pair_kernel = 1;    // EBIC_PAIR_KERNEL: 1 position-indexed counts (slab_pair_kernel), 0 slab_simd_kernel (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
 };

@@ -190,8 +190,10 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
 // ceil(nv / 32) of them, a template parameter so the accumulators live in
 // registers) and issues all J loads of a pair before combining them.  Same
 // outputs and error codes as table_count_kernel.  (Measured on B200: batching
-// several pairs' loads or prefetching the next candidate costs more in
-// registers / occupancy than it gains at these sizes.)
+// several candidates per warp, several pairs' loads in flight, or prefetching
+// the next candidate cost more in registers / occupancy than they gain; the
+// kernel runs at 70-90% of the random-2.5-KB-chunk read ceiling measured by
+// scripts/microbench/random_chunks.cu.)
 template <int J, bool NEG, bool MASK>
 __global__ void __launch_bounds__(256)
 table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
