@@ -19,11 +19,18 @@ done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c3_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
 for c in c3 c2 c4 c5; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slab_" -s 5 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slab_|table_count" -s 5 -c 1 \
       -o $OUT/prof_${c}_$TAG -f python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_${c}_$TAG.log 2>&1
 done
 for c in c2 c4 c5; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_${c}_$TAG.json 2> $OUT/bench_${c}_$TAG.err
 done
+# the slab kernel (no index) on c3 for comparison, and its ncu capture
+timeout 600 python bench.py --config c3 --path plane --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c3_plane_$TAG.json 2> $OUT/bench_c3_plane_$TAG.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slab_" -s 5 -c 1 \
+    -o $OUT/prof_c3_plane_$TAG -f python bench.py --config c3 --path plane --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_c3_plane_$TAG.log 2>&1
+# index build kernel
+timeout 900 ncu --set full --clock-control none -k regex:"build_pair_table" -c 1 \
+    -o $OUT/prof_c3_build_$TAG -f python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 python scripts/run_e2e.py > $OUT/run_e2e_$TAG.txt 2>&1
 echo done

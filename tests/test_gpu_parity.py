@@ -563,3 +563,47 @@ def test_pair_trend_index_budget_and_fallback(evaluator):
         np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams()), want)
     finally:
         evaluator.set_table_budget(24 << 30)
+
+
+@pytest.mark.parametrize("layout", ["separate", "one_block"])
+def test_zero_copy_pipelined_pieces(evaluator, layout):
+    """Large page-locked populations go over in pieces while earlier pieces are
+    evaluated (index path): counts and errors as the single-shot path, for
+    ragged piece boundaries and long candidates."""
+    rng = np.random.default_rng(99)
+    m = rng.standard_normal((5000, 300)).astype(np.float32)
+    m[:800] = np.sort(m[:800], axis=1)
+    seqs = [rng.choice(300, size=int(rng.integers(1, 12)), replace=False) for _ in range(9001)]
+    seqs[4500] = np.sort(rng.choice(300, size=60, replace=False))
+    pop = Population.from_sequences(seqs)
+    evaluator.upload(m)
+    keep = []
+    if layout == "one_block":
+        t, buf = _pinned_u32(np.concatenate([pop.offsets, pop.cols]))
+        keep.append(t)
+        ppop = Population(buf[pop.offsets.size:], buf[: pop.offsets.size])
+    else:
+        (t1, c), (t2, o) = _pinned_u32(pop.cols), _pinned_u32(pop.offsets)
+        keep += [t1, t2]
+        ppop = Population(c, o)
+    t3, out = _pinned_u32(np.zeros(len(pop), np.uint32))
+    keep.append(t3)
+    for approx, neg in ((0.03, False), (0.1, True)):
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+        np.testing.assert_array_equal(evaluator.evaluate_population(ppop, TrendParams(approx, neg), out=out), want)
+    assert evaluator.index_info()[1]
+    # a bad column in the last piece and an empty candidate in the first
+    bad = ppop.cols.copy()
+    bad[-1] = 300
+    tb, bc = _pinned_u32(bad)
+    keep.append(tb)
+    with pytest.raises(EbicError, match="out of range"):
+        evaluator.evaluate_population(Population(bc, ppop.offsets), TrendParams(), out=out)
+    offs = ppop.offsets.copy()
+    offs[3] = offs[2]
+    to, bo = _pinned_u32(offs)
+    keep.append(to)
+    with pytest.raises(EbicError, match="empty"):
+        evaluator.evaluate_population(Population(ppop.cols, bo), TrendParams(), out=out)
+    want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
+    np.testing.assert_array_equal(evaluator.evaluate_population(ppop, TrendParams(), out=out), want)
