@@ -429,7 +429,7 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
   bool found = false;
   if (!mask && ctx->path != EBIC_PATH_PLANE_U32) {
     // packed pairs: the first layout (in measured order of speed on B200, see
-    // profiles/r1_layout_ab.txt) whose slab fits in 128 KB.  The other
+    // profiles/r1b_layout_ab.txt) whose slab fits in 128 KB.  The other
     // layouts are reachable through ebic_ctx_set_pair_layout.
     // (P = 4 would need > 64 registers per thread at 1024 threads: spills)
     struct Opt { int p, sub; uint32_t rt; };
@@ -518,7 +518,7 @@ ebic::SlabArgs make_slab_args(const ebic_ctx* ctx, const SlabCfg& cfg, const uin
   a.mask_wpc = ctx->ld / 32;
   a.err = ctx->d_err;
   // L2 prefetch of the next slab (EBIC_PREFETCH=0/1 forces it).  Measured on
-  // B200 (profiles/r1_ab_prefetch.txt): +4% when the plane is L2-resident
+  // B200 (profiles/archive/r1_ab_prefetch.txt): +4% when the plane is L2-resident
   // (20k x 1000, 80 MB), -5% when it streams from HBM (200k x 2000, 1.6 GB,
   // where the extra requests compete with other chunks' reuse of the same
   // slabs).  Default: on iff the plane fits comfortably in the 126 MB L2.

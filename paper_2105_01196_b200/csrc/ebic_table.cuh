@@ -30,13 +30,14 @@ constexpr int kTableRowsPerCta = 1024;  // rows per builder CTA (32 words)
 
 // Builder: CTA (row block rb, a-tile) -- warp w owns column a = a0 + w and keeps
 // the threshold keys of its 1024 rows in registers (lane l, i: row 32 i + l);
-// the CTA streams W_b blocks of every column b through double-buffered shared
-// memory.  Word i of B(a, b) is one ballot over the warp; lane i keeps it, so
+// the CTA streams W_b blocks of every column b through shared memory (two
+// columns per barrier, the next two already loading into registers).  Word i
+// of B(a, b) is one ballot over the warp; lane i keeps it, so
 // the 32 words of a pair vector leave as one coalesced 128-byte store.
 __global__ void __launch_bounds__(kTableBuildWarps * 32)
 build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
                         uint32_t wp, uint32_t* __restrict__ table) {
-  __shared__ uint32_t s_wb[2][kTableRowsPerCta];
+  __shared__ uint32_t s_wb[2][2][kTableRowsPerCta];  // [iteration parity][column of the pair][row]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r0 = blockIdx.x * kTableRowsPerCta;
   const uint32_t a = blockIdx.y * kTableBuildWarps + warp;
@@ -48,23 +49,36 @@ build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_
     // rows past the matrix never pass: no 32-bit word exceeds 0xFFFFFFFF
     ka[i] = (a_ok && r < n_rows) ? plane_key(__ldg(plane + (uint64_t)a * ld + r)) : 0xFFFFFFFFu;
   }
-  auto stage = [&](uint32_t b, int buf) {
-    const uint32_t r = r0 + threadIdx.x;
-    s_wb[buf][threadIdx.x] = r < n_rows ? __ldg(plane + (uint64_t)b * ld + r) : 0u;
+  // W_b blocks, two columns per barrier, register double-buffered: the loads
+  // of the next two columns are in flight while the current two are compared
+  const uint32_t r = r0 + threadIdx.x;
+  auto fetch = [&](uint32_t b) -> uint32_t {
+    return (b < n_cols && r < n_rows) ? __ldg(plane + (uint64_t)b * ld + r) : 0u;
   };
   const uint32_t w0 = r0 / 32;  // first word of this row block
-  stage(0, 0);
-  for (uint32_t b = 0; b < n_cols; ++b) {
-    __syncthreads();  // s_wb[b & 1] staged; s_wb[(b + 1) & 1] no longer read
-    if (b + 1 < n_cols) stage(b + 1, (b + 1) & 1);
-    const uint32_t* wb = s_wb[b & 1];
-    uint32_t word = 0;
+  uint32_t n0 = fetch(0), n1 = fetch(1);
+  int par = 0;
+  for (uint32_t b = 0; b < n_cols; b += 2, par ^= 1) {
+    // one barrier per two columns: the buffers alternate between iterations,
+    // so writing this pair never races the previous pair's readers
+    s_wb[par][0][threadIdx.x] = n0;
+    s_wb[par][1][threadIdx.x] = n1;
+    __syncthreads();
+    n0 = fetch(b + 2);
+    n1 = fetch(b + 3);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const uint32_t bits = __ballot_sync(kFull, wb[32 * i + lane] > ka[i]);
-      if (lane == i) word = bits;
+    for (int h = 0; h < 2; ++h) {
+      if (b + h < n_cols) {
+        const uint32_t* wb = s_wb[par][h];
+        uint32_t word = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t bits = __ballot_sync(kFull, wb[32 * i + lane] > ka[i]);
+          if (lane == i) word = bits;
+        }
+        if (a_ok && w0 + lane < wp) table[((uint64_t)a * n_cols + b + h) * wp + w0 + lane] = word;
+      }
     }
-    if (a_ok && w0 + lane < wp) table[((uint64_t)a * n_cols + b) * wp + w0 + lane] = word;
   }
 }
 

@@ -33,4 +33,15 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sla
 timeout 900 ncu --set full --clock-control none -k regex:"build_pair_table" -c 1 \
     -o $OUT/prof_c3_build_$TAG -f python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 python scripts/run_e2e.py > $OUT/run_e2e_$TAG.txt 2>&1
-echo done
+
+# keep gpurun_out under the 64 MiB merge cap: raw-page CSVs of every capture,
+# the .ncu-rep files only for the C3 kernels
+for f in $OUT/prof_*_$TAG.ncu-rep; do
+  [ -f "$f" ] || continue
+  ncu -i "$f" --page raw --csv > "${f%.ncu-rep}.raw.csv" 2>/dev/null
+  case "$f" in
+    *prof_c3_$TAG.ncu-rep|*prof_c3_plane_$TAG.ncu-rep) ;;
+    *) rm -f "$f" ;;
+  esac
+done
+du -sh $OUT

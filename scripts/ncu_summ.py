@@ -1,6 +1,9 @@
 import csv, subprocess, sys
-rep = sys.argv[1]
-out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+rep = sys.argv[1]  # an .ncu-rep, or the --page raw --csv export of one
+if rep.endswith('.csv'):
+    out = open(rep).read()
+else:
+    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
 h = r[0]; u = r[1]
 want = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'lts__t_bytes.sum',
