@@ -325,6 +325,8 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     flush_sink = torch.empty((), dtype=torch.float32, device=dev)
 
     def flush_l2():
+        if os.environ.get("EBIC_BENCH_NO_FLUSH"):  # experiments only (L2-warm inputs)
+            return
         torch.sum(flush, dim=0, out=flush_sink)
 
     def step(i, ev_k0=None, ev_k1=None):

@@ -176,7 +176,6 @@ struct ebic_ctx {
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
   int chunk_groups = 1;   // EBIC_CHUNK_GROUPS: slab_pair_kernel CTAs in per-chunk groups (1) or linear units (0)
-  int table_align = 4;     // EBIC_TABLE_ALIGN: pair-vector length granule in words (A/B)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (warp per candidate up to 256 slices), 2 CTA per candidate (A/B)
   int pair_kernel = 1;    // EBIC_PAIR_KERNEL: 1 position-indexed counts (slab_pair_kernel), 0 slab_simd_kernel (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
@@ -286,9 +285,12 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
 // ---- pair-trend index ------------------------------------------------------
 constexpr int kTableNoMemory = -1;  // internal status: the index does not fit (fall back)
 
+// Words per pair vector: a multiple of 4 (uint4 slices); vectors of more than
+// 32 slices are padded to a multiple of 32 slices, so the warp kernel's lanes
+// own exactly J = nv / 32 slices each (unpredicated loads).
 uint64_t table_wp(const ebic_ctx* ctx) {
-  const uint64_t al = (uint64_t)ctx->table_align;  // words; a multiple of 4 (uint4 vectors)
-  return ((ctx->n_rows + 31) / 32 + al - 1) / al * al;
+  const uint64_t words = (ctx->n_rows + 31) / 32;
+  return words > 128 ? (words + 127) / 128 * 128 : (words + 3) / 4 * 4;
 }
 uint64_t table_bytes(const ebic_ctx* ctx) { return ctx->n_cols * ctx->n_cols * table_wp(ctx) * sizeof(uint32_t); }
 
@@ -903,8 +905,6 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (cg) ctx->chunk_groups = std::atoi(cg) ? 1 : 0;
     const char* tb = std::getenv("EBIC_TABLE_BUDGET_MB");
     if (tb) ctx->table_budget_user = (uint64_t)std::strtoull(tb, nullptr, 10) << 20;
-    const char* ta = std::getenv("EBIC_TABLE_ALIGN");
-    if (ta) ctx->table_align = std::max(4, std::atoi(ta) / 4 * 4);
     const char* hp = std::getenv("EBIC_HOST_PIECES");
     if (hp) ctx->pipeline_pieces = std::max(1, std::min(4, std::atoi(hp)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");

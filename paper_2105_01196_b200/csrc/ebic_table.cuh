@@ -149,10 +149,17 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
           const uint4* rev = t4 + ((uint64_t)pc[g + 1] * n_cols + pc[g]) * nv;
 #pragma unroll
           for (int u = 0; u < J; ++u) {
-            const uint32_t v = v0 + u * T + t;
-            const bool ok = live && v < nv;
-            x[g][u] = ok ? __ldg(fwd + v) : make_uint4(~0u, ~0u, ~0u, ~0u);
-            if (NEG) y[g][u] = ok ? __ldg(rev + v) : make_uint4(~0u, ~0u, ~0u, ~0u);
+            // unconditional loads (see table_count_warp_kernel): a dead pair
+            // re-reads the live pair-0 vector and its result is discarded
+            const uint32_t v = min(v0 + u * T + t, nv - 1);
+            const uint4* src = live ? fwd : t4 + ((uint64_t)pc[0] * n_cols + pc[1]) * nv;
+            const uint4* srr = live ? rev : t4 + ((uint64_t)pc[1] * n_cols + pc[0]) * nv;
+            const uint4 a = __ldg(src + v);
+            x[g][u] = live ? a : make_uint4(~0u, ~0u, ~0u, ~0u);
+            if (NEG) {
+              const uint4 c = __ldg(srr + v);
+              y[g][u] = live ? c : make_uint4(~0u, ~0u, ~0u, ~0u);
+            }
           }
         }
 #pragma unroll
@@ -250,14 +257,20 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
     uint32_t cp = __shfl_sync(kFull, c_lane, 0);
     for (uint32_t k = 1; k < L; ++k) {
       const uint32_t cc = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : __ldg(cols + b + k);
-      const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv;
-      const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv;
+      // all J loads unconditional, at immediate offsets from one base, so they
+      // issue back to back (a predicated load lets ptxas reuse one destination
+      // register and serialise the J round trips).  The host pads vectors of
+      // more than 32 slices to a multiple of 32 (nv == 32 J); below that the
+      // lanes past the vector re-read its last slice (same line; their
+      // accumulators start at 0)
+      const uint32_t lv = J == 1 ? min((uint32_t)lane, nv - 1) : (uint32_t)lane;
+      const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv + lv;
+      const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv + lv;
       uint4 x[J], y[J];
 #pragma unroll
       for (int u = 0; u < J; ++u) {
-        const uint32_t v = u * 32 + lane;
-        x[u] = v < nv ? __ldg(fwd + v) : make_uint4(0u, 0u, 0u, 0u);
-        if (NEG) y[u] = v < nv ? __ldg(rev + v) : make_uint4(0u, 0u, 0u, 0u);
+        x[u] = __ldg(fwd + u * 32);
+        if (NEG) y[u] = __ldg(rev + u * 32);
       }
 #pragma unroll
       for (int u = 0; u < J; ++u) {

@@ -22,6 +22,36 @@ __global__ void chunk_read(const uint4* __restrict__ buf, const uint32_t* __rest
   if (acc == 0x12345678u) atomicAdd(sink, 1ull);
 }
 
+// the index kernel's shape: a warp ANDs G chunks (one candidate's pairs);
+// DEP: the chunks are read one after another (the next load waits for the
+// AND), else all G chunks' loads are issued before combining
+template <int G, bool DEP>
+__global__ void chunk_and(const uint4* __restrict__ buf, const uint32_t* __restrict__ idx, uint32_t n_groups,
+                          uint32_t chunk_v4, unsigned long long* sink) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_groups) return;
+  uint32_t acc = 0;
+  for (uint32_t v = lane; v < chunk_v4; v += 32) {
+    uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (DEP) {
+      for (int g = 0; g < G; ++g) {
+        const uint4 x = __ldg(buf + (uint64_t)idx[w * G + g] * chunk_v4 + v);
+        f.x &= x.x; f.y &= x.y; f.z &= x.z; f.w &= x.w;
+        if (f.x == 0x9u) break;  // data-dependent: the next load waits for this one
+      }
+    } else {
+      uint4 x[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) x[g] = __ldg(buf + (uint64_t)idx[w * G + g] * chunk_v4 + v);
+#pragma unroll
+      for (int g = 0; g < G; ++g) { f.x &= x[g].x; f.y &= x[g].y; f.z &= x[g].z; f.w &= x[g].w; }
+    }
+    acc += __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
 int main() {
   const size_t total = 2560ull << 20;  // 2.5 GiB buffer
   uint4* buf;
@@ -64,6 +94,30 @@ int main() {
     }
     cudaFree(d);
     cudaFree(ds);
+  }
+  {  // 2560-B chunks, groups of 3 per warp (a length-4 candidate), dependent vs batched
+    const uint32_t chunk = 2560, n = (uint32_t)(read_bytes / chunk) / 3 * 3, n_slots = (uint32_t)(total / chunk);
+    std::vector<uint32_t> h(n);
+    for (auto& x : h) x = rng() % n_slots;
+    uint32_t* d;
+    cudaMalloc(&d, n * 4);
+    cudaMemcpy(d, h.data(), n * 4, cudaMemcpyHostToDevice);
+    for (int mode = 0; mode < 2; ++mode) {
+      float best = 1e9f;
+      for (int rep = 0; rep < 8; ++rep) {
+        cudaMemset(buf, rep, 256ull << 20);
+        cudaEventRecord(e0);
+        if (mode) chunk_and<3, false><<<(n / 3 + 7) / 8, 256>>>(buf, d, n / 3, chunk / 16, sink);
+        else chunk_and<3, true><<<(n / 3 + 7) / 8, 256>>>(buf, d, n / 3, chunk / 16, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+      }
+      printf("chunk %6u B x3 per warp %-9s %8u chunks: %.4f ms  %.0f GB/s\n", chunk, mode ? "batched" : "dependent", n,
+             best, n * (double)chunk / (best * 1e-3) / 1e9);
+    }
   }
   return 0;
 }
