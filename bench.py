@@ -15,9 +15,15 @@ of its numeric targets (>= 60% HBM roofline at 20k x 1000; >= 6x at 8 GPUs
 row-sharded) are quoted on this configuration; configs[1] is the bit-exact
 parity case (tests/test_gpu_parity.py::test_config2_bit_exact).
 
-N > 1 (torchrun, one process per GPU): rows are sharded across ranks and the
-per-candidate partial counts are summed with one NCCL all_reduce per step
-(strong scaling: the total work is fixed).
+N > 1 (torchrun, one process per GPU), --shard:
+  replica (default) -- candidates are independent, so the units are partitioned
+           with no data-path collective: every rank evaluates its own P-candidate
+           population against the replicated matrix (weak scaling; value = the
+           whole job's N*P evals per step / the slowest rank's step time).
+  rows     -- matrix rows sharded; every rank evaluates the whole population on
+           its shard and the partial counts are summed with one NCCL all_reduce
+           per step (strong scaling; for matrices too large to replicate).
+  pop      -- one population split across ranks, counts all-gathered (strong).
 
 value    : device-resident inputs (population CSR already in HBM), per-step CUDA
            events on the launching stream around kernel + all_reduce; L2 is
@@ -170,14 +176,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": "nvml, ~1 ms polling"}
 
 
-def make_inputs(cfg, n_pops: int):
+def make_inputs(cfg, n_pops: int, seed0: int = 42):
     from paper_2105_01196_b200 import synth
 
     m, _ = synth.planted_trend_matrix(cfg["rows"], cfg["cols"], 3, cfg["bic"][0], cfg["bic"][1], seed=1)
     if cfg["len_min"] == cfg["len_max"]:
-        pops = [synth.exact_len_population(cfg["pop"], cfg["cols"], cfg["len_min"], seed=42 + i) for i in range(n_pops)]
+        pops = [synth.exact_len_population(cfg["pop"], cfg["cols"], cfg["len_min"], seed=seed0 + i)
+                for i in range(n_pops)]
     else:
-        pops = [synth.random_population(cfg["pop"], cfg["cols"], cfg["len_min"], cfg["len_max"], seed=42 + i)
+        pops = [synth.random_population(cfg["pop"], cfg["cols"], cfg["len_min"], cfg["len_max"], seed=seed0 + i)
                 for i in range(n_pops)]
     return m, pops
 
@@ -289,7 +296,9 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     dev = torch.device("cuda", local_rank)
     tp = TrendParams(approx=cfg["approx"], negative_trends=cfg["negative"])
     n_pops = 4
-    m, pops = make_inputs(cfg, n_pops)
+    # replica mode: every rank evaluates its OWN populations (different seeds)
+    replica = args.shard == "replica" and world > 1
+    m, pops = make_inputs(cfg, n_pops, seed0=42 + (1000 * rank if replica else 0))
     R, Ccols, P = cfg["rows"], cfg["cols"], cfg["pop"]
     b, e = row_range(R, rank, world) if args.shard == "rows" else (0, R)
 
@@ -337,7 +346,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp, stream=stream.cuda_stream)
         if ev_k1 is not None:
             ev_k1.record(stream)
-        if world > 1:
+        if world > 1 and not replica:
             if args.shard == "rows":
                 dist.all_reduce(counts_full, op=dist.ReduceOp.SUM)
             else:
@@ -380,7 +389,8 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = P / (ms_per_step / 1e3)
+    p_total = P * world if replica else P  # candidates evaluated per step by the whole job
+    value = p_total / (ms_per_step / 1e3)
 
     # roofline of the fitness kernel on this rank
     sum_len = [int(dp[3]) for dp in d_pops]
@@ -398,7 +408,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
 
     # ---- e2e through the public host API -----------------------------------
     e2e_ms = []
-    if world > 1:
+    if world > 1 and not replica:
         sev = ShardedEvaluator(ev, m, mode=args.shard, dist=dist)
         call = sev.evaluate_population
     else:
@@ -442,7 +452,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_tot = float(t.item())
-    e2e_value = P / (e2e_tot / args.steps / 1e3)
+    e2e_value = p_total / (e2e_tot / args.steps / 1e3)
     pop0 = pops[0]
     h2d = int(pop0.cols.nbytes + pop0.offsets.nbytes)
     d2h = 4 * P
@@ -454,16 +464,21 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     dev_counts = counts_full.cpu().numpy().view(np.uint32)
     ev.set_stream(None)
     host0 = call(pops[0], tp)
-    parity_dev_vs_host = bool(np.array_equal(dev_counts[:len(host0)], host0)) if args.shard == "rows" else None
+    parity_dev_vs_host = (bool(np.array_equal(dev_counts[:len(host0)], host0))
+                          if (args.shard == "rows" or replica) else None)
 
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if args.shard == "rows" else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "weak" if args.shard in ("replica", "pop") else "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "row_checks_per_s": value * R,
         "config": {"workload": cfg["label"], "rows": R, "cols": Ccols, "population": P,
-                   "parallelism": f"{args.shard}-sharded x{world}" if world > 1 else "1 GPU",
+                   "population_per_step_total": p_total,
+                   "parallelism": ("1 GPU" if world == 1 else
+                                   f"population-sharded x{world}: every rank evaluates its own {P}-candidate "
+                                   f"population against the replicated matrix, no collective (weak)" if replica
+                                   else f"{args.shard}-sharded x{world}"),
                    "l2": "flushed before every timed step (512 MiB device read, outside the step events)",
                    "shard": args.shard, "path": args.path},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -484,7 +499,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                              "the matrix is re-read from L2 by many candidates, so achieved can exceed HBM peak"},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_tot / args.steps,
-                "api": "ebic_eval_counts (Evaluator.evaluate_population), pinned host arrays" if world == 1
+                "api": "ebic_eval_counts (Evaluator.evaluate_population), pinned host arrays" if (world == 1 or replica)
                        else f"ShardedEvaluator({args.shard}) over ebic_eval_counts + NCCL"},
         "gpu_launches": int(launches),
         "store": {"upload_ms": upload_ms, "index_build_ms": prepare_ms,
@@ -524,7 +539,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--shard", choices=["rows", "pop"], default="rows")
+    ap.add_argument("--shard", choices=["replica", "rows", "pop"], default="replica",
+                    help="N > 1: replica = every rank evaluates its own population on the replicated matrix, "
+                         "no collective (weak scaling, the default: candidates are independent); rows = matrix "
+                         "rows sharded, NCCL all_reduce of the partial counts (strong); pop = one population "
+                         "split across ranks + all_gather (strong)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="collective backend for N > 1 (gloo lets N ranks share one GPU to test the sharded path)")

@@ -12,7 +12,7 @@ timeout 1500 python -m pytest tests -q -m gpu -rs > $OUT/pytest_gpu_$TAG.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke exit $?" >> $OUT/smoke_$TAG.log
 timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-for sh in rows pop; do
+for sh in replica rows pop; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 \
       bench.py --gpus 2 --steps 5 --warmup 3 --backend gloo --shard $sh > $OUT/bench_gloo2_${sh}_$TAG.json 2> $OUT/bench_gloo2_${sh}_$TAG.err
 done
