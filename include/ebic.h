@@ -182,9 +182,9 @@ int ebic_ctx_set_path(ebic_ctx* ctx, int path);
  * benchmarking. */
 int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_per_warp);
 
-/* Memory budget of the pair-trend index (bytes; default 24 GiB, env
+/* Memory budget of the pair-trend index (bytes; default 128 GiB, env
  * EBIC_TABLE_BUDGET_MB); AUTO uses the index only if it needs <= min(budget,
- * free device memory / 2 at upload). */
+ * free device memory at upload minus a reserve of max(8 GiB, 10%)). */
 int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes);
 /* Bytes the pair-trend index of the resident matrix needs (0 if the matrix is
  * too wide for the rank plane) and whether it is built. */

@@ -168,7 +168,7 @@ struct ebic_ctx {
   bool table_valid = false, table_failed = false;
   double table_approx = 0.0;
   uint64_t table_budget = 0;
-  uint64_t table_budget_user = 24ull << 30;  // ebic_ctx_set_table_budget / EBIC_TABLE_BUDGET_MB
+  uint64_t table_budget_user = 128ull << 30;  // ebic_ctx_set_table_budget / EBIC_TABLE_BUDGET_MB
   double plane_approx = 0.0;
   int path = EBIC_PATH_AUTO;
   int n_sms = 148;
@@ -283,6 +283,14 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
 }
 
 // ---- pair-trend index ------------------------------------------------------
+// Device memory the index may take out of `free_bytes`: all but a reserve of
+// max(8 GiB, 10%) for the caller's own buffers (a B200 has 180 GB of HBM: a
+// 100-GB index for a 200k x 2000 matrix fits next to everything else).
+uint64_t index_headroom(uint64_t free_bytes) {
+  const uint64_t reserve = std::max<uint64_t>(8ull << 30, free_bytes / 10);
+  return free_bytes > reserve ? free_bytes - reserve : 0;
+}
+
 constexpr int kTableNoMemory = -1;  // internal status: the index does not fit (fall back)
 
 // Words per pair vector: a multiple of 4 (uint4 slices); vectors of more than
@@ -813,7 +821,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
       cudaGetLastError();
       fr = 0;
     }
-    ctx->table_budget = std::min<uint64_t>(ctx->table_budget_user, fr / 2);
+    ctx->table_budget = std::min<uint64_t>(ctx->table_budget_user, index_headroom(fr));
   }
   if (store_out) *store_out = chosen;
   return EBIC_OK;
@@ -1370,7 +1378,7 @@ int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes) {
       cudaGetLastError();
       fr = 0;
     }
-    ctx->table_budget = std::min<uint64_t>(bytes, fr / 2 + (ctx->d_table ? table_bytes(ctx) : 0));
+    ctx->table_budget = std::min<uint64_t>(bytes, index_headroom(fr + (ctx->d_table ? table_bytes(ctx) : 0)));
   }
   return EBIC_OK;
 }

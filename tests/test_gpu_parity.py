@@ -562,7 +562,7 @@ def test_pair_trend_index_budget_and_fallback(evaluator):
         want = oracle.evaluate_population(m2, pop.cols, pop.offsets, 0.03, False)
         np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams()), want)
     finally:
-        evaluator.set_table_budget(24 << 30)
+        evaluator.set_table_budget(128 << 30)
 
 
 @pytest.mark.parametrize("layout", ["separate", "one_block"])
