@@ -1,30 +1,61 @@
-"""Small workloads for compute-sanitizer (memcheck / racecheck / synccheck):
-every kernel family once -- upload (check + transpose), rank-plane build, both
-packed-pair and 32-bit slab kernels (+ MASK), value kernels (f32 filter, f64,
-native), row scatter, single-row check."""
+"""Small workloads for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): every kernel family once -- upload (check + transpose), rank-plane
+build, pair-trend index build + both index kernels (warp per candidate for
+short vectors, CTA per candidate for long; counts and MASK), the slab kernels
+(packed pairs with position-indexed counts, 32-bit plane words, + MASK), the
+value kernels (f32 filter, f64, native), row scatter, single-row check; the
+zero-copy host path (page-locked in/out), the marshaller and the device API."""
 import sys
 from pathlib import Path
 
 import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
 import oracle  # noqa: E402
 from paper_2105_01196_b200 import Evaluator, Population, TrendParams, synth  # noqa: E402
-from paper_2105_01196_b200._lib import EBIC_PATH_AUTO, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE  # noqa: E402
+from paper_2105_01196_b200._lib import (EBIC_PATH_AUTO, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32,  # noqa: E402
+                                        EBIC_PATH_TABLE, EBIC_PATH_VALUE)
+
+
+def pinned(a):
+    t = torch.empty(max(a.size, 1), dtype=torch.int32, pin_memory=True)
+    v = t.numpy().view(np.uint32)[: a.size]
+    v[:] = a
+    return t, v
+
 
 rng = np.random.default_rng(0)
 ev = Evaluator(0)
 ok = True
-for R, Cn in ((700, 40), (300, 700), (257, 1500)):
+keep = []
+for R, Cn in ((700, 40), (300, 700), (257, 1500), (40000, 12)):
     m = rng.standard_normal((R, Cn)).astype(np.float32)
-    pop = synth.random_population(200, Cn, 2, 9, seed=1)
-    for path in (EBIC_PATH_AUTO, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE):
+    pop = synth.random_population(200, Cn, 2, min(9, Cn), seed=1)
+    paths = (EBIC_PATH_AUTO, EBIC_PATH_TABLE, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE)
+    for path in paths if R < 40000 else (EBIC_PATH_TABLE,):
         ev.set_path(path)
         for mat in (m, m.astype(np.float64) + 1e-12):  # f32 store, then a non-f32-exact f64 store
             ev.upload(mat)
             for approx, neg in ((0.03, True), (0.0, False)):
-                got = ev.evaluate_population(pop, TrendParams(approx, neg))
-                ok &= np.array_equal(got, oracle.evaluate_population(mat, pop.cols, pop.offsets, approx, neg))
+                want = oracle.evaluate_population(mat, pop.cols, pop.offsets, approx, neg)
+                got = ev.evaluate_population(pop, TrendParams(approx, neg))  # marshaller (pageable)
+                ok &= np.array_equal(got, want)
+                # zero-copy host path: one page-locked [offsets | cols] block, page-locked output
+                tb, blk = pinned(np.concatenate([pop.offsets, pop.cols]))
+                to, out = pinned(np.zeros(len(pop), np.uint32))
+                keep += [tb, to]
+                ppop = Population(blk[pop.offsets.size:], blk[: pop.offsets.size])
+                ok &= np.array_equal(ev.evaluate_population(ppop, TrendParams(approx, neg), out=out), want)
+                # device API
+                d_c = torch.from_numpy(pop.cols.view(np.int32)).cuda()
+                d_o = torch.from_numpy(pop.offsets.view(np.int32)).cuda()
+                d_n = torch.zeros(len(pop), dtype=torch.int32, device="cuda")
+                ev.evaluate_population_device(d_c.data_ptr(), d_o.data_ptr(), len(pop), d_n.data_ptr(),
+                                              TrendParams(approx, neg))
+                ev.sync()
+                ok &= np.array_equal(d_n.cpu().numpy().view(np.uint32), want)
                 rows = ev.supporting_rows_batch(Population(pop.cols[:pop.offsets[5]], pop.offsets[:6]),
                                                 TrendParams(approx, neg))
                 ok &= all(np.array_equal(r, oracle.supporting_rows(mat, pop.sequence(i), approx, neg))
