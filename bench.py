@@ -495,8 +495,14 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                                   } if index_used else None),
                      "algorithmic_bytes_per_launch": statistics.mean(alg_bytes),
                      "peak_source": peak_src,
-                     "note": "algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "
-                             "the matrix is re-read from L2 by many candidates, so achieved can exceed HBM peak"},
+                     "note": ("algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once, "
+                              "SURVEY 8(d)); the pair-trend index kernel never reads the matrix -- it streams "
+                              "(L-1) x R/8 index bytes per eval -- so achieved/frac exceed the HBM peak; "
+                              "roofline.physical is that kernel's real HBM traffic over the same time "
+                              "(and roofline.traffic the ncu DRAM bytes per launch)") if index_used else
+                             ("algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "
+                              "the matrix is re-read from L2/shared memory by many candidates, so achieved can "
+                              "exceed the HBM peak")},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_tot / args.steps,
                 "api": "ebic_eval_counts (Evaluator.evaluate_population), pinned host arrays" if (world == 1 or replica)
