@@ -721,6 +721,13 @@ int validate_population(const ebic_ctx* ctx, const uint32_t* cols, const uint32_
                         uint64_t n_cand, bool check_cols = true) {
   if (n_cand && (!cols || !offsets)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null population pointer");
   if (n_cand && offsets[0] != 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "offsets[0] must be 0");
+  if (!check_cols) {
+    // branch-free (vectorisable) scan first; the detailed loop below only runs
+    // to name the first bad candidate
+    uint32_t bad = 0;
+    for (uint64_t i = 0; i < n_cand; ++i) bad |= offsets[i + 1] <= offsets[i] ? 1u : 0u;
+    if (!bad) return EBIC_OK;
+  }
   for (uint64_t i = 0; i < n_cand; ++i) {
     if (offsets[i + 1] <= offsets[i])
       return fail(EBIC_ERR_INVALID_ARGUMENT, "candidate %llu is empty or offsets decrease",
@@ -1223,13 +1230,15 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
       d_offs = ctx->d_tmp_offs.p;
       d_cols = ctx->d_tmp_cols.p;
     }
-    if (validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false) != EBIC_OK) {
+    bool direct = false;
+    EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
+    // the index kernel checks every candidate's offsets on device (increasing,
+    // within offsets[n_cand]); the other kernels need them checked here
+    if (!table && validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false) != EBIC_OK) {
       const std::string msg = g_last_error;
       cudaStreamSynchronize(s);  // the scratch buffers may be reused by the next call
       return fail(EBIC_ERR_INVALID_ARGUMENT, "%s", msg.c_str());
     }
-    bool direct = false;
-    EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
     if (direct) {
       EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, out_dev, err_dev, s, n_idx));
     } else {
@@ -1238,7 +1247,9 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
       EBIC_CUDA(cudaMemcpyAsync(counts_out, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     }
     EBIC_CUDA(cudaStreamSynchronize(s));
-    if (*(volatile int*)ctx->h_err1.p) return bad_column_error(ctx);
+    const int e = *(volatile int*)ctx->h_err1.p;
+    if (e == 2) return fail(EBIC_ERR_INVALID_ARGUMENT, "a candidate is empty or its offsets decrease");
+    if (e) return bad_column_error(ctx);
     return EBIC_OK;
   }
   uint64_t t = 0;
