@@ -311,6 +311,14 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     t0 = time.perf_counter()
     ev.prepare(cfg["approx"])
     prepare_ms = (time.perf_counter() - t0) * 1e3
+    # rows mode over peer memory: every rank's exchange window mapped into every
+    # rank (CUDA IPC handles exchanged once through the process group)
+    p2p = world > 1 and args.shard == "rows" and args.exchange == "p2p"
+    if p2p:
+        h = ev.xchg_create(world, rank, P)
+        handles = [None] * world
+        dist.all_gather_object(handles, h)
+        ev.xchg_open(handles)
     # a dedicated (non-default) stream: kernels, NCCL and the timing events all run on it
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -343,10 +351,15 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         out = counts_full[:n] if args.shard == "pop" else counts_full
         if ev_k0 is not None:
             ev_k0.record(stream)
-        ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp, stream=stream.cuda_stream)
+        if p2p:  # count kernel + the fused peer-memory sum (one call, two kernels)
+            ev.evaluate_population_rows_sum_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp,
+                                                   stream=stream.cuda_stream)
+        else:
+            ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp,
+                                          stream=stream.cuda_stream)
         if ev_k1 is not None:
             ev_k1.record(stream)
-        if world > 1 and not replica:
+        if world > 1 and not replica and not p2p:
             if args.shard == "rows":
                 dist.all_reduce(counts_full, op=dist.ReduceOp.SUM)
             else:
@@ -480,7 +493,9 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                                    f"population against the replicated matrix, no collective (weak)" if replica
                                    else f"{args.shard}-sharded x{world}"),
                    "l2": "flushed before every timed step (512 MiB device read, outside the step events)",
-                   "shard": args.shard, "path": args.path},
+                   "shard": args.shard, "path": args.path,
+                   "exchange": ("peer memory (fused sum kernel)" if p2p else "NCCL all_reduce")
+                   if (world > 1 and args.shard == "rows") else None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, world),
                      "kernel": ("table_count_kernel (pair-trend index)" if index_used else
@@ -550,6 +565,9 @@ def main():
                          "no collective (weak scaling, the default: candidates are independent); rows = matrix "
                          "rows sharded, NCCL all_reduce of the partial counts (strong); pop = one population "
                          "split across ranks + all_gather (strong)")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="rows mode: sum the partial counts over peer memory (exchange windows mapped with "
+                         "CUDA IPC, one fused kernel) or with an NCCL all_reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="collective backend for N > 1 (gloo lets N ranks share one GPU to test the sharded path)")

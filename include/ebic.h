@@ -195,6 +195,33 @@ int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use);
  * per-(matrix, approx) index: a GA run uses one approx for all generations. */
 int ebic_matrix_prepare(ebic_ctx* ctx, double approx);
 
+/* ---- row-sharded step: count reduction over peer memory -----------------
+ * Row sharding (rank g holds rows [g*R/G, (g+1)*R/G)) needs the G partial
+ * counts of every candidate summed.  Instead of an NCCL all_reduce, each rank
+ * owns an exchange window in its HBM that every peer maps (CUDA IPC over
+ * NVLink / NVSwitch); one kernel pushes this rank's partial counts into every
+ * rank's window, signals, waits for all ranks and sums (ebic_xchg.cuh).
+ * Sequence per rank: ebic_xchg_create -> exchange the handles (e.g.
+ * torch.distributed all_gather_object) -> ebic_xchg_open -> every step
+ * ebic_eval_counts_rows_sum (all ranks, same order).  ebic_xchg_open_local
+ * maps windows of contexts in the SAME process instead (device pointers from
+ * ebic_xchg_window).  A rank that never arrives makes the kernel give up after
+ * ~2 s; the next ebic_ctx_sync reports it.  Ranks sharing one GPU (tests) must
+ * build their index first (ebic_matrix_prepare): a device allocation inside a
+ * step can wait for the device to go idle, i.e. for a peer's spinning kernel. */
+#define EBIC_IPC_HANDLE_BYTES 64
+#define EBIC_XCHG_MAX_RANKS 16
+int ebic_xchg_create(ebic_ctx* ctx, int world, int rank, uint64_t max_cand, void* handle_out);
+int ebic_xchg_open(ebic_ctx* ctx, const void* handles /* world x EBIC_IPC_HANDLE_BYTES, rank order */);
+int ebic_xchg_open_local(ebic_ctx* ctx, void* const* windows /* world device pointers, rank order */);
+int ebic_xchg_window(ebic_ctx* ctx, void** window_out);
+int ebic_xchg_destroy(ebic_ctx* ctx);
+/* Device pointers, asynchronous on `stream`: counts of this rank's row shard,
+ * summed over all ranks, land in d_counts on every rank. */
+int ebic_eval_counts_rows_sum(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
+                              uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
+                              void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,12 @@ SIGNATURES = {
     "ebic_ctx_set_pair_layout": (C.c_int, [_vp, C.c_int, C.c_int]),
     "ebic_ctx_set_table_budget": (C.c_int, [_vp, C.c_uint64]),
     "ebic_matrix_index_info": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
+    "ebic_xchg_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_uint64, _vp]),
+    "ebic_xchg_open": (C.c_int, [_vp, _vp]),
+    "ebic_xchg_open_local": (C.c_int, [_vp, _vp]),
+    "ebic_xchg_window": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
+    "ebic_xchg_destroy": (C.c_int, [_vp]),
+    "ebic_eval_counts_rows_sum": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double, C.c_int, _vp, _vp]),
     "ebic_matrix_prepare": (C.c_int, [_vp, C.c_double]),
 }
 
@@ -61,6 +67,7 @@ EBIC_PATH_VALUE = 1
 EBIC_PATH_PLANE = 2
 EBIC_PATH_PLANE_U32 = 3
 EBIC_PATH_TABLE = 4
+EBIC_IPC_HANDLE_BYTES = 64
 
 
 class EbicError(RuntimeError):

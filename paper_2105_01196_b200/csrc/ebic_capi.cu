@@ -22,6 +22,7 @@
 #include "ebic_simd.cuh"
 #include "ebic_pair.cuh"
 #include "ebic_table.cuh"
+#include "ebic_xchg.cuh"
 
 namespace {
 
@@ -151,6 +152,13 @@ struct ebic_ctx {
   // previous piece is evaluated (piece_ev[k]: piece k has landed)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t piece_ev[5] = {};  // [kMaxPieces] arrivals + [kMaxPieces] "previous work done"
+  // row-shard exchange window over peer memory (ebic_xchg.cuh)
+  unsigned char* xchg_win = nullptr;               // this rank's window (device)
+  unsigned char* xchg_peer[ebic::kMaxRanks] = {};  // every rank's window as mapped here
+  bool xchg_ipc_opened[ebic::kMaxRanks] = {};      // peer windows opened through CUDA IPC
+  int xchg_world = 0, xchg_rank = 0;
+  uint64_t xchg_max = 0, xchg_epoch = 0;
+  DevBuf<uint32_t> d_xchg_local;                   // this rank's partial counts
   int pipeline_pieces = 1;       // EBIC_HOST_PIECES (1 = no pipelining; measured faster on B200 at 16K candidates)
   Slot slots[EBIC_MARSHAL_SLOTS];
   uint64_t next_ticket = 1;
@@ -956,6 +964,7 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   ctx->d_tmp_counts.release();
   ctx->d_row_offsets.release();
   ctx->h_tmp_counts.release();
+  ebic_xchg_destroy(ctx);
   ctx->d_acc.release();
   ctx->d_done.release();
   ctx->h_err1.release();
@@ -983,6 +992,7 @@ int ebic_ctx_sync(ebic_ctx* ctx) {
   EBIC_CUDA(cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err) {
     EBIC_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)));
+    if (err == 4) return fail(EBIC_ERR_CUDA, "peer exchange timed out: a rank did not arrive");
     return fail(EBIC_ERR_INVALID_ARGUMENT,
                 "device detected an empty candidate or an out-of-range column index");
   }
@@ -1417,6 +1427,109 @@ int ebic_matrix_prepare(ebic_ctx* ctx, double approx) {
   bool table = false;
   EBIC_TRY(use_table(ctx, approx, ctx->stream, &table));
   EBIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return EBIC_OK;
+}
+
+// ---- row-shard exchange over peer memory ----------------------------------
+
+int ebic_xchg_create(ebic_ctx* ctx, int world, int rank, uint64_t max_cand, void* handle_out) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (world < 1 || world > ebic::kMaxRanks || rank < 0 || rank >= world)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "bad world/rank (%d, %d); at most %d ranks", world, rank, ebic::kMaxRanks);
+  if (max_cand == 0 || max_cand > 0xffffffffull) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad max_cand");
+  EBIC_TRY(set_device(ctx));
+  EBIC_TRY(ebic_xchg_destroy(ctx));
+  const size_t bytes = ebic::kMaxRanks * ebic::kXchgFlagStride * sizeof(uint64_t) +
+                       2ull * ebic::kMaxRanks * max_cand * sizeof(uint32_t);
+  EBIC_CUDA(cudaMalloc(&ctx->xchg_win, bytes));
+  EBIC_CUDA(cudaMemset(ctx->xchg_win, 0, bytes));
+  // the step must not allocate: a device allocation can wait for an idle
+  // device, i.e. for another rank's exchange kernel on a shared GPU
+  EBIC_TRY(ensure(ctx->d_xchg_local, max_cand));
+  ctx->xchg_world = world;
+  ctx->xchg_rank = rank;
+  ctx->xchg_max = max_cand;
+  ctx->xchg_epoch = 0;
+  for (auto& p : ctx->xchg_peer) p = nullptr;
+  ctx->xchg_peer[rank] = ctx->xchg_win;
+  if (handle_out) {
+    cudaIpcMemHandle_t h;
+    EBIC_CUDA(cudaIpcGetMemHandle(&h, ctx->xchg_win));
+    std::memcpy(handle_out, &h, sizeof(h));
+  }
+  return EBIC_OK;
+}
+
+int ebic_xchg_window(ebic_ctx* ctx, void** window_out) {
+  if (!ctx || !window_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
+  *window_out = ctx->xchg_win;
+  return EBIC_OK;
+}
+
+int ebic_xchg_open(ebic_ctx* ctx, const void* handles) {
+  if (!ctx || !handles) return fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
+  EBIC_TRY(set_device(ctx));
+  for (int g = 0; g < ctx->xchg_world; ++g) {
+    if (g == ctx->xchg_rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)g * EBIC_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    EBIC_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->xchg_peer[g] = static_cast<unsigned char*>(p);
+    ctx->xchg_ipc_opened[g] = true;
+  }
+  return EBIC_OK;
+}
+
+int ebic_xchg_open_local(ebic_ctx* ctx, void* const* windows) {
+  if (!ctx || !windows) return fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
+  for (int g = 0; g < ctx->xchg_world; ++g)
+    if (g != ctx->xchg_rank) ctx->xchg_peer[g] = static_cast<unsigned char*>(windows[g]);
+  return EBIC_OK;
+}
+
+int ebic_xchg_destroy(ebic_ctx* ctx) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  cudaSetDevice(ctx->device);
+  for (int g = 0; g < ebic::kMaxRanks; ++g) {
+    if (ctx->xchg_ipc_opened[g] && ctx->xchg_peer[g]) cudaIpcCloseMemHandle(ctx->xchg_peer[g]);
+    ctx->xchg_ipc_opened[g] = false;
+    ctx->xchg_peer[g] = nullptr;
+  }
+  if (ctx->xchg_win) cudaFree(ctx->xchg_win);
+  ctx->xchg_win = nullptr;
+  ctx->xchg_world = 0;
+  ctx->d_xchg_local.release();
+  return EBIC_OK;
+}
+
+int ebic_eval_counts_rows_sum(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets, uint64_t n_cand,
+                              double approx, int negative_trends, uint32_t* d_counts, void* stream) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
+  for (int g = 0; g < ctx->xchg_world; ++g)
+    if (!ctx->xchg_peer[g]) return fail(EBIC_ERR_INVALID_ARGUMENT, "peer window %d not opened", g);
+  if (n_cand > ctx->xchg_max)
+    return fail(EBIC_ERR_CAPACITY, "%llu candidates exceed the exchange window (%llu)",
+                (unsigned long long)n_cand, (unsigned long long)ctx->xchg_max);
+  if (n_cand && (!d_cols || !d_offsets || !d_counts)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null device pointer");
+  EBIC_TRY(set_device(ctx));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  // every rank runs the same sequence of steps, so the epochs agree
+  const uint64_t epoch = ++ctx->xchg_epoch;
+  EBIC_TRY(ensure(ctx->d_xchg_local, std::max<uint64_t>(n_cand, 1)));
+  EBIC_TRY(count_into(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, ctx->d_xchg_local.p, nullptr, s));
+  ebic::XchgPeers peers;
+  for (int g = 0; g < ebic::kMaxRanks; ++g) peers.win[g] = ctx->xchg_peer[g];
+  ebic::xchg_sum_kernel<<<ebic::kXchgCtas, 256, 0, s>>>(ctx->d_xchg_local.p, (uint32_t)n_cand, peers,
+                                                         ctx->xchg_world, ctx->xchg_rank, epoch,
+                                                         (uint32_t)ctx->xchg_max, d_counts, ctx->d_err);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
   return EBIC_OK;
 }
 

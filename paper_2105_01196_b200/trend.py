@@ -169,6 +169,39 @@ class Evaluator:
         check(self._L.ebic_matrix_index_info(self._h, C.byref(nb), C.byref(used)))
         return int(nb.value), bool(used.value)
 
+    # -- row-shard exchange over peer memory (ebic.h, ebic_xchg.cuh) ------------
+    def xchg_create(self, world: int, rank: int, max_cand: int) -> bytes:
+        """Allocate this rank's exchange window; returns its CUDA IPC handle."""
+        h = C.create_string_buffer(64)
+        check(self._L.ebic_xchg_create(self._h, int(world), int(rank), int(max_cand), h))
+        return h.raw
+
+    def xchg_open(self, handles: Sequence[bytes]) -> None:
+        """Map the peers' windows from their IPC handles (rank order)."""
+        buf = C.create_string_buffer(b"".join(bytes(h).ljust(64, b"\0")[:64] for h in handles), 64 * len(handles))
+        check(self._L.ebic_xchg_open(self._h, buf))
+
+    def xchg_open_local(self, windows: Sequence[int]) -> None:
+        """Map windows of contexts in this process (device pointers, rank order)."""
+        arr = (C.c_void_p * len(windows))(*[int(w) for w in windows])
+        check(self._L.ebic_xchg_open_local(self._h, arr))
+
+    def xchg_window(self) -> int:
+        p = C.c_void_p(0)
+        check(self._L.ebic_xchg_window(self._h, C.byref(p)))
+        return int(p.value or 0)
+
+    def xchg_destroy(self) -> None:
+        check(self._L.ebic_xchg_destroy(self._h))
+
+    def evaluate_population_rows_sum_device(self, d_cols: int, d_offsets: int, n_cand: int, d_counts: int,
+                                            params: TrendParams | None = None, stream: int | None = None) -> None:
+        """Row-sharded step: this shard's counts summed over all ranks through peer memory."""
+        p = params or TrendParams()
+        check(self._L.ebic_eval_counts_rows_sum(self._h, C.c_void_p(d_cols), C.c_void_p(d_offsets), int(n_cand),
+                                                float(p.approx), int(bool(p.negative_trends)),
+                                                C.c_void_p(d_counts), C.c_void_p(stream or 0)))
+
     def prepare(self, approx: float) -> None:
         """Build the rank plane for `approx` now (otherwise built on first use)."""
         check(self._L.ebic_matrix_prepare(self._h, float(approx)))

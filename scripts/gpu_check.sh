@@ -16,6 +16,8 @@ for sh in replica rows pop; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 \
       bench.py --gpus 2 --steps 5 --warmup 3 --backend gloo --shard $sh > $OUT/bench_gloo2_${sh}_$TAG.json 2> $OUT/bench_gloo2_${sh}_$TAG.err
 done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 \
+    bench.py --gpus 2 --steps 5 --warmup 3 --backend gloo --shard rows --exchange nccl > $OUT/bench_gloo2_rows_allreduce_$TAG.json 2> $OUT/bench_gloo2_rows_allreduce_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c3_$TAG.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
 for c in c3 c2 c4 c5; do
