@@ -448,7 +448,8 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         out_pinned = pinned(np.zeros(P, dtype=np.uint32))
 
         def call(pop, params):
-            return ev.evaluate_population(pop, params, out=out_pinned).copy()
+            # the counts land in the page-locked out_pinned (the step's D2H); no extra copy
+            return ev.evaluate_population(pop, params, out=out_pinned)
     ev.set_stream(None)
     for i in range(max(args.warmup, 8)):  # >= 2x the marshaller ring: every pinned slot allocated
         call(pops[i % n_pops], tp)
@@ -476,7 +477,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     torch.cuda.synchronize()
     dev_counts = counts_full.cpu().numpy().view(np.uint32)
     ev.set_stream(None)
-    host0 = call(pops[0], tp)
+    host0 = np.array(call(pops[0], tp), copy=True)
     parity_dev_vs_host = (bool(np.array_equal(dev_counts[:len(host0)], host0))
                           if (args.shard == "rows" or replica) else None)
 

@@ -148,6 +148,7 @@ struct ebic_ctx {
   // arrival counters, both zero between launches (the kernel re-zeroes them)
   DevBuf<uint32_t> d_acc, d_done;
   HostBuf<int> h_err1;  // page-locked, device-mapped: error flag of the zero-copy host path
+  int* h_err1_dev = nullptr;  // its device alias
   // zero-copy host path, pipelined: input pieces DMA'd on copy_stream while the
   // previous piece is evaluated (piece_ev[k]: piece k has landed)
   cudaStream_t copy_stream = nullptr;
@@ -1151,18 +1152,21 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
   // them (ONE copy when the offsets are immediately followed by the columns in
   // memory) and the pair kernel writes the counts straight into counts_out
   // over the bus.  Otherwise go through the marshaller's pinned staging slots.
-  uint32_t* out_dev = (n_cand && ctx && ctx->d_mat && cols && offsets && counts_out && dev_alias(cols) &&
-                       dev_alias(offsets))
-                          ? static_cast<uint32_t*>(dev_alias(counts_out))
-                          : nullptr;
+  uint32_t* out_dev = nullptr;
+  if (n_cand && ctx && ctx->d_mat && cols && offsets && counts_out) {
+    if (dev_alias(offsets) && dev_alias(cols)) out_dev = static_cast<uint32_t*>(dev_alias(counts_out));
+  }
   if (out_dev) {
     EBIC_TRY(check_approx(approx));
     if (offsets[0] != 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "offsets[0] must be 0");
     EBIC_TRY(set_device(ctx));
     cudaStream_t s = ctx->stream;
     const uint64_t n_idx = offsets[n_cand];
-    EBIC_TRY(ensure(ctx->h_err1, 1));
-    int* err_dev = static_cast<int*>(dev_alias(ctx->h_err1.p));
+    if (!ctx->h_err1.p) {
+      EBIC_TRY(ensure(ctx->h_err1, 1));
+      ctx->h_err1_dev = static_cast<int*>(dev_alias(ctx->h_err1.p));
+    }
+    int* err_dev = ctx->h_err1_dev;
     if (!err_dev) return fail(EBIC_ERR_CUDA, "page-locked error flag is not device-mapped");
     ctx->h_err1.p[0] = 0;
     const bool one_copy = offsets + (n_cand + 1) == cols;

@@ -44,6 +44,9 @@ class TrendParams:
             raise ValueError("TrendParams: col_cap must be >= 2")
 
 
+_DEFAULT_PARAMS = TrendParams()
+
+
 class Population:
     """A batch of candidate column sequences in CSR form (uint32 cols, uint32 offsets)."""
 
@@ -245,15 +248,17 @@ class Evaluator:
         If the population arrays and `out` are page-locked (e.g. numpy views of
         torch pin_memory tensors), the library DMAs them directly (no staging copy).
         """
-        p = params or TrendParams()
-        pop = _as_population(pop)
+        p = params or _DEFAULT_PARAMS
+        if type(pop) is not Population:
+            pop = _as_population(pop)
+        n = pop.offsets.size - 1
         if out is None:
-            out = np.zeros(len(pop), dtype=np.uint32)
-        elif out.dtype != np.uint32 or not out.flags.c_contiguous or out.size < len(pop):
+            out = np.zeros(n, dtype=np.uint32)
+        elif out.dtype != np.uint32 or not out.flags.c_contiguous or out.size < n:
             raise ValueError("out must be a contiguous uint32 array of at least len(pop) elements")
-        if len(pop) == 0:
+        if n == 0:
             return out
-        check(self._L.ebic_eval_counts(self._h, _ptr(pop.cols), _ptr(pop.offsets), len(pop),
+        check(self._L.ebic_eval_counts(self._h, _ptr(pop.cols), _ptr(pop.offsets), n,
                                        float(p.approx), int(bool(p.negative_trends)), _ptr(out)))
         return out
 
