@@ -184,9 +184,7 @@ struct ebic_ctx {
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
-  int chunk_groups = 1;   // EBIC_CHUNK_GROUPS: slab_pair_kernel CTAs in per-chunk groups (1) or linear units (0)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (warp per candidate up to 256 slices), 2 CTA per candidate (A/B)
-  int pair_kernel = 1;    // EBIC_PAIR_KERNEL: 1 position-indexed counts (slab_pair_kernel), 0 slab_simd_kernel (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
 };
 
@@ -427,8 +425,8 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
 }
 
 struct SlabCfg {
-  bool simd = false;  // packed 16-bit rank pairs (slab_simd_kernel); p = pair-words per lane
-  bool v2 = false;    // ... with position-indexed counts (slab_pair_kernel)
+  bool simd = false;  // packed 16-bit rank pairs (slab_pair_kernel); p = pair-words per lane
+  bool v2 = false;    // (always with simd: the pair kernel publishes final counts itself)
   int p = 1;
   int rpl = 1, sub = 1;
   uint32_t rt = 32;
@@ -466,7 +464,7 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
       }
     }
   }
-  if (found && ctx->pair_kernel) {
+  if (found) {
     // slab_pair_kernel: per position a record (<= 16 B), a count and a slot; the
     // (kClasses - 1) swept classes are each padded to the sweep stride
     const size_t slab = C * c.rt * 4;
@@ -477,16 +475,6 @@ SlabCfg choose_slab(const ebic_ctx* ctx, uint64_t n_cand, bool mask) {
     c.chunk = (uint32_t)((n_cand + n_chunks - 1) / n_chunks);
     c.smem = fixed + (size_t)c.chunk * ebic::kPairPosBytes;
     c.v2 = true;
-    c.ok = true;
-    return c;
-  }
-  if (found) {
-    const size_t slab = C * c.rt * 4;
-    const size_t fixed = slab + (size_t)ebic::kClasses * ebic::kSlabWarps * c.sub * 16 + 16;
-    const uint64_t cmax = std::min<uint64_t>((budget - fixed) / 20, 16384);
-    const uint64_t n_chunks = (n_cand + cmax - 1) / cmax;
-    c.chunk = (uint32_t)((n_cand + n_chunks - 1) / n_chunks);
-    c.smem = fixed + (size_t)c.chunk * 20;
     c.ok = true;
     return c;
   }
@@ -575,17 +563,16 @@ struct PairOut {       // where slab_pair_kernel publishes its results
 template <int P, int SUB, bool NEG>
 int launch_simd_t(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const uint32_t* d_offs,
                   uint64_t n_cand, uint32_t* d_counts, const PairOut* po, cudaStream_t s) {
-  auto kern = cfg.v2 ? ebic::slab_pair_kernel<P, SUB, NEG> : ebic::slab_simd_kernel<P, SUB, NEG>;
-  static std::atomic<uint64_t> attr_done[2] = {{0}, {0}};
+  auto kern = ebic::slab_pair_kernel<P, SUB, NEG>;
+  static std::atomic<uint64_t> attr_done{0};
   const uint64_t bit = 1ull << (ctx->device & 63);
-  if (!(attr_done[cfg.v2].load(std::memory_order_relaxed) & bit)) {
+  if (!(attr_done.load(std::memory_order_relaxed) & bit)) {
     EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ctx->smem_optin - 1024)));
-    attr_done[cfg.v2].fetch_or(bit);
+    attr_done.fetch_or(bit);
   }
   ebic::SlabArgs a = make_slab_args(ctx, cfg, d_cols, d_offs, n_cand, d_counts, nullptr);
-  const uint64_t units = (uint64_t)a.n_chunks * a.n_slabs;
-  unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)ctx->n_sms);
-  if (cfg.v2) {
+  unsigned grid = 0;
+  {
     if (!po || !po->out) return fail(EBIC_ERR_INVALID_ARGUMENT, "internal: pair kernel without an output");
     // chunk groups of `group` CTAs (a CTA per SM; up to n_sms % n_chunks SMs idle):
     // the groups walk the plane in step, and every CTA packs its chunk once
@@ -925,16 +912,12 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (pb) ctx->plane_builder = std::atoi(pb);
     const char* pf = std::getenv("EBIC_PREFETCH");
     if (pf) ctx->prefetch = std::atoi(pf) ? 1 : 0;
-    const char* cg = std::getenv("EBIC_CHUNK_GROUPS");
-    if (cg) ctx->chunk_groups = std::atoi(cg) ? 1 : 0;
     const char* tb = std::getenv("EBIC_TABLE_BUDGET_MB");
     if (tb) ctx->table_budget_user = (uint64_t)std::strtoull(tb, nullptr, 10) << 20;
     const char* hp = std::getenv("EBIC_HOST_PIECES");
     if (hp) ctx->pipeline_pieces = std::max(1, std::min(4, std::atoi(hp)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");
     if (tk) ctx->table_kernel = std::atoi(tk);
-    const char* pk = std::getenv("EBIC_PAIR_KERNEL");
-    if (pk) ctx->pair_kernel = std::atoi(pk) ? 1 : 0;
     const char* sc = std::getenv("EBIC_PAIR_LAYOUT");
     int fp = 0, fs = 0;
     if (sc && std::sscanf(sc, "%d,%d", &fp, &fs) == 2) ctx->simd_force = fp * 16 + fs;

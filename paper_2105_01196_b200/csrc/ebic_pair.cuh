@@ -1,7 +1,7 @@
 // ebic_pair.cuh -- the hot kernel: packed rank pairs over a shared-memory row
 // slab, with position-indexed counts.
 //
-// Same exact pair test as slab_simd_kernel (ebic_simd.cuh): a slab column line
+// The packed-pair test of ebic_simd.cuh: a slab column line
 // holds interleaved 16-bit row pairs (stage_pairs) and one IADD
 // tests two rows.  What changes is the per-candidate bookkeeping, which on
 // B200 is what competes with the column loads for the shared-memory pipe:

@@ -1,4 +1,5 @@
-// ebic_simd.cuh -- two rows per 32-bit word: the packed-rank slab kernel.
+// ebic_simd.cuh -- two rows per 32-bit word: the packed-rank-pair helpers of
+// the slab kernel (slab_pair_kernel, ebic_pair.cuh).
 //
 // Same rank-plane test as slab_count_kernel (R(y) > T(x) <=> v_y > thr(v_x),
 // see ebic_plane.cuh), but each slab column is restaged as 16-bit row PAIRS:
@@ -79,199 +80,6 @@ __device__ __forceinline__ uint32_t popc_words(const M& v) {
 #pragma unroll
   for (int q = 0; q < P; ++q) n += __popc(wget(v, q));
   return n;
-}
-
-// Fixed-length body: L vector loads (both words of every column), then the
-// L-1 forward tests Rg(c_k) + NT(c_{k-1}) (and reversed Rg(c_{k-1}) + NT(c_k)).
-// Returns the guard bits of the lane's row pairs that support the candidate.
-template <int L, int P, bool NEG, uint32_t COLSHIFT>
-__device__ __forceinline__ typename PairVec<P>::M simd_eval(uint32_t lane_base, const uint4& rec,
-                                                          typename PairVec<P>::M vmask) {
-  using V = typename PairVec<P>::V;
-  using M = typename PairVec<P>::M;
-  const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
-                                 hi16(rec.z), lo16(rec.w), hi16(rec.w)};
-  V w[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) w[k] = lds<V>(lane_base + (cc[k] << COLSHIFT));
-  M f = vmask;
-#pragma unroll
-  for (int k = 1; k < L; ++k) and_pair<P>(f, w[k], w[k - 1]);
-  if constexpr (NEG) {
-    M r = vmask;
-#pragma unroll
-    for (int k = 1; k < L; ++k) and_pair<P>(r, w[k - 1], w[k]);
-    or_into<P>(f, r);
-  }
-  return f;
-}
-
-template <int P, int SUB, bool NEG, int L, uint32_t COLSHIFT>
-__device__ __forceinline__ void simd_sweep_class(const SlabArgs& a, uint32_t sa_rec, uint32_t lane_base,
-                                                 uint32_t* s_cnt, uint32_t n_padded, uint32_t class_base,
-                                                 uint32_t c_begin, typename PairVec<P>::M vmask, int warp,
-                                                 int lane, int sub) {
-  using V = typename PairVec<P>::V;
-  using M = typename PairVec<P>::M;
-  constexpr int LPC = 32 / SUB;
-  constexpr uint32_t stride = kSlabWarps * SUB;
-  for (uint32_t t = warp * SUB + sub; t < n_padded; t += stride) {
-    const uint4 rec = lds<uint4>(sa_rec + (class_base + t) * 16);
-    const uint32_t j = lo16(rec.x);
-    M ok;
-    if constexpr (L == 1) {
-      ok = vmask;  // no pair: every row supports (the trend.cpp:19 loop never runs)
-    } else if constexpr (L < 8) {
-      ok = simd_eval<L, P, NEG, COLSHIFT>(lane_base, rec, vmask);
-    } else {
-      // >= 8 columns: first 7 from the record, the tail from the CSR
-      const uint32_t cc[kRecCols] = {hi16(rec.x), lo16(rec.y), hi16(rec.y), lo16(rec.z),
-                                     hi16(rec.z), lo16(rec.w), hi16(rec.w)};
-      M f = vmask, r = NEG ? vmask : M{};
-      V wp = lds<V>(lane_base + (cc[0] << COLSHIFT));
-      auto step = [&](uint32_t col) {
-        const V wc = lds<V>(lane_base + (col << COLSHIFT));
-        and_pair<P>(f, wc, wp);
-        if (NEG) and_pair<P>(r, wp, wc);
-        wp = wc;
-      };
-#pragma unroll
-      for (int k = 1; k < kRecCols; ++k) step(cc[k]);
-      if (j < a.chunk) {
-        // the tail in blocks of TB columns: TB independent index loads, then TB
-        // shared loads, then the pair tests (no load-to-load dependency chain)
-        constexpr int TB = P == 1 ? 8 : (NEG ? 2 : 4);  // register budget: 64 per thread
-        const uint32_t b = a.offs[c_begin + j], e = a.offs[c_begin + j + 1];
-        for (uint32_t k0 = b + kRecCols; k0 < e; k0 += TB) {
-          uint32_t any = 0;
-#pragma unroll
-          for (int q = 0; q < P; ++q) any |= wget(f, q) | wget(r, q);
-          if (!any) break;  // this lane's rows are all decided
-          uint32_t idx[TB];
-#pragma unroll
-          for (int i = 0; i < TB; ++i) idx[i] = k0 + i < e ? __ldg(a.cols + k0 + i) : 0u;
-          V wv[TB];
-#pragma unroll
-          for (int i = 0; i < TB; ++i) wv[i] = lds<V>(lane_base + (idx[i] << COLSHIFT));
-#pragma unroll
-          for (int i = 0; i < TB; ++i) {
-            if (k0 + i < e) {
-              and_pair<P>(f, wv[i], wp);
-              if (NEG) and_pair<P>(r, wp, wv[i]);
-              wp = wv[i];
-            }
-          }
-        }
-      }
-      if (NEG) or_into<P>(f, r);
-      ok = f;
-    }
-    // count: per-lane popcount, summed per candidate with ONE REDUX for all SUB
-    // candidates of the warp: candidate `sub` owns bit field [sub*FW, (sub+1)*FW)
-    // (a slab count is <= RT = 2*P*LPC rows, which fits its field)
-    constexpr uint32_t FW = 32 / SUB;
-    static_assert(SUB == 1 || (2u * P * LPC) < (1u << FW), "count field too narrow");
-    const uint32_t n = popc_words<P>(ok) << (FW * sub);
-    const uint32_t tot = __reduce_add_sync(kFull, n);
-    if (lane % LPC == 0)
-      atomicAdd(&s_cnt[j], SUB == 1 ? tot : (tot >> (FW * sub)) & ((1u << (FW % 32)) - 1u));
-  }
-}
-
-template <int P, int SUB, bool NEG>
-__global__ void __launch_bounds__(kSlabThreads, 1)
-slab_simd_kernel(const SlabArgs a) {
-  using M = typename PairVec<P>::M;
-  constexpr int LPC = 32 / SUB;
-  constexpr uint32_t RT = LPC * 2 * P;             // rows per slab
-  constexpr uint32_t CW = RT;                      // words per column line: RT/2 x (Rg, NT)
-  constexpr uint32_t COLSHIFT = CW == 16 ? 6 : CW == 32 ? 7 : CW == 64 ? 8 : CW == 128 ? 9 : 10;  // log2(CW*4)
-  static_assert((1u << COLSHIFT) == CW * 4, "column stride must be a power of two");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* s_slab = reinterpret_cast<uint32_t*>(smem_raw);               // [C][RT/2 x (Rg, NT)]
-  uint4* s_rec = reinterpret_cast<uint4*>(s_slab + (size_t)a.n_cols * CW);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_rec + a.chunk + kClasses * kSlabWarps * SUB);
-  __shared__ uint32_t s_hist[kClasses], s_base[kClasses], s_fill[kClasses];
-  const uint32_t sa_slab = (uint32_t)__cvta_generic_to_shared(s_slab);
-  const uint32_t sa_rec = (uint32_t)__cvta_generic_to_shared(s_rec);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane / LPC, rl = lane % LPC;
-  const uint32_t lane_base = sa_slab + rl * P * 8;  // this lane's (Rg, NT) pair(s) in column 0
-  const uint64_t U = (uint64_t)a.n_chunks * a.n_slabs;
-  const uint64_t u_begin = blockIdx.x * U / gridDim.x, u_end = (blockIdx.x + 1) * U / gridDim.x;
-  uint32_t cur_chunk = 0xffffffffu, c_begin = 0, c_n = 0;
-
-  auto flush = [&]() {
-    if (cur_chunk == 0xffffffffu) return;
-    for (uint32_t j = threadIdx.x; j < c_n; j += blockDim.x)
-      if (s_cnt[j]) atomicAdd(&a.counts[c_begin + j], s_cnt[j]);
-  };
-
-  for (uint64_t u = u_begin; u < u_end; ++u) {
-    const uint32_t chunk = (uint32_t)(u / a.n_slabs), slab = (uint32_t)(u % a.n_slabs);
-    const uint32_t row0 = slab * RT;
-    __syncthreads();
-    if (chunk != cur_chunk) {
-      flush();
-      cur_chunk = chunk;
-      c_begin = chunk * a.chunk;
-      c_n = min(a.chunk, a.n_cand - c_begin);
-      pack_chunk<kSlabWarps * SUB>(a, c_begin, c_n, s_rec, s_cnt, s_hist, s_base, s_fill);
-    }
-    // stage + repack: each thread takes 4 consecutive rows (one uint4 of plane
-    // words) of one column -> 2 row pairs -> 4 words (Rg, NT, Rg, NT) of the line;
-    // a round of UNR loads is in flight before any store
-    {
-      constexpr uint32_t Q = RT / 4;  // uint4 per column
-      constexpr int UNR = 4;
-      const uint32_t total = a.n_cols * Q;
-      const uint4* src = reinterpret_cast<const uint4*>(a.plane);
-      const uint64_t ld4 = a.ld / 4, r4 = row0 / 4;
-      for (uint32_t t0 = threadIdx.x; t0 < total; t0 += UNR * blockDim.x) {
-        uint4 w[UNR];
-#pragma unroll
-        for (int k = 0; k < UNR; ++k) {
-          const uint32_t t = t0 + k * blockDim.x;
-          if (t < total) w[k] = __ldg(src + (uint64_t)(t / Q) * ld4 + r4 + t % Q);
-        }
-#pragma unroll
-        for (int k = 0; k < UNR; ++k) {
-          const uint32_t t = t0 + k * blockDim.x;
-          if (t < total) {
-            const uint32_t c = t / Q, q = t % Q;
-            *reinterpret_cast<uint4*>(s_slab + (size_t)c * CW + 4 * q) = stage_pairs<P>(w[k]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    prefetch_next_slab<RT>(a, u + 1, u_end);
-
-    // validity guard bits of this lane's row pairs (rows beyond n_rows never count)
-    const uint32_t valid_rows = min(RT, a.n_rows - row0);
-    M vmask;
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const uint32_t r = (rl * P + q) * 2;
-      wref(vmask, q) = (r < valid_rows ? 0x8000u : 0u) | (r + 1 < valid_rows ? 0x80000000u : 0u);
-    }
-
-#define EBIC_SIMD_SWEEP(L)                                                                                      \
-  simd_sweep_class<P, SUB, NEG, L, COLSHIFT>(a, sa_rec, lane_base, s_cnt, s_hist[L], s_base[L], c_begin, vmask, \
-                                             warp, lane, sub)
-    EBIC_SIMD_SWEEP(4);
-    EBIC_SIMD_SWEEP(3);
-    EBIC_SIMD_SWEEP(5);
-    EBIC_SIMD_SWEEP(2);
-    EBIC_SIMD_SWEEP(6);
-    EBIC_SIMD_SWEEP(7);
-    EBIC_SIMD_SWEEP(8);
-    EBIC_SIMD_SWEEP(1);
-#undef EBIC_SIMD_SWEEP
-  }
-  __syncthreads();
-  flush();
 }
 
 }  // namespace ebic
