@@ -51,6 +51,7 @@ extern "C" {
 #define EBIC_ERR_CAPACITY 4         /* output buffer too small; required size returned */
 #define EBIC_ERR_NOT_EXACT 5        /* EBIC_STORE_F32 requested for a matrix that is not f32-representable */
 #define EBIC_ERR_NO_DEVICE 6        /* no CUDA device / bad device ordinal */
+#define EBIC_ERR_IO 7               /* file cannot be opened / read */
 
 /* matrix store precision */
 #define EBIC_STORE_AUTO 0 /* float32 if every value is exactly representable, else float64 */
@@ -94,6 +95,22 @@ int ebic_matrix_upload_f32(ebic_ctx* ctx, const float* row_major, uint64_t n_row
 int ebic_matrix_info(ebic_ctx* ctx, uint64_t* n_rows, uint64_t* n_cols, uint64_t* ld,
                      int* store, uint64_t* row_base);
 int ebic_matrix_free(ebic_ctx* ctx);
+
+/* ---- matrix ingest (reference: parse_matrix_tsv, io.cpp:78-111) ---------
+ * The reference's TSV format and rules (header of column labels with an
+ * optional corner cell, one line per row of label + values, '\r' stripped,
+ * trailing empty lines ignored, every value parsed with std::from_chars and
+ * required finite) with its error messages, parsed on n_threads host threads
+ * (<= 0: all).  Values are bit-identical to the reference parser's. */
+/* Row-major doubles into values_out (cap elements).  *rows_out / *cols_out
+ * receive the shape; EBIC_ERR_CAPACITY (shape filled) if cap is too small, so
+ * a call with cap = 0 queries the shape. */
+int ebic_tsv_read(const char* path, int n_threads, double* values_out, uint64_t cap, uint64_t* rows_out,
+                  uint64_t* cols_out);
+/* Parse into page-locked memory and upload as the context's matrix (as
+ * ebic_matrix_upload_f64 with row_base 0). */
+int ebic_matrix_load_tsv(ebic_ctx* ctx, const char* path, int n_threads, int store, int* store_out,
+                         uint64_t* rows_out, uint64_t* cols_out);
 
 /* ---- fitness counts (reference: evaluate_population, trend.cpp:56-72) ---- */
 

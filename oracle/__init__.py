@@ -94,6 +94,10 @@ def reference():
             L.ref_fitness.restype = C.c_double
             L.ref_fitness.argtypes = [C.c_uint64] * 4
             L.ref_test_chromosomes.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp]
+            if hasattr(L, "ref_parse_matrix_tsv"):  # io.cpp compiled in (needs nlohmann json.hpp at build)
+                L.ref_parse_matrix_tsv.argtypes = [C.c_char_p, _vp, C.c_uint64, C.POINTER(C.c_uint64),
+                                                   C.POINTER(C.c_uint64)]
+                L.ref_write_matrix_tsv.argtypes = [C.c_char_p, _vp, C.c_uint64, C.c_uint64]
             _ref = L
     return _ref
 
@@ -244,3 +248,33 @@ def ref_test_chromosomes(seed: int, n: int, num_cols: int):
     offs = np.empty(n + 1, dtype=np.uint32)
     L.ref_test_chromosomes(seed, n, num_cols, _p(cols), _p(offs))
     return cols[:offs[-1]].copy(), offs
+
+
+class RefParseError(Exception):
+    """The reference parser's ParseError (message verbatim)."""
+
+
+def ref_io_available() -> bool:
+    return reference_available() and hasattr(reference(), "ref_parse_matrix_tsv")
+
+
+def ref_parse_matrix_tsv(path) -> np.ndarray:
+    """The reference TSV reader (io.cpp:78-111): row-major float64 values."""
+    L = reference()
+    r, c = C.c_uint64(0), C.c_uint64(0)
+    st = L.ref_parse_matrix_tsv(str(path).encode(), None, 0, C.byref(r), C.byref(c))
+    if st == 1:
+        raise RefParseError(L.ref_last_error().decode())
+    out = np.empty((r.value, c.value), dtype=np.float64)
+    if L.ref_parse_matrix_tsv(str(path).encode(), _p(out), out.size, C.byref(r), C.byref(c)):
+        raise RefParseError(L.ref_last_error().decode())
+    return out
+
+
+def ref_write_matrix_tsv(path, m: np.ndarray) -> None:
+    """The reference TSV writer (io.cpp:113-130, %.17g, labels r0../c0..)."""
+    L = reference()
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    if L.ref_write_matrix_tsv(str(path).encode(), _p(m), m.shape[0], m.shape[1]):
+        raise RuntimeError(L.ref_last_error().decode())
+

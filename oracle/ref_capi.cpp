@@ -16,6 +16,9 @@
 #include <vector>
 
 #include "bicseek/datagen.hpp"
+#ifdef REF_HAVE_IO
+#include "bicseek/io.hpp"
+#endif
 #include "bicseek/evolution.hpp"
 #include "bicseek/rng.hpp"
 #include "bicseek/trend.hpp"
@@ -203,4 +206,34 @@ int ref_test_chromosomes(uint64_t seed, uint64_t n, uint64_t num_cols, uint32_t*
   return 0;
 }
 
+
+#ifdef REF_HAVE_IO
+// The reference TSV reader (io.cpp:78-111): row-major values into out (cap
+// elements), shape into rows/cols.  1 on error (ref_last_error: the reference's
+// own ParseError message), 2 if cap is too small (shape filled).
+int ref_parse_matrix_tsv(const char* path, double* out, uint64_t cap, uint64_t* rows, uint64_t* cols) {
+  try {
+    const ExpressionMatrix m = parse_matrix_tsv(path);
+    *rows = m.rows();
+    *cols = m.cols();
+    if (cap < m.rows() * m.cols()) return 2;
+    std::memcpy(out, m.values().data(), m.values().size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+
+// The reference TSV writer (io.cpp:113-130, %.17g) with generated labels.
+int ref_write_matrix_tsv(const char* path, const double* v, uint64_t rows, uint64_t cols) {
+  try {
+    ExpressionMatrix m(std::vector<double>(v, v + rows * cols), rows, cols, default_labels('r', rows),
+                       default_labels('c', cols));
+    write_matrix_tsv(path, m);
+    return 0;
+  } catch (const std::exception& e) {
+    return guard(e);
+  }
+}
+#endif
 }  // extern "C"

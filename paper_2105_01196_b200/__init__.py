@@ -18,6 +18,7 @@ from .trend import (  # noqa: F401
     device_count,
     evaluate_population,
     fitness,
+    read_matrix_tsv,
     row_supports,
     supporting_rows,
 )

@@ -18,6 +18,7 @@ EBIC_ERR_NO_MATRIX = 3
 EBIC_ERR_CAPACITY = 4
 EBIC_ERR_NOT_EXACT = 5
 EBIC_ERR_NO_DEVICE = 6
+EBIC_ERR_IO = 7
 
 EBIC_STORE_AUTO = 0
 EBIC_STORE_F32 = 1
@@ -53,6 +54,9 @@ SIGNATURES = {
     "ebic_ctx_set_pair_layout": (C.c_int, [_vp, C.c_int, C.c_int]),
     "ebic_ctx_set_table_budget": (C.c_int, [_vp, C.c_uint64]),
     "ebic_matrix_index_info": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
+    "ebic_tsv_read": (C.c_int, [C.c_char_p, C.c_int, _vp, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "ebic_matrix_load_tsv": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "ebic_xchg_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_uint64, _vp]),
     "ebic_xchg_open": (C.c_int, [_vp, _vp]),
     "ebic_xchg_open_local": (C.c_int, [_vp, _vp]),

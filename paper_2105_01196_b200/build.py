@@ -40,7 +40,7 @@ def _nvcc() -> str:
 
 
 def _sources():
-    return [CSRC / "ebic_capi.cu", *sorted(CSRC.glob("*.cuh")), REPO / "include" / "ebic.h"]
+    return [CSRC / "ebic_capi.cu", CSRC / "ebic_tsv.cpp", *sorted(CSRC.glob("*.cuh")), REPO / "include" / "ebic.h"]
 
 
 def needs_rebuild() -> bool:
@@ -54,7 +54,8 @@ def build_ext(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_rebuild():
         return LIB_PATH
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{REPO / 'include'}", "-o", str(tmp), str(CSRC / "ebic_capi.cu")]
+    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{REPO / 'include'}", "-o", str(tmp), str(CSRC / "ebic_capi.cu"),
+           str(CSRC / "ebic_tsv.cpp"), "-Xcompiler", "-pthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
     (PKG_DIR / "build_ptxas.log").write_text(log)

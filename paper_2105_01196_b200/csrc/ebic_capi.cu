@@ -1417,6 +1417,36 @@ int ebic_matrix_prepare(ebic_ctx* ctx, double approx) {
   return EBIC_OK;
 }
 
+// ---- matrix ingest (ebic_tsv.cpp) -------------------------------------------
+
+__attribute__((visibility("hidden"))) int ebic_internal_fail(int code, const char* msg) {
+  return fail(code, "%s", msg);
+}
+
+int ebic_matrix_load_tsv(ebic_ctx* ctx, const char* path, int n_threads, int store, int* store_out,
+                         uint64_t* rows_out, uint64_t* cols_out) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  uint64_t rows = 0, cols = 0;
+  const int st = ebic_tsv_read(path, n_threads, nullptr, 0, &rows, &cols);
+  if (st != EBIC_ERR_CAPACITY) return st;  // the shape query reports CAPACITY on success
+  EBIC_TRY(set_device(ctx));
+  // parse straight into page-locked memory: the upload DMAs it from there
+  HostBuf<double> staging;
+  EBIC_TRY(ensure(staging, rows * cols));
+  const int st2 = ebic_tsv_read(path, n_threads, staging.p, rows * cols, &rows, &cols);
+  if (st2 != EBIC_OK) {
+    staging.release();
+    return st2;
+  }
+  const int st3 = upload_impl<double>(ctx, staging.p, rows, cols, 0, store, store_out);
+  staging.release();
+  if (st3 == EBIC_OK) {
+    if (rows_out) *rows_out = rows;
+    if (cols_out) *cols_out = cols;
+  }
+  return st3;
+}
+
 // ---- row-shard exchange over peer memory ----------------------------------
 
 int ebic_xchg_create(ebic_ctx* ctx, int world, int rank, uint64_t max_cand, void* handle_out) {

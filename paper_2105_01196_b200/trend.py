@@ -205,6 +205,15 @@ class Evaluator:
                                                 float(p.approx), int(bool(p.negative_trends)),
                                                 C.c_void_p(d_counts), C.c_void_p(stream or 0)))
 
+    def load_tsv(self, path, threads: int = 0, store: int = EBIC_STORE_AUTO) -> tuple[int, int, int]:
+        """Parse a reference-format TSV matrix (io.cpp:78-111) on all host threads
+        straight into page-locked memory and upload it; returns (rows, cols, store)."""
+        st, r, c = C.c_int(0), C.c_uint64(0), C.c_uint64(0)
+        check(self._L.ebic_matrix_load_tsv(self._h, str(path).encode(), int(threads), int(store), C.byref(st),
+                                           C.byref(r), C.byref(c)))
+        self.n_rows, self.n_cols = int(r.value), int(c.value)
+        return int(r.value), int(c.value), int(st.value)
+
     def prepare(self, approx: float) -> None:
         """Build the rank plane for `approx` now (otherwise built on first use)."""
         check(self._L.ebic_matrix_prepare(self._h, float(approx)))
@@ -364,3 +373,18 @@ __all__ = [
     "row_supports", "supporting_rows", "evaluate_population", "fitness",
     "EBIC_STORE_AUTO", "EBIC_STORE_F32", "EBIC_STORE_F64",
 ]
+
+
+def read_matrix_tsv(path, threads: int = 0) -> np.ndarray:
+    """The reference's TSV matrix format (io.cpp:78-111) parsed on all host
+    threads (no device needed); same values and error messages."""
+    L = _lib.lib()
+    r, c = C.c_uint64(0), C.c_uint64(0)
+    st = L.ebic_tsv_read(str(path).encode(), int(threads), None, 0, C.byref(r), C.byref(c))
+    if st != _lib.EBIC_ERR_CAPACITY:
+        check(st)
+    out = np.empty((r.value, c.value), dtype=np.float64)
+    check(L.ebic_tsv_read(str(path).encode(), int(threads), _ptr(out) if out.size else None, out.size,
+                          C.byref(r), C.byref(c)))
+    return out
+

@@ -607,3 +607,22 @@ def test_zero_copy_pipelined_pieces(evaluator, layout):
         evaluator.evaluate_population(Population(ppop.cols, bo), TrendParams(), out=out)
     want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
     np.testing.assert_array_equal(evaluator.evaluate_population(ppop, TrendParams(), out=out), want)
+
+
+def test_load_tsv_into_device_store(evaluator, tmp_path):
+    """ebic_matrix_load_tsv: the reference TSV format parsed on all host threads
+    into page-locked memory and uploaded; counts identical to the reference
+    evaluator on the reference parser's matrix."""
+    if not oracle.ref_io_available():
+        pytest.skip("reference io.cpp not built")
+    m = synth.planted_trend_matrix(3000, 150, 2, 300, 10, seed=4)[0].astype(np.float64)
+    m[5, 7] = 0.1  # not float32-exact: the store stays f64
+    f = tmp_path / "m.tsv"
+    oracle.ref_write_matrix_tsv(f, m)
+    rows, cols, store = evaluator.load_tsv(f)
+    assert (rows, cols, store) == (3000, 150, EBIC_STORE_F64)
+    ref_m = oracle.ref_parse_matrix_tsv(f)
+    pop = synth.random_population(2000, 150, seed=5)
+    for approx, neg in ((0.03, False), (0.0, True)):
+        want = oracle.evaluate_population(ref_m, pop.cols, pop.offsets, approx, neg)
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
