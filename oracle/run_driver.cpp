@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "bicseek/datagen.hpp"
 #include "bicseek/evolution.hpp"
@@ -58,6 +60,7 @@ int main(int argc, char** argv) {
   p.max_iterations = 200;
   bool quantize = true;
   bool warm = false;
+  int jobs = 1;
   std::string engine = "reference";
   for (int i = 1; i + 1 < argc; i += 2) {
     const std::string k = argv[i];
@@ -79,10 +82,38 @@ int main(int argc, char** argv) {
     else if (k == "--quantize") quantize = std::atoi(v) != 0;
     else if (k == "--warm") warm = std::atoi(v) != 0;
     else if (k == "--engine") engine = v;
+    else if (k == "--jobs") jobs = std::atoi(v);
     else {
       std::fprintf(stderr, "unknown option %s\n", k.c_str());
       return 2;
     }
+  }
+  if (jobs > 1) {
+    // independent datasets, one run() per thread (bench.cpp:103-121's --jobs):
+    // job j uses data seed + j and GA seed + j; one JSON line per job, in order
+    std::vector<std::string> lines(jobs);
+    std::vector<std::thread> pool;
+    for (int j = 0; j < jobs; ++j)
+      pool.emplace_back([&, j] {
+        ScenarioSpec sj = s;
+        sj.seed = s.seed + j;
+        EvolutionParams pj = p;
+        pj.seed = p.seed + j;
+        GeneratedDataset dj = gen_scenario(sj);
+        std::vector<double> vj = dj.matrix.values();
+        if (quantize)
+          for (double& x : vj) x = static_cast<double>(static_cast<float>(x));
+        const ExpressionMatrix mj(std::move(vj), dj.matrix.rows(), dj.matrix.cols(), dj.matrix.row_labels(),
+                                  dj.matrix.col_labels());
+        const RunResult rj = run(mj, pj);
+        char buf[160];
+        std::snprintf(buf, sizeof buf, ",\"generations\":%zu,\"termination\":\"%s\"}", rj.report.generations,
+                      rj.report.termination.c_str());
+        lines[j] = "{\"job\":" + std::to_string(j) + ",\"result\":" + bics_json(rj.biclusters) + buf;
+      });
+    for (auto& t : pool) t.join();
+    for (const auto& l : lines) std::printf("%s\n", l.c_str());
+    return 0;
   }
   GeneratedDataset d = gen_scenario(s);
   std::vector<double> v = d.matrix.values();

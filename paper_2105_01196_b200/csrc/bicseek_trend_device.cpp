@@ -22,9 +22,11 @@
 // that happens to reuse a freed buffer is never mistaken for the cached one).
 // EBIC_SHIM_TRUST_POINTER=1 skips the content comparison for very large
 // matrices whose identity the caller guarantees (e.g. one run()).
-// EBIC_DEVICE selects the CUDA device (default 0).  State is thread_local, so
+// EBIC_DEVICE=<n> pins the CUDA device; by default each thread's context goes
+// to the next visible device round-robin.  State is thread_local, so
 // concurrent run()s on different threads (bench.cpp:103-121) get independent
-// contexts and streams.
+// contexts and streams -- on different GPUs when there are several.
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -70,12 +72,22 @@ bool trust_pointer() {
   return e && e[0] == '1';
 }
 
+// Device of a new (per-thread) context.  EBIC_DEVICE=<n> pins every thread to
+// GPU n; otherwise threads are spread round-robin over the visible GPUs, so
+// independent datasets run concurrently (bench --jobs, bench.cpp:103-121)
+// land on different GPUs -- dataset-level multi-GPU.
+int pick_device() {
+  const char* e = std::getenv("EBIC_DEVICE");
+  if (e && *e && std::strcmp(e, "all") != 0) return std::atoi(e);
+  int n = 0;
+  if (ebic_device_count(&n) != EBIC_OK || n <= 1) return 0;
+  static std::atomic<unsigned> next{0};
+  return static_cast<int>(next.fetch_add(1) % static_cast<unsigned>(n));
+}
+
 ebic_ctx* bind(const ExpressionMatrix& m) {
   DeviceState& s = g_dev;
-  if (!s.ctx) {
-    const char* e = std::getenv("EBIC_DEVICE");
-    check(ebic_ctx_create(e ? std::atoi(e) : 0, &s.ctx), "context");
-  }
+  if (!s.ctx) check(ebic_ctx_create(pick_device(), &s.ctx), "context");
   const std::vector<double>& v = m.values();
   const bool same = s.key == v.data() && s.rows == m.rows() && s.cols == m.cols() &&
                     (trust_pointer() ||

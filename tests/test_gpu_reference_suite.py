@@ -72,3 +72,19 @@ def test_device_aware_driver_matches_reference_at_scale():
     b = json.loads(subprocess.run([str(exe_b), "--engine", "device", *args], check=True, capture_output=True,
                                   text=True, timeout=600).stdout)
     assert a["result"] == b["result"] and a["generations"] == b["generations"]
+
+
+def test_concurrent_runs_one_context_per_thread():
+    """bench --jobs style: four independent datasets, one unchanged run() per
+    thread; every thread's drop-in TU gets its own device context (spread
+    round-robin over the visible GPUs -- dataset-level multi-GPU).  Each job's
+    result equals the reference CPU build's."""
+    exe_ref, exe_dev = _need("run_ref"), _need("run_device")
+    args = ["--jobs", "4", "--rows", "2000", "--cols", "200", "--bic-rows", "200", "--bic-cols", "10",
+            "--pop", "512", "--iters", "30", "--tabu", "1000000000000"]
+    want = subprocess.run([str(exe_ref), *args], check=True, capture_output=True, text=True, timeout=600).stdout
+    got = subprocess.run([str(exe_dev), *args], check=True, capture_output=True, text=True, timeout=600).stdout
+    want_l, got_l = want.strip().splitlines(), got.strip().splitlines()
+    assert len(got_l) == len(want_l) == 4
+    for a, b in zip(want_l, got_l):
+        assert json.loads(a) == json.loads(b)
