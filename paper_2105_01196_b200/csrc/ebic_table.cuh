@@ -215,7 +215,7 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
 // the next candidate cost more in registers / occupancy than they gain; the
 // kernel runs at 70-90% of the random-2.5-KB-chunk read ceiling measured by
 // scripts/microbench/random_chunks.cu.)
-template <int J, bool NEG, bool MASK>
+template <int J, bool NEG, bool MASK, bool MULTI = false>
 __global__ void __launch_bounds__(256)
 table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
                         const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
@@ -223,7 +223,7 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
                         uint64_t mask_wpc) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-  const uint32_t nv = wp / 4;  // uint4 per pair vector (<= 32 J)
+  const uint32_t nv = wp / 4;  // uint4 per pair vector (== 32 J unless MULTI or J == 1)
   const uint4* t4 = reinterpret_cast<const uint4*>(table);
   for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_cand; i += warps) {
     const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
@@ -240,59 +240,71 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
     }
     // the candidate's columns, 32 at a time in lane registers (shuffled out per pair)
     const uint32_t c_lane = lane < L ? __ldg(cols + b + lane) : 0u;
-    uint4 f[J], r[J];
-#pragma unroll
-    for (int u = 0; u < J; ++u) {
-      // valid-row bits of the four words of slice v (word w covers rows [32 w, 32 w + 32))
-      const uint32_t v = u * 32 + lane;
-      uint32_t m[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t r0 = 32 * (4 * v + q);
-        m[q] = (v < nv && r0 < n_rows) ? (n_rows - r0 >= 32 ? 0xFFFFFFFFu : (1u << (n_rows - r0)) - 1u) : 0u;
-      }
-      f[u] = make_uint4(m[0], m[1], m[2], m[3]);
-      r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
-    }
-    uint32_t cp = __shfl_sync(kFull, c_lane, 0);
-    for (uint32_t k = 1; k < L; ++k) {
-      const uint32_t cc = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : __ldg(cols + b + k);
-      // all J loads unconditional, at immediate offsets from one base, so they
-      // issue back to back (a predicated load lets ptxas reuse one destination
-      // register and serialise the J round trips).  The host pads vectors of
-      // more than 32 slices to a multiple of 32 (nv == 32 J); below that the
-      // lanes past the vector re-read its last slice (same line; their
-      // accumulators start at 0)
-      const uint32_t lv = J == 1 ? min((uint32_t)lane, nv - 1) : (uint32_t)lane;
-      const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv + lv;
-      const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv + lv;
-      uint4 x[J], y[J];
-#pragma unroll
-      for (int u = 0; u < J; ++u) {
-        x[u] = __ldg(fwd + u * 32);
-        if (NEG) y[u] = __ldg(rev + u * 32);
-      }
-#pragma unroll
-      for (int u = 0; u < J; ++u) {
-        f[u].x &= x[u].x; f[u].y &= x[u].y; f[u].z &= x[u].z; f[u].w &= x[u].w;
-        if (NEG) {
-          r[u].x &= y[u].x; r[u].y &= y[u].y; r[u].z &= y[u].z; r[u].w &= y[u].w;
-        }
-      }
-      cp = cc;
-    }
     uint32_t n = 0;
+    // MULTI: vectors longer than 32 J slices are swept in passes of 32 J
+    for (uint32_t v0 = 0; v0 < (MULTI ? nv : 1u); v0 += 32 * J) {
+      uint4 f[J], r[J];
 #pragma unroll
-    for (int u = 0; u < J; ++u) {
-      const uint32_t v = u * 32 + lane;
-      const uint4 s = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
-      n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
-      if (MASK && v < nv) {
-        uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
-        const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+      for (int u = 0; u < J; ++u) {
+        // valid-row bits of the four words of slice v (word w covers rows [32 w, 32 w + 32))
+        const uint32_t v = v0 + u * 32 + lane;
+        uint32_t m[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (4 * v + q < mask_wpc) mw[q] = words[q];
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t r0 = 32 * (4 * v + q);
+          m[q] = (v < nv && r0 < n_rows) ? (n_rows - r0 >= 32 ? 0xFFFFFFFFu : (1u << (n_rows - r0)) - 1u) : 0u;
+        }
+        f[u] = make_uint4(m[0], m[1], m[2], m[3]);
+        r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
+      }
+      uint32_t cp = __shfl_sync(kFull, c_lane, 0);
+      for (uint32_t k = 1; k < L; ++k) {
+        const uint32_t cc = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : __ldg(cols + b + k);
+        // all J loads unconditional, at immediate offsets from one base, so they
+        // issue back to back (a predicated load lets ptxas reuse one destination
+        // register and serialise the J round trips).  The host pads vectors of
+        // more than 32 slices to a multiple of 32 (nv == 32 J); below that the
+        // lanes past the vector re-read its last slice (same line; their
+        // accumulators start at 0).  MULTI clamps every slice index instead.
+        const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv;
+        const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv;
+        uint4 x[J], y[J];
+        if constexpr (MULTI) {
+#pragma unroll
+          for (int u = 0; u < J; ++u) {
+            const uint32_t v = min(v0 + u * 32 + lane, nv - 1);
+            x[u] = __ldg(fwd + v);
+            if (NEG) y[u] = __ldg(rev + v);
+          }
+        } else {
+          const uint32_t lv = J == 1 ? min((uint32_t)lane, nv - 1) : (uint32_t)lane;
+#pragma unroll
+          for (int u = 0; u < J; ++u) {
+            x[u] = __ldg(fwd + lv + u * 32);
+            if (NEG) y[u] = __ldg(rev + lv + u * 32);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < J; ++u) {
+          f[u].x &= x[u].x; f[u].y &= x[u].y; f[u].z &= x[u].z; f[u].w &= x[u].w;
+          if (NEG) {
+            r[u].x &= y[u].x; r[u].y &= y[u].y; r[u].z &= y[u].z; r[u].w &= y[u].w;
+          }
+        }
+        cp = cc;
+      }
+#pragma unroll
+      for (int u = 0; u < J; ++u) {
+        const uint32_t v = v0 + u * 32 + lane;
+        const uint4 s = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+        n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
+        if (MASK && v < nv) {
+          uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
+          const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (4 * v + q < mask_wpc) mw[q] = words[q];
+        }
       }
     }
     n = __reduce_add_sync(kFull, n);

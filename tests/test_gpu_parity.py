@@ -626,3 +626,23 @@ def test_load_tsv_into_device_store(evaluator, tmp_path):
     for approx, neg in ((0.03, False), (0.0, True)):
         want = oracle.evaluate_population(ref_m, pop.cols, pop.offsets, approx, neg)
         np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
+
+
+@pytest.mark.parametrize("neg", [False, True])
+def test_pair_trend_index_long_vectors_many_candidates(evaluator, neg):
+    """Long pair vectors (40000 rows: 320 uint4 slices) and enough candidates
+    to select the multi-pass warp kernel; ragged last pass; vs the oracle."""
+    rng = np.random.default_rng(40)
+    R, Cn = 40000, 16
+    m = rng.standard_normal((R, Cn)).astype(np.float32)
+    m[:9000] = np.sort(m[:9000], axis=1)
+    pop = Population.from_sequences([rng.choice(Cn, size=int(rng.integers(1, 7)), replace=False)
+                                     for _ in range(5000)])
+    evaluator.upload(m)
+    evaluator.set_path(EBIC_PATH_TABLE)
+    try:
+        for approx in (0.03, 0.0):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
+    finally:
+        evaluator.set_path(EBIC_PATH_AUTO)
