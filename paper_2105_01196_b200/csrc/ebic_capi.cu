@@ -184,7 +184,8 @@ struct ebic_ctx {
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
-  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (warp per candidate up to 256 slices, CTA beyond), 1 warps everywhere, 2 CTAs everywhere (A/B)
+  int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
+  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (TMA warps up to 256 slices; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
 };
 
@@ -381,8 +382,50 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
                                 d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err,
                                 d_mask, ctx->ld / 32);
     };
-    if (neg) go(ebic::table_count_warp_kernel<8, true, MASK, true>);
-    else go(ebic::table_count_warp_kernel<8, false, MASK, true>);
+    if (neg) go(ebic::table_count_warp_multi_kernel<8, true, MASK>);
+    else go(ebic::table_count_warp_multi_kernel<8, false, MASK>);
+    ctx->launches++;
+    EBIC_CUDA(cudaGetLastError());
+    return EBIC_OK;
+  }
+  if (nv <= 256 && (ctx->table_kernel == 0 || ctx->table_kernel == 3)) {
+    // short vectors (the default): through the TMA engine -- bulk copies of
+    // whole pair vectors into per-warp shared-memory slots, mbarrier
+    // completion (27.5 vs 31 us for the register-load warp kernel at C3, ncu)
+    const uint32_t J = (nv + 31) / 32;
+    const int S = ctx->tma_slots;
+    const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + ebic::kTmaWarps - 1) / ebic::kTmaWarps, 1u << 30);
+    auto go = [&](auto kern) -> int {
+      EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, ebic::kTmaWarps * 32, smem, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
+                                                   (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand,
+                                                   (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,
+                                                   ctx->ld / 32);
+      return EBIC_OK;
+    };
+    auto pickj = [&](auto negc, auto sc) -> int {
+      constexpr bool N = decltype(negc)::value;
+      constexpr int SS = decltype(sc)::value;
+      switch (J) {
+        case 1: return go(ebic::table_count_tma_kernel<1, SS, N, MASK>);
+        case 2: return go(ebic::table_count_tma_kernel<2, SS, N, MASK>);
+        case 3: return go(ebic::table_count_tma_kernel<3, SS, N, MASK>);
+        case 4: return go(ebic::table_count_tma_kernel<4, SS, N, MASK>);
+        case 5: return go(ebic::table_count_tma_kernel<5, SS, N, MASK>);
+        case 6: return go(ebic::table_count_tma_kernel<6, SS, N, MASK>);
+        case 7: return go(ebic::table_count_tma_kernel<7, SS, N, MASK>);
+        default: return go(ebic::table_count_tma_kernel<8, SS, N, MASK>);
+      }
+    };
+    int st;
+    if (S >= 4) st = neg ? pickj(std::true_type{}, std::integral_constant<int, 4>{})
+                         : pickj(std::false_type{}, std::integral_constant<int, 4>{});
+    else if (S == 3) st = neg ? pickj(std::true_type{}, std::integral_constant<int, 3>{})
+                              : pickj(std::false_type{}, std::integral_constant<int, 3>{});
+    else st = neg ? pickj(std::true_type{}, std::integral_constant<int, 2>{})
+                  : pickj(std::false_type{}, std::integral_constant<int, 2>{});
+    EBIC_TRY(st);
     ctx->launches++;
     EBIC_CUDA(cudaGetLastError());
     return EBIC_OK;
@@ -934,6 +977,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (tb) ctx->table_budget_user = (uint64_t)std::strtoull(tb, nullptr, 10) << 20;
     const char* hp = std::getenv("EBIC_HOST_PIECES");
     if (hp) ctx->pipeline_pieces = std::max(1, std::min(4, std::atoi(hp)));
+    const char* ts = std::getenv("EBIC_TMA_SLOTS");
+    if (ts) ctx->tma_slots = std::max(2, std::min(4, std::atoi(ts)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");
     if (tk) ctx->table_kernel = std::atoi(tk);
     const char* sc = std::getenv("EBIC_PAIR_LAYOUT");

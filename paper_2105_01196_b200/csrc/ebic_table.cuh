@@ -13,9 +13,10 @@
 // with no shared-memory gathers.  supporting_rows (trend.cpp:48-54) is the same
 // AND, written out as the row mask (bit r = row r, natural order).
 //
-// Layout: table[(a * C + b) * wp + w], w < wp = round_up(ceil(R / 32), 32)
-// words per pair (every vector starts on a 128-byte line); bits of rows >= R
-// are zero.  Size
+// Layout: table[(a * C + b) * wp + w]; word w covers rows 32 w .. 32 w + 31
+// (even rows in the low half, odd rows in the high half: index_valid_bits);
+// wp = ceil(R / 32) rounded up to 4 words, or to 128 above 128 words; bits of
+// rows >= R are zero.  Size
 // C^2 * wp * 4 bytes: 2.5 GB at 20k x 1000 -- it is used when it fits the
 // context's memory budget, otherwise the slab kernels run.
 #pragma once
@@ -28,55 +29,95 @@ namespace ebic {
 constexpr int kTableBuildWarps = 32;   // a-columns per builder CTA
 constexpr int kTableRowsPerCta = 1024;  // rows per builder CTA (32 words)
 
-// Builder: CTA (row block rb, a-tile) -- warp w owns column a = a0 + w and keeps
-// the threshold keys of its 1024 rows in registers (lane l, i: row 32 i + l);
-// the CTA streams W_b blocks of every column b through shared memory (two
-// columns per barrier, the next two already loading into registers).  Word i
-// of B(a, b) is one ballot over the warp; lane i keeps it, so
-// the 32 words of a pair vector leave as one coalesced 128-byte store.
+// Bit order inside an index word.  Word w covers rows 32 w .. 32 w + 31 with
+// the EVEN rows in the low half and the ODD rows in the high half: bit j (j <
+// 16) is row 32 w + 2 j, bit 16 + j is row 32 w + 2 j + 1 -- the order in
+// which the builder's packed two-row compare produces them.  Counting does not
+// care; the valid-row masks and the row-mask output (supporting_rows) use
+// these helpers.
+__host__ __device__ __forceinline__ uint32_t index_valid_bits(uint32_t n_rows, uint32_t word) {
+  // branch-free: rem = valid rows of the word (0..32); rows 2j < rem fill the
+  // low half, rows 2j + 1 < rem the high half (shifts stay <= 16)
+  const uint32_t r0 = 32 * word;
+  const uint32_t rem = n_rows > r0 ? min(n_rows - r0, 32u) : 0u;
+  const uint32_t even = (rem + 1) >> 1, odd = rem >> 1;
+  return ((1u << even) - 1u) | (((1u << odd) - 1u) << 16);
+}
+__device__ __forceinline__ uint32_t spread_even(uint32_t x) {  // bit i of a 16-bit value -> bit 2 i
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+// index word -> natural order (bit k = row 32 w + k)
+__device__ __forceinline__ uint32_t index_to_natural(uint32_t w) {
+  return spread_even(w) | (spread_even(w >> 16) << 1);
+}
+
+// Builder: CTA = (row block of 1024 rows, tile of 32 columns a).  Warp w owns
+// column a = a0 + w; lane l owns the 32 rows of word l of the block and keeps
+// their negated thresholds as 16 packed row pairs (NT, as in the slab kernel:
+// 0 - (T_even | T_odd << 16) - 0x00010001).  The CTA streams every column b's
+// guarded ranks (Rg = R | 0x8000 per row, two rows per word) through shared
+// memory, two columns per barrier, the next two already loading.  For a pair
+// word, D = Rg(b) + NT(a) has bit 15 set iff R_b > T_a for the even row and
+// bit 31 for the odd row (ebic_simd.cuh), so one IADD tests two rows and one
+// shift + OR files both bits: 16 such steps make the lane's index word, and
+// the warp's 32 words leave as one coalesced 128-byte store.  About 2
+// instructions per output word (a ballot-based builder needs 5).  Shared
+// layout: pair j of word l at 16 l + (j ^ ((l >> 1) & 15)) -- conflict-free
+// for the 32 lanes reading pair j of their words at once.
 __global__ void __launch_bounds__(kTableBuildWarps * 32)
 build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
                         uint32_t wp, uint32_t* __restrict__ table) {
-  __shared__ uint32_t s_wb[2][2][kTableRowsPerCta];  // [iteration parity][column of the pair][row]
+  __shared__ uint32_t s_rg[2][2][kTableRowsPerCta / 2];  // [iteration parity][column of the pair][swizzled pair]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r0 = blockIdx.x * kTableRowsPerCta;
   const uint32_t a = blockIdx.y * kTableBuildWarps + warp;
   const bool a_ok = a < n_cols;
-  uint32_t ka[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const uint32_t r = r0 + 32 * i + lane;
-    // rows past the matrix never pass: no 32-bit word exceeds 0xFFFFFFFF
-    ka[i] = (a_ok && r < n_rows) ? plane_key(__ldg(plane + (uint64_t)a * ld + r)) : 0xFFFFFFFFu;
-  }
-  // W_b blocks, two columns per barrier, register double-buffered: the loads
-  // of the next two columns are in flight while the current two are compared
-  const uint32_t r = r0 + threadIdx.x;
-  auto fetch = [&](uint32_t b) -> uint32_t {
-    return (b < n_cols && r < n_rows) ? __ldg(plane + (uint64_t)b * ld + r) : 0u;
-  };
   const uint32_t w0 = r0 / 32;  // first word of this row block
-  uint32_t n0 = fetch(0), n1 = fetch(1);
+  // this lane's 32 rows of column a -> 16 negated threshold pairs
+  uint32_t nt[16];
+  {
+    const uint32_t rl = r0 + 32 * lane;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t re = rl + 2 * j;
+      const uint32_t te = (a_ok && re < n_rows) ? (__ldg(plane + (uint64_t)a * ld + re) & 0xFFFFu) : 0u;
+      const uint32_t to = (a_ok && re + 1 < n_rows) ? (__ldg(plane + (uint64_t)a * ld + re + 1) & 0xFFFFu) : 0u;
+      nt[j] = 0u - (te | (to << 16)) - 0x00010001u;
+    }
+  }
+  const uint32_t valid = a_ok ? index_valid_bits(n_rows, w0 + lane) : 0u;
+  // staging: thread t < 512 packs row pair t of column b, t >= 512 of column b + 1
+  const uint32_t tp = threadIdx.x & 511, th = threadIdx.x >> 9;
+  const uint32_t re = r0 + 2 * tp;
+  const uint32_t sidx = 16 * (tp >> 4) + ((tp & 15) ^ ((tp >> 5) & 15));  // pair j = tp & 15 of word l = tp >> 4
+  auto fetch = [&](uint32_t b) -> uint32_t {
+    if (b >= n_cols) return 0u;
+    const uint32_t we = re < n_rows ? __ldg(plane + (uint64_t)b * ld + re) : 0u;
+    const uint32_t wo = re + 1 < n_rows ? __ldg(plane + (uint64_t)b * ld + re + 1) : 0u;
+    return ((we >> 16) | 0x8000u) | (((wo >> 16) | 0x8000u) << 16);  // guarded ranks Rg of the pair
+  };
+  uint32_t nxt = fetch(th);
+  const uint32_t sw = (uint32_t)(lane >> 1) & 15u;
   int par = 0;
   for (uint32_t b = 0; b < n_cols; b += 2, par ^= 1) {
     // one barrier per two columns: the buffers alternate between iterations,
     // so writing this pair never races the previous pair's readers
-    s_wb[par][0][threadIdx.x] = n0;
-    s_wb[par][1][threadIdx.x] = n1;
+    s_rg[par][th][sidx] = nxt;
     __syncthreads();
-    n0 = fetch(b + 2);
-    n1 = fetch(b + 3);
+    nxt = fetch(b + 2 + th);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (b + h < n_cols) {
-        const uint32_t* wb = s_wb[par][h];
+        const uint32_t* rg = s_rg[par][h] + 16 * lane;
         uint32_t word = 0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const uint32_t bits = __ballot_sync(kFull, wb[32 * i + lane] > ka[i]);
-          if (lane == i) word = bits;
-        }
-        if (a_ok && w0 + lane < wp) table[((uint64_t)a * n_cols + b + h) * wp + w0 + lane] = word;
+        for (int j = 0; j < 16; ++j) word |= ((rg[j ^ sw] + nt[j]) & 0x80008000u) >> (15 - j);
+        if (a_ok && w0 + lane < wp) table[((uint64_t)a * n_cols + b + h) * wp + w0 + lane] = word & valid;
       }
     }
   }
@@ -128,10 +169,7 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
         const uint32_t v = v0 + u * T + t;
         uint32_t m[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t r0 = 32 * (4 * v + q);
-          m[q] = (v < nv && r0 < n_rows) ? (n_rows - r0 >= 32 ? 0xFFFFFFFFu : (1u << (n_rows - r0)) - 1u) : 0u;
-        }
+        for (int q = 0; q < 4; ++q) m[q] = v < nv ? index_valid_bits(n_rows, 4 * v + q) : 0u;
         f[u] = make_uint4(m[0], m[1], m[2], m[3]);
         r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
       }
@@ -186,7 +224,8 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
         n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
         if (MASK && v < nv) {
           uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
-          const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+          const uint32_t words[4] = {index_to_natural(s.x), index_to_natural(s.y), index_to_natural(s.z),
+                                     index_to_natural(s.w)};
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (4 * v + q < mask_wpc) mw[q] = words[q];
@@ -215,9 +254,102 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
 // the next candidate cost more in registers / occupancy than they gain; the
 // kernel runs at 70-90% of the random-2.5-KB-chunk read ceiling measured by
 // scripts/microbench/random_chunks.cu.)
-template <int J, bool NEG, bool MASK, bool MULTI = false>
+template <int J, bool NEG, bool MASK>
 __global__ void __launch_bounds__(256)
 table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
+                        const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
+                        uint32_t n_idx, uint32_t* __restrict__ out, int* err_out, uint32_t* __restrict__ mask,
+                        uint64_t mask_wpc) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t nv = wp / 4;  // uint4 per pair vector (<= 32 J)
+  const uint4* t4 = reinterpret_cast<const uint4*>(table);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_cand; i += warps) {
+    const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
+    const bool bad_offs = e <= b || e > n_idx;
+    const uint32_t L = bad_offs ? 0 : e - b;
+    bool badc = false;
+    for (uint32_t k = b + lane; k < b + L; k += 32) badc |= __ldg(cols + k) >= n_cols;
+    if (__any_sync(kFull, bad_offs || badc)) {
+      if (lane == 0) {
+        out[i] = 0;
+        *err_out = bad_offs ? 2 : 1;
+      }
+      continue;
+    }
+    if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
+      if (lane == 0) out[i] = n_rows;
+      if (MASK)
+        for (uint32_t w = lane; w < mask_wpc; w += 32) mask[(uint64_t)i * mask_wpc + w] =
+            index_to_natural(index_valid_bits(n_rows, w));
+      continue;
+    }
+    // the candidate's columns, 32 at a time in lane registers (shuffled out per pair)
+    const uint32_t c_lane = lane < L ? __ldg(cols + b + lane) : 0u;
+    // accumulators start all-ones: the index has no bits past the last row, so
+    // after the first pair they hold exactly the supporting rows
+    uint4 f[J], r[J];
+#pragma unroll
+    for (int u = 0; u < J; ++u) {
+      f[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    uint32_t cp = __shfl_sync(kFull, c_lane, 0);
+    for (uint32_t k = 1; k < L; ++k) {
+      const uint32_t cc = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : __ldg(cols + b + k);
+      // all J loads unconditional, at immediate offsets from one base, so they
+      // issue back to back (a predicated load lets ptxas reuse one destination
+      // register and serialise the J round trips).  The host pads vectors of
+      // more than 32 slices to a multiple of 32 (nv == 32 J); below that the
+      // lanes past the vector re-read its last slice (same line; their
+      // accumulators start at 0)
+      const uint32_t lv = J == 1 ? min((uint32_t)lane, nv - 1) : (uint32_t)lane;
+      const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv + lv;
+      const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv + lv;
+      uint4 x[J], y[J];
+#pragma unroll
+      for (int u = 0; u < J; ++u) {
+        x[u] = __ldg(fwd + u * 32);
+        if (NEG) y[u] = __ldg(rev + u * 32);
+      }
+#pragma unroll
+      for (int u = 0; u < J; ++u) {
+        f[u].x &= x[u].x; f[u].y &= x[u].y; f[u].z &= x[u].z; f[u].w &= x[u].w;
+        if (NEG) {
+          r[u].x &= y[u].x; r[u].y &= y[u].y; r[u].z &= y[u].z; r[u].w &= y[u].w;
+        }
+      }
+      cp = cc;
+    }
+    uint32_t n = 0;
+#pragma unroll
+    for (int u = 0; u < J; ++u) {
+      const uint32_t v = u * 32 + lane;
+      const uint4 o = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+      // (J == 1: lanes past the vector re-read its last slice -- drop them)
+      const uint4 s = (J > 1 || v < nv) ? o : make_uint4(0u, 0u, 0u, 0u);
+      n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
+      if (MASK && v < nv) {
+        uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
+        const uint32_t words[4] = {index_to_natural(s.x), index_to_natural(s.y), index_to_natural(s.z),
+                                   index_to_natural(s.w)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (4 * v + q < mask_wpc) mw[q] = words[q];
+      }
+    }
+    n = __reduce_add_sync(kFull, n);
+    if (lane == 0) out[i] = n;
+  }
+}
+
+// Long vectors (> 256 slices) with many candidates: the same warp-per-
+// candidate scheme sweeping the vectors in passes of 32 J slices (every slice
+// index clamped, loads still unconditional).  A separate kernel so that the
+// single-pass kernel above keeps its register allocation and load schedule.
+template <int J, bool NEG, bool MASK, bool MULTI = true>
+__global__ void __launch_bounds__(256)
+table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
                         const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
                         uint32_t n_idx, uint32_t* __restrict__ out, int* err_out, uint32_t* __restrict__ mask,
                         uint64_t mask_wpc) {
@@ -250,10 +382,7 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
         const uint32_t v = v0 + u * 32 + lane;
         uint32_t m[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t r0 = 32 * (4 * v + q);
-          m[q] = (v < nv && r0 < n_rows) ? (n_rows - r0 >= 32 ? 0xFFFFFFFFu : (1u << (n_rows - r0)) - 1u) : 0u;
-        }
+        for (int q = 0; q < 4; ++q) m[q] = v < nv ? index_valid_bits(n_rows, 4 * v + q) : 0u;
         f[u] = make_uint4(m[0], m[1], m[2], m[3]);
         r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
       }
@@ -300,11 +429,164 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
         n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
         if (MASK && v < nv) {
           uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
-          const uint32_t words[4] = {s.x, s.y, s.z, s.w};
+          const uint32_t words[4] = {index_to_natural(s.x), index_to_natural(s.y), index_to_natural(s.z),
+                                     index_to_natural(s.w)};
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (4 * v + q < mask_wpc) mw[q] = words[q];
         }
+      }
+    }
+    n = __reduce_add_sync(kFull, n);
+    if (lane == 0) out[i] = n;
+  }
+}
+
+// TMA variant of the warp-per-candidate kernel (short vectors, nv <= 256
+// slices).  One elected lane issues a bulk copy (cp.async.bulk, the TMA
+// engine) per pair vector -- S pairs at a time, into the warp's shared-memory
+// slots -- that completes on the warp's mbarrier; the lanes then read their
+// slices from shared memory.  The HBM requests of all S pairs are in flight at
+// once with no registers tied up (the register-load version is at the mercy
+// of ptxas interleaving its loads with the ANDs), and a 2.5-KB pair vector is
+// one copy instruction instead of 160 vector loads.
+constexpr int kTmaWarps = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <int J, int S, bool NEG, bool MASK>
+__global__ void __launch_bounds__(kTmaWarps * 32)
+table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
+                       const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
+                       uint32_t n_idx, uint32_t* __restrict__ out, int* err_out, uint32_t* __restrict__ mask,
+                       uint64_t mask_wpc) {
+  extern __shared__ __align__(128) unsigned char smem[];  // [warp][S (x2 with NEG)][pair vector]
+  __shared__ __align__(8) uint64_t s_bar[kTmaWarps];    // "full": the slots' bulk copies have landed
+  __shared__ __align__(8) uint64_t s_empty[kTmaWarps];  // "empty": all 32 lanes are done reading the slots
+  constexpr int NS = NEG ? 2 * S : S;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nv = wp / 4, slot = wp * 4;  // uint4 / bytes per pair vector
+  const uint32_t my = smem_u32(smem) + (uint32_t)warp * NS * slot;
+  const uint32_t bar = smem_u32(&s_bar[warp]), empty = smem_u32(&s_empty[warp]);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(empty, 32);
+  }
+  __syncwarp();
+  uint32_t phase = 0, ephase = 0;
+  const uint32_t warps = gridDim.x * kTmaWarps;
+  for (uint32_t i = blockIdx.x * kTmaWarps + warp; i < n_cand; i += warps) {
+    const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
+    const bool bad_offs = e <= b || e > n_idx;
+    const uint32_t L = bad_offs ? 0 : e - b;
+    bool badc = false;
+    for (uint32_t k = b + lane; k < b + L; k += 32) badc |= __ldg(cols + k) >= n_cols;
+    if (__any_sync(kFull, bad_offs || badc)) {
+      if (lane == 0) {
+        out[i] = 0;
+        *err_out = bad_offs ? 2 : 1;
+      }
+      continue;
+    }
+    if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
+      if (lane == 0) out[i] = n_rows;
+      if (MASK)
+        for (uint32_t w = lane; w < mask_wpc; w += 32)
+          mask[(uint64_t)i * mask_wpc + w] = index_to_natural(index_valid_bits(n_rows, w));
+      continue;
+    }
+    const uint32_t c_lane = lane < L ? __ldg(cols + b + lane) : 0u;
+    uint4 f[J], r[J];
+#pragma unroll
+    for (int u = 0; u < J; ++u) {
+      f[u] = make_uint4(~0u, ~0u, ~0u, ~0u);  // the index has no bits past the last row
+      r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    uint32_t cp = __shfl_sync(kFull, c_lane, 0);
+    for (uint32_t k0 = 1; k0 < L; k0 += S) {
+      const uint32_t g = min((uint32_t)S, L - k0);  // pairs in this group (warp-uniform)
+      uint32_t pc[S + 1];
+      pc[0] = cp;
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint32_t k = k0 + q;
+        pc[q + 1] = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : (k < L ? __ldg(cols + b + k) : 0u);
+      }
+      if (lane == 0) {
+        mbar_expect_tx(bar, g * slot * (NEG ? 2u : 1u));
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          if ((uint32_t)q < g) {
+            bulk_g2s(my + q * slot, table + ((uint64_t)pc[q] * n_cols + pc[q + 1]) * wp, slot, bar);
+            if (NEG) bulk_g2s(my + (S + q) * slot, table + ((uint64_t)pc[q + 1] * n_cols + pc[q]) * wp, slot, bar);
+          }
+        }
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        if ((uint32_t)q < g) {
+#pragma unroll
+          for (int u = 0; u < J; ++u) {
+            // (J == 1: a vector shorter than the warp -- lanes past it re-read
+            // its last slice instead of another slot; their result is dropped)
+            const uint32_t v = J == 1 ? min((uint32_t)lane, nv - 1) : u * 32 + lane;
+            const uint4 x = lds<uint4>(my + q * slot + v * 16);
+            f[u].x &= x.x; f[u].y &= x.y; f[u].z &= x.z; f[u].w &= x.w;
+            if (NEG) {
+              const uint4 y = lds<uint4>(my + (S + q) * slot + v * 16);
+              r[u].x &= y.x; r[u].y &= y.y; r[u].z &= y.z; r[u].w &= y.w;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 1; q <= S; ++q)
+        if ((uint32_t)q == g) cp = pc[q];
+      // release the slots: every lane arrives once its reads are done; the
+      // issuing lane waits for all 32 before the next bulk copies refill them
+      // (the canonical consumer-release / producer-acquire handshake)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty) : "memory");
+      if (lane == 0) mbar_wait(empty, ephase);
+      ephase ^= 1u;
+      __syncwarp();
+    }
+    uint32_t n = 0;
+#pragma unroll
+    for (int u = 0; u < J; ++u) {
+      const uint32_t v = u * 32 + lane;
+      const uint4 o = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+      const uint4 s = v < nv ? o : make_uint4(0u, 0u, 0u, 0u);  // (lanes past a short vector)
+      n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
+      if (MASK && v < nv) {
+        uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
+        const uint32_t words[4] = {index_to_natural(s.x), index_to_natural(s.y), index_to_natural(s.z),
+                                   index_to_natural(s.w)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (4 * v + q < mask_wpc) mw[q] = words[q];
       }
     }
     n = __reduce_add_sync(kFull, n);
