@@ -160,17 +160,20 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
       }
       continue;
     }
+    if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
+      if (t == 0) out[i] = n_rows;
+      if (MASK)
+        for (uint32_t w = t; w < mask_wpc; w += T)
+          mask[(uint64_t)i * mask_wpc + w] = index_to_natural(index_valid_bits(n_rows, w));
+      continue;
+    }
     uint32_t n = 0;
     for (uint32_t v0 = 0; v0 < nv; v0 += T * J) {
+      // accumulators start all-ones: the index has no bits past the last row
       uint4 f[J], r[J];
 #pragma unroll
       for (int u = 0; u < J; ++u) {
-        // valid-row bits of the four words of slice v (word w covers rows [32 w, 32 w + 32))
-        const uint32_t v = v0 + u * T + t;
-        uint32_t m[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) m[q] = v < nv ? index_valid_bits(n_rows, 4 * v + q) : 0u;
-        f[u] = make_uint4(m[0], m[1], m[2], m[3]);
+        f[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
         r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
       }
       uint32_t cp = __ldg(cols + b);
@@ -220,7 +223,8 @@ table_count_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t
 #pragma unroll
       for (int u = 0; u < J; ++u) {
         const uint32_t v = v0 + u * T + t;
-        const uint4 s = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+        const uint4 o = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+        const uint4 s = v < nv ? o : make_uint4(0u, 0u, 0u, 0u);  // (threads past the vector re-read its end)
         n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
         if (MASK && v < nv) {
           uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
@@ -370,20 +374,22 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
       }
       continue;
     }
+    if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
+      if (lane == 0) out[i] = n_rows;
+      if (MASK)
+        for (uint32_t w = lane; w < mask_wpc; w += 32)
+          mask[(uint64_t)i * mask_wpc + w] = index_to_natural(index_valid_bits(n_rows, w));
+      continue;
+    }
     // the candidate's columns, 32 at a time in lane registers (shuffled out per pair)
     const uint32_t c_lane = lane < L ? __ldg(cols + b + lane) : 0u;
     uint32_t n = 0;
     // MULTI: vectors longer than 32 J slices are swept in passes of 32 J
     for (uint32_t v0 = 0; v0 < (MULTI ? nv : 1u); v0 += 32 * J) {
-      uint4 f[J], r[J];
+      uint4 f[J], r[J];  // all-ones: the index has no bits past the last row
 #pragma unroll
       for (int u = 0; u < J; ++u) {
-        // valid-row bits of the four words of slice v (word w covers rows [32 w, 32 w + 32))
-        const uint32_t v = v0 + u * 32 + lane;
-        uint32_t m[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) m[q] = v < nv ? index_valid_bits(n_rows, 4 * v + q) : 0u;
-        f[u] = make_uint4(m[0], m[1], m[2], m[3]);
+        f[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
         r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
       }
       uint32_t cp = __shfl_sync(kFull, c_lane, 0);
@@ -425,7 +431,8 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
 #pragma unroll
       for (int u = 0; u < J; ++u) {
         const uint32_t v = v0 + u * 32 + lane;
-        const uint4 s = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+        const uint4 o = NEG ? make_uint4(f[u].x | r[u].x, f[u].y | r[u].y, f[u].z | r[u].z, f[u].w | r[u].w) : f[u];
+        const uint4 s = v < nv ? o : make_uint4(0u, 0u, 0u, 0u);  // (clamped re-reads past the vector)
         n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
         if (MASK && v < nv) {
           uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
