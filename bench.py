@@ -479,7 +479,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     ev.set_stream(None)
     host0 = np.array(call(pops[0], tp), copy=True)
     parity_dev_vs_host = (bool(np.array_equal(dev_counts[:len(host0)], host0))
-                          if (args.shard == "rows" or replica) else None)
+                          if (world == 1 or args.shard == "rows" or replica) else None)
 
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -290,6 +291,21 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   return EBIC_OK;
 }
 
+// Raise a kernel's dynamic shared-memory limit to the opt-in maximum, once per
+// (kernel, device): the attribute call is a driver round trip, so it stays off
+// the per-launch path.  Keyed by the kernel's address (the instantiations of
+// one template share a function TYPE, so a per-type static would not do).
+int allow_max_smem(const void* kern, const ebic_ctx* ctx) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == kern && d.second == ctx->device) return EBIC_OK;
+  EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ctx->smem_optin - 1024)));
+  done.emplace_back(kern, ctx->device);
+  return EBIC_OK;
+}
+
 // ---- pair-trend index ------------------------------------------------------
 // Device memory the index may take out of `free_bytes`: all but a reserve of
 // max(8 GiB, 10%) for the caller's own buffers (a B200 has 180 GB of HBM: a
@@ -397,7 +413,7 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
     const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + ebic::kTmaWarps - 1) / ebic::kTmaWarps, 1u << 30);
     auto go = [&](auto kern) -> int {
-      EBIC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(kern), ctx));
       kern<<<grid, ebic::kTmaWarps * 32, smem, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
                                                    (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand,
                                                    (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,

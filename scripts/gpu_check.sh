@@ -47,3 +47,7 @@ for f in $OUT/prof_*_$TAG.ncu-rep; do
   esac
 done
 du -sh $OUT
+# memory / race checking of every kernel family, and the ingest benchmark
+bash scripts/gpu_sanitize.sh $TAG
+timeout 900 python scripts/ingest_bench.py > $OUT/ingest_$TAG.txt 2>&1
+echo done
