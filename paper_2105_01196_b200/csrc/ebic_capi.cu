@@ -306,6 +306,23 @@ int allow_max_smem(const void* kern, const ebic_ctx* ctx) {
   return EBIC_OK;
 }
 
+// Resident CTAs per SM of a kernel at a block size / dynamic shared memory
+// (cached: the occupancy query is a driver call).
+int resident_ctas(const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& c : cache)
+    if (c.first.first == kern && c.first.second == smem) return c.second;
+  int n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache.push_back({{kern, smem}, std::max(1, n)});
+  return std::max(1, n);
+}
+
 // ---- pair-trend index ------------------------------------------------------
 // Device memory the index may take out of `free_bytes`: all but a reserve of
 // max(8 GiB, 10%) for the caller's own buffers (a B200 has 180 GB of HBM: a
@@ -411,9 +428,13 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     const uint32_t J = (nv + 31) / 32;
     const int S = ctx->tma_slots;
     const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
-    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + ebic::kTmaWarps - 1) / ebic::kTmaWarps, 1u << 30);
     auto go = [&](auto kern) -> int {
       EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(kern), ctx));
+      // persistent warps: as many CTAs as are resident at once (the kernel
+      // pipelines each warp's candidates), never more than the candidates need
+      const uint64_t per_sm = (uint64_t)resident_ctas(reinterpret_cast<const void*>(kern), ebic::kTmaWarps * 32, smem);
+      const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + ebic::kTmaWarps - 1) / ebic::kTmaWarps,
+                                                         std::max<uint64_t>(1, per_sm) * ctx->n_sms);
       kern<<<grid, ebic::kTmaWarps * 32, smem, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
                                                    (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand,
                                                    (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,

@@ -502,28 +502,52 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
   }
   __syncwarp();
   uint32_t phase = 0, ephase = 0;
+  // Persistent warps, software-pipelined over candidates: the next candidate's
+  // offsets are loaded at the top of an iteration and its columns once the
+  // first bulk copies have landed, so the offsets -> columns -> pair vectors
+  // chain of one candidate overlaps the previous candidate's copies.
   const uint32_t warps = gridDim.x * kTmaWarps;
-  for (uint32_t i = blockIdx.x * kTmaWarps + warp; i < n_cand; i += warps) {
-    const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
+  uint32_t i = blockIdx.x * kTmaWarps + warp;
+  uint32_t b = 0, e = 0, c_lane = 0;
+  if (i < n_cand) {
+    b = __ldg(offs + i);
+    e = __ldg(offs + i + 1);
+    const uint32_t L0 = (e > b && e <= n_idx) ? e - b : 0u;
+    c_lane = lane < L0 ? __ldg(cols + b + lane) : 0u;
+  }
+  for (; i < n_cand; i += warps) {
+    const uint32_t inext = i + warps;
+    uint32_t bn = 0, en = 0, cn = 0;
+    bool next_cols = false;
+    if (inext < n_cand) {  // in flight while this candidate is processed
+      bn = __ldg(offs + inext);
+      en = __ldg(offs + inext + 1);
+    }
+    auto fetch_next_cols = [&]() {
+      if (next_cols) return;
+      next_cols = true;
+      const uint32_t Ln = (inext < n_cand && en > bn && en <= n_idx) ? en - bn : 0u;
+      cn = lane < Ln ? __ldg(cols + bn + lane) : 0u;
+    };
+    do {  // one candidate; `break` = done with it
     const bool bad_offs = e <= b || e > n_idx;
     const uint32_t L = bad_offs ? 0 : e - b;
-    bool badc = false;
-    for (uint32_t k = b + lane; k < b + L; k += 32) badc |= __ldg(cols + k) >= n_cols;
+    bool badc = lane < L && c_lane >= n_cols;
+    for (uint32_t k = b + 32 + lane; k < b + L; k += 32) badc |= __ldg(cols + k) >= n_cols;
     if (__any_sync(kFull, bad_offs || badc)) {
       if (lane == 0) {
         out[i] = 0;
         *err_out = bad_offs ? 2 : 1;
       }
-      continue;
+      break;
     }
     if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
       if (lane == 0) out[i] = n_rows;
       if (MASK)
         for (uint32_t w = lane; w < mask_wpc; w += 32)
           mask[(uint64_t)i * mask_wpc + w] = index_to_natural(index_valid_bits(n_rows, w));
-      continue;
+      break;
     }
-    const uint32_t c_lane = lane < L ? __ldg(cols + b + lane) : 0u;
     uint4 f[J], r[J];
 #pragma unroll
     for (int u = 0; u < J; ++u) {
@@ -552,6 +576,7 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
       }
       mbar_wait(bar, phase);
       phase ^= 1u;
+      fetch_next_cols();  // the next candidate's offsets have arrived by now
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         if ((uint32_t)q < g) {
@@ -598,6 +623,11 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
     }
     n = __reduce_add_sync(kFull, n);
     if (lane == 0) out[i] = n;
+    } while (false);
+    fetch_next_cols();
+    b = bn;
+    e = en;
+    c_lane = cn;
   }
 }
 
