@@ -97,3 +97,26 @@ def test_last_error_is_thread_local(L):
     t.start()
     t.join()
     assert seen == [b""]
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/ebic.h is a C ABI: it compiles as C99 (no C++ or torch types) and
+    a C program that calls every entry point links against libebic.so."""
+    import re
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    hdr = REPO / "include" / "ebic.h"
+    names = re.findall(r"^\w[\w\s\*]*?\b(ebic_\w+)\s*\(", hdr.read_text(), flags=re.M)
+    calls = "\n".join(f"  (void)&{n};" for n in sorted(set(names)))
+    src = tmp_path / "use.c"
+    src.write_text(f'#include "ebic.h"\nint main(void) {{\n{calls}\n  return ebic_abi_version() > 0 ? 0 : 1;\n}}\n')
+    lib_dir = REPO / "paper_2105_01196_b200"
+    res = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-pedantic", f"-I{REPO / 'include'}", str(src),
+                          f"-L{lib_dir}", "-lebic", f"-Wl,-rpath,{lib_dir}", "-o", str(tmp_path / "use")],
+                         capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    assert subprocess.run([str(tmp_path / "use")]).returncode == 0
