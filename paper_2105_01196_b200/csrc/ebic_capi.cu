@@ -397,6 +397,11 @@ int use_table(ebic_ctx* ctx, double approx, cudaStream_t s, bool* yes) {
   return EBIC_OK;
 }
 
+// True when launch_table takes the TMA kernel (short pair vectors).
+bool tma_table_kernel(const ebic_ctx* ctx) {
+  return table_wp(ctx) / 4 <= 256 && (ctx->table_kernel == 0 || ctx->table_kernel == 3);
+}
+
 // Counts WRITTEN to out (any device-accessible pointer), optional row masks.
 // n_idx bounds the offsets (checked on device).
 template <bool MASK>
@@ -421,7 +426,7 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     EBIC_CUDA(cudaGetLastError());
     return EBIC_OK;
   }
-  if (nv <= 256 && (ctx->table_kernel == 0 || ctx->table_kernel == 3)) {
+  if (tma_table_kernel(ctx)) {
     // short vectors (the default): through the TMA engine -- bulk copies of
     // whole pair vectors into per-warp shared-memory slots, mbarrier
     // completion (27.5 vs 31 us for the register-load warp kernel at C3, ncu)
