@@ -157,6 +157,19 @@ int ebic_support_rows_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t*
                             uint64_t n_cand, double approx, int negative_trends,
                             uint32_t* rows_out, uint64_t cap, uint64_t* row_offsets);
 
+/* Row-set overlaps of a batch, for the archive's overlap filter without row
+ * lists (reference: TopRankList::insert evolution.cpp:76-105,
+ * induced_jaccard evolution.cpp:44-51, sorted_intersection_size).
+ * sizes_out[i] = |supporting_rows(c_i)| (n_cand entries) and
+ * inter_out[i * n_cand + j] = |supporting_rows(c_i) n supporting_rows(c_j)|
+ * (n_cand * n_cand entries, symmetric, diagonal = sizes).  The row sets stay on
+ * the device as bitmasks; only the counts come back.  At most
+ * EBIC_OVERLAP_MAX candidates per call. */
+#define EBIC_OVERLAP_MAX 4096
+int ebic_support_overlap_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
+                               uint64_t n_cand, double approx, int negative_trends,
+                               uint64_t* sizes_out, uint64_t* inter_out);
+
 /* Single (row, candidate) predicate on device.  `row` is a GLOBAL row index
  * inside the resident shard. */
 int ebic_row_supports(ebic_ctx* ctx, uint64_t row, const uint32_t* cols, uint32_t len,

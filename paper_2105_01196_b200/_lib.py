@@ -46,6 +46,7 @@ SIGNATURES = {
     "ebic_eval_wait": (C.c_int, [_vp, C.c_uint64]),
     "ebic_support_rows": (C.c_int, [_vp, _vp, C.c_uint32, C.c_double, C.c_int, _vp, C.c_uint64, _u64p]),
     "ebic_support_rows_batch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double, C.c_int, _vp, C.c_uint64, _vp]),
+    "ebic_support_overlap_batch": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double, C.c_int, _vp, _vp]),
     "ebic_row_supports": (C.c_int, [_vp, C.c_uint64, _vp, C.c_uint32, C.c_double, C.c_int, C.POINTER(C.c_int)]),
     "ebic_fitness": (C.c_double, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ebic_ctx_launch_count": (C.c_int, [_vp, _u64p]),

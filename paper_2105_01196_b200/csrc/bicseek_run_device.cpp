@@ -13,11 +13,17 @@
 //     random_chromosome/chromosome_hash, same Rng).  Evaluation consumes no
 //     randomness, so every K offspring are handed to the pinned-memory marshaller
 //     (ebic_eval_submit).  The GPU counts chunk k while chunk k+1 is bred.
-//  3. Archive row sets come in batches.  TopRankList::insert (evolution.cpp:76-105)
-//     needs supporting_rows only for candidates that can place.  When the next
-//     insert needs rows, the driver fetches them, in one ebic_support_rows_batch,
-//     for every following offspring that could place under the current archive.
-//     Rows are a pure function of the candidate, so speculation is exact.
+//  3. The archive's overlap filter runs on device counts.  TopRankList::insert
+//     (evolution.cpp:76-105) needs a candidate's rows only through
+//     induced_jaccard (:44-51): |rows|, and |rows n entry.rows| for each entry.
+//     When the next insert needs them, one ebic_support_overlap_batch over
+//     [the entries, that candidate and the following offspring that could place
+//     under the current archive] returns the sizes and pairwise intersections
+//     from row bitmasks that never leave the device; only the emitted
+//     biclusters' row lists are fetched, once, at the end.  Rows are a pure
+//     function of the candidate, so speculation is exact, and the Jaccard
+//     arithmetic on those integers is the reference's.  (EBIC_ARCHIVE_ROWS=1
+//     fetches row lists instead, with ebic_support_rows_batch.)
 //
 // The archive acceptance rule, the operator draw, the breeding loop and the
 // small helpers the reference keeps in an anonymous namespace are re-expressed
@@ -29,6 +35,7 @@
 #include <tuple>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -70,11 +77,13 @@ bool archive_before(const RankedIndividual& x, const RankedIndividual& y) {
 }
 
 // Cell Jaccard of an archive entry and a candidate bicluster (evolution.cpp:44-51):
-// cells are products, so the intersection is |rows n| * |cols n|.
-double cell_overlap(const TopRankEntry& e, const std::vector<std::size_t>& rows,
-                    const std::vector<std::size_t>& sorted_cols) {
-  const std::size_t shared = sorted_intersection_size(e.rows, rows) * sorted_intersection_size(e.cols, sorted_cols);
-  const std::size_t cells_e = e.rows.size() * e.cols.size(), cells_c = rows.size() * sorted_cols.size();
+// cells are products, so the intersection is |rows n| * |cols n|.  The row
+// intersection and the two row-set sizes come in as counts (from the row lists,
+// or from the device's row bitmasks); the arithmetic is the reference's.
+double cell_overlap(std::size_t shared_rows, std::size_t rows_e, const std::vector<std::size_t>& cols_e,
+                    std::size_t rows_c, const std::vector<std::size_t>& sorted_cols) {
+  const std::size_t shared = shared_rows * sorted_intersection_size(cols_e, sorted_cols);
+  const std::size_t cells_e = rows_e * cols_e.size(), cells_c = rows_c * sorted_cols.size();
   return static_cast<double>(shared) / static_cast<double>(cells_e + cells_c - shared);
 }
 
@@ -154,13 +163,34 @@ class ChunkedEval {
   std::vector<std::vector<uint32_t>> outs_;  // stable storage: written when the ticket is waited
 };
 
+// An archive entry: the reference's TopRankEntry plus its row-set size and an
+// id for the overlap counts.  In overlap mode `rows` stays empty until the run
+// ends (only the emitted entries' rows are fetched).
+struct Entry : TopRankEntry {
+  std::size_t n_rows = 0;
+  std::uint64_t uid = 0;
+};
+
+// What the acceptance rule needs to know about a candidate's rows.
+struct CandidateRows {
+  std::size_t n_rows = 0;
+  std::uint64_t uid = 0;
+  std::vector<std::size_t> rows;                      // row-list mode
+  std::unordered_map<std::uint64_t, std::size_t> shared;  // overlap mode: entry uid -> |rows n|
+  bool lists = false;
+  std::size_t shared_with(const Entry& e) const {
+    return lists ? sorted_intersection_size(e.rows, rows) : shared.at(e.uid);
+  }
+};
+
 // The top-rank archive (evolution.hpp:78-98): the acceptance rule of
-// TopRankList::insert (evolution.cpp:76-105), fed with precomputed row sets.
+// TopRankList::insert (evolution.cpp:76-105), fed with precomputed row data.
 class Archive {
  public:
   Archive(std::size_t capacity, double overlap) : capacity_(capacity), overlap_(overlap) {}
 
-  const std::vector<TopRankEntry>& entries() const { return entries_; }
+  const std::vector<Entry>& entries() const { return entries_; }
+  std::vector<Entry>& entries() { return entries_; }
   bool full() const { return entries_.size() >= capacity_; }
   double min_score() const { return entries_.empty() ? 0.0 : entries_.back().ind.score; }
 
@@ -170,19 +200,22 @@ class Archive {
     return ind.score > 0.0 && !(full() && ind.score <= min_score());
   }
 
-  bool insert(const RankedIndividual& ind, const std::vector<std::size_t>& rows) {
+  bool insert(const RankedIndividual& ind, const CandidateRows& cr) {
     if (!could_place(ind)) return false;
-    TopRankEntry fresh;
+    Entry fresh;
     fresh.ind = ind;
-    fresh.rows = rows;
+    if (cr.lists) fresh.rows = cr.rows;
+    fresh.n_rows = cr.n_rows;
+    fresh.uid = cr.uid;
     fresh.cols = ind.chromosome.columns;
     std::sort(fresh.cols.begin(), fresh.cols.end());
     // entries overlapping the candidate too much are displaced -- unless one of
     // them scores at least as high, in which case the candidate is rejected
     std::vector<char> displaced(entries_.size(), 0);
     for (std::size_t i = 0; i < entries_.size(); ++i) {
-      if (cell_overlap(entries_[i], fresh.rows, fresh.cols) < overlap_) continue;
-      if (entries_[i].ind.score >= ind.score) return false;
+      const Entry& e = entries_[i];
+      if (cell_overlap(cr.shared_with(e), e.n_rows, e.cols, cr.n_rows, fresh.cols) < overlap_) continue;
+      if (e.ind.score >= ind.score) return false;
       displaced[i] = 1;
     }
     std::size_t keep = 0;
@@ -194,66 +227,138 @@ class Archive {
     entries_.resize(keep);
     // entries are kept in archive order: the candidate goes before the first
     // entry it outranks
-    const auto at = std::upper_bound(entries_.begin(), entries_.end(), fresh,
-                                     [](const TopRankEntry& a, const TopRankEntry& b) {
-                                       return archive_before(a.ind, b.ind);
-                                     });
+    const auto at = std::upper_bound(entries_.begin(), entries_.end(), fresh, [](const Entry& a, const Entry& b) {
+      return archive_before(a.ind, b.ind);
+    });
     entries_.insert(at, std::move(fresh));
     if (entries_.size() > capacity_) entries_.resize(capacity_);
     // placed iff it survived the truncation
-    return std::any_of(entries_.begin(), entries_.end(), [&](const TopRankEntry& e) {
+    return std::any_of(entries_.begin(), entries_.end(), [&](const Entry& e) {
       return e.ind.score == ind.score && e.ind.chromosome.columns == ind.chromosome.columns;
     });
   }
 
  private:
-  std::vector<TopRankEntry> entries_;
+  std::vector<Entry> entries_;
   std::size_t capacity_;
   double overlap_;
 };
 
-// Serial archive inserts in offspring order, with speculative batched row sets.
+void append_candidate(const Chromosome& c, std::vector<uint32_t>& cols, std::vector<uint32_t>& offs) {
+  for (std::size_t x : c.columns) cols.push_back(static_cast<uint32_t>(x));
+  offs.push_back(static_cast<uint32_t>(cols.size()));
+}
+
+// Serial archive inserts in offspring order, with speculative batches.  When
+// the next insert needs row data, the driver computes it for that candidate
+// and up to batch-1 following offspring that could place under the current
+// archive -- rows are a pure function of the candidate, so speculation is
+// exact.  Two modes:
+//  * overlap (default): one ebic_support_overlap_batch over [current entries,
+//    picked candidates] returns the row-set sizes and pairwise intersection
+//    counts; no row list crosses the bus.  A cached candidate is reused only
+//    if its counts cover every entry now in the archive.
+//  * lists (EBIC_ARCHIVE_ROWS=1, or an archive too large for one overlap
+//    batch): ebic_support_rows_batch row lists, intersected on the host.
 class RowBatcher {
  public:
-  RowBatcher(Device& dev, std::size_t batch) : dev_(dev), batch_(std::max<std::size_t>(batch, 1)) {}
+  RowBatcher(Device& dev, std::size_t batch, bool lists) : dev_(dev), batch_(std::max<std::size_t>(batch, 1)),
+                                                           lists_(lists) {}
 
-  const std::vector<std::size_t>& rows_for(std::size_t i, const std::vector<RankedIndividual>& inds,
-                                           const Archive& arch) {
+  bool lists() const { return lists_; }
+
+  const CandidateRows& rows_for(std::size_t i, const std::vector<RankedIndividual>& inds, const Archive& arch) {
     auto it = cache_.find(i);
-    if (it != cache_.end()) return it->second;
+    if (it != cache_.end() && covers(it->second, arch)) return it->second;
     // i itself plus up to batch-1 later candidates that could place right now
     std::vector<std::size_t> pick{i};
     for (std::size_t k = i + 1; k < inds.size() && pick.size() < batch_; ++k)
       if (arch.could_place(inds[k]) && cache_.find(k) == cache_.end()) pick.push_back(k);
-    std::vector<uint32_t> cols, offs{0};
-    for (std::size_t k : pick) {
-      for (std::size_t c : inds[k].chromosome.columns) cols.push_back(static_cast<uint32_t>(c));
-      offs.push_back(static_cast<uint32_t>(cols.size()));
-    }
-    std::vector<uint64_t> row_offs(pick.size() + 1);
-    std::vector<uint32_t> rows(cap_);
-    int st = ebic_support_rows_batch(dev_.ctx, cols.data(), offs.data(), pick.size(), dev_.approx, dev_.neg,
-                                     rows.data(), rows.size(), row_offs.data());
-    if (st == EBIC_ERR_CAPACITY) {
-      cap_ = row_offs.back() + row_offs.back() / 2;
-      rows.assign(cap_, 0);
-      st = ebic_support_rows_batch(dev_.ctx, cols.data(), offs.data(), pick.size(), dev_.approx, dev_.neg,
-                                   rows.data(), rows.size(), row_offs.data());
-    }
-    check(st, "supporting_rows");
-    for (std::size_t b = 0; b < pick.size(); ++b)
-      cache_[pick[b]] = std::vector<std::size_t>(rows.begin() + static_cast<std::ptrdiff_t>(row_offs[b]),
-                                                 rows.begin() + static_cast<std::ptrdiff_t>(row_offs[b + 1]));
-    return cache_[i];
+    if (lists_) fetch_lists(pick, inds);
+    else fetch_overlaps(pick, inds, arch);
+    return cache_.at(i);
   }
 
   void clear() { cache_.clear(); }
 
+  // row lists of the given chromosomes (the emitted entries at the end of a run)
+  std::vector<std::vector<std::size_t>> lists_of(const std::vector<const Chromosome*>& cs) {
+    std::vector<uint32_t> cols, offs{0};
+    for (const Chromosome* c : cs) append_candidate(*c, cols, offs);
+    std::vector<uint64_t> row_offs(cs.size() + 1);
+    std::vector<uint32_t> rows(cap_);
+    int st = ebic_support_rows_batch(dev_.ctx, cols.data(), offs.data(), cs.size(), dev_.approx, dev_.neg,
+                                     rows.data(), rows.size(), row_offs.data());
+    if (st == EBIC_ERR_CAPACITY) {
+      cap_ = row_offs.back() + row_offs.back() / 2;
+      rows.assign(cap_, 0);
+      st = ebic_support_rows_batch(dev_.ctx, cols.data(), offs.data(), cs.size(), dev_.approx, dev_.neg,
+                                   rows.data(), rows.size(), row_offs.data());
+    }
+    check(st, "supporting_rows");
+    std::vector<std::vector<std::size_t>> out(cs.size());
+    for (std::size_t b = 0; b < cs.size(); ++b)
+      out[b].assign(rows.begin() + static_cast<std::ptrdiff_t>(row_offs[b]),
+                    rows.begin() + static_cast<std::ptrdiff_t>(row_offs[b + 1]));
+    return out;
+  }
+
  private:
+  bool covers(const CandidateRows& cr, const Archive& arch) const {
+    if (cr.lists) return true;
+    for (const Entry& e : arch.entries())
+      if (!cr.shared.count(e.uid)) return false;
+    return true;
+  }
+
+  void fetch_lists(const std::vector<std::size_t>& pick, const std::vector<RankedIndividual>& inds) {
+    std::vector<const Chromosome*> cs;
+    for (std::size_t k : pick) cs.push_back(&inds[k].chromosome);
+    auto rows = lists_of(cs);
+    for (std::size_t b = 0; b < pick.size(); ++b) {
+      CandidateRows& cr = cache_[pick[b]];
+      cr.lists = true;
+      cr.rows = std::move(rows[b]);
+      cr.n_rows = cr.rows.size();
+      cr.uid = next_uid_++;
+    }
+  }
+
+  void fetch_overlaps(const std::vector<std::size_t>& pick, const std::vector<RankedIndividual>& inds,
+                      const Archive& arch) {
+    const auto& ents = arch.entries();
+    std::vector<uint32_t> cols, offs{0};
+    std::vector<std::uint64_t> uids;
+    for (const Entry& e : ents) {
+      append_candidate(e.ind.chromosome, cols, offs);
+      uids.push_back(e.uid);
+    }
+    for (std::size_t k : pick) {
+      append_candidate(inds[k].chromosome, cols, offs);
+      uids.push_back(next_uid_++);
+    }
+    const std::size_t n = uids.size();
+    std::vector<uint64_t> sizes(n), inter(n * n);
+    check(ebic_support_overlap_batch(dev_.ctx, cols.data(), offs.data(), n, dev_.approx, dev_.neg, sizes.data(),
+                                     inter.data()),
+          "supporting_rows overlaps");
+    for (std::size_t b = 0; b < pick.size(); ++b) {
+      const std::size_t q = ents.size() + b;
+      CandidateRows& cr = cache_[pick[b]];
+      cr = CandidateRows{};
+      cr.n_rows = sizes[q];
+      cr.uid = uids[q];
+      for (std::size_t j = 0; j < n; ++j)
+        if (j != q) cr.shared[uids[j]] = inter[q * n + j];
+    }
+  }
+
   Device& dev_;
   std::size_t batch_;
+  bool lists_;
   std::size_t cap_ = 1 << 16;
-  std::unordered_map<std::size_t, std::vector<std::size_t>> cache_;
+  std::uint64_t next_uid_ = 1;
+  std::unordered_map<std::size_t, CandidateRows> cache_;
 };
 
 struct State {
@@ -320,7 +425,9 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
 
   Device dev(m, p.trend, device);
   const std::size_t chunk = std::max<std::size_t>(256, p.population_size / 4);
-  RowBatcher rows(dev, 64);
+  const char* lists_env = std::getenv("EBIC_ARCHIVE_ROWS");
+  const bool lists = (lists_env && std::atoi(lists_env)) || p.top_rank_capacity() + 64 > EBIC_OVERLAP_MAX;
+  RowBatcher rows(dev, 64, lists);
 
   // init_state (evolution.cpp:233-246)
   State st(p.top_rank_capacity(), p.overlap_threshold, p.seed);
@@ -365,11 +472,19 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
   }
 
   RunResult result;
-  for (const auto& entry : st.top_rank.entries()) {
-    if (result.biclusters.size() >= p.num_biclusters) break;
+  std::vector<Entry*> emit;
+  for (auto& entry : st.top_rank.entries()) {
+    if (emit.size() >= p.num_biclusters) break;
     if (entry.ind.support_count < p.trend.min_rows) continue;
-    result.biclusters.biclusters.emplace_back(entry.rows, entry.cols);
+    emit.push_back(&entry);
   }
+  if (!rows.lists() && !emit.empty()) {  // overlap mode: the emitted entries' rows, in one batch
+    std::vector<const Chromosome*> cs;
+    for (const Entry* e : emit) cs.push_back(&e->ind.chromosome);
+    auto lists_out = rows.lists_of(cs);
+    for (std::size_t b = 0; b < emit.size(); ++b) emit[b]->rows = std::move(lists_out[b]);
+  }
+  for (const Entry* e : emit) result.biclusters.biclusters.emplace_back(e->rows, e->cols);
   result.report.generations = st.generation;
   result.report.termination = reason;
   result.report.wall_time_seconds =

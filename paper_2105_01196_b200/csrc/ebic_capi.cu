@@ -145,6 +145,8 @@ struct ebic_ctx {
   DevBuf<uint32_t> d_mask, d_rows, d_tmp_cols, d_tmp_offs, d_tmp_counts;
   DevBuf<uint64_t> d_row_offsets;
   HostBuf<uint32_t> h_tmp_counts;
+  DevBuf<uint32_t> d_inter;  // ebic_support_overlap_batch: n x n intersections
+  HostBuf<uint32_t> h_inter;
   // slab_pair_kernel: per-candidate partial-count accumulators and per-chunk
   // arrival counters, both zero between launches (the kernel re-zeroes them)
   DevBuf<uint32_t> d_acc, d_done;
@@ -1053,6 +1055,8 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   ctx->d_tmp_counts.release();
   ctx->d_row_offsets.release();
   ctx->h_tmp_counts.release();
+  ctx->d_inter.release();
+  ctx->h_inter.release();
   ebic_xchg_destroy(ctx);
   ctx->d_acc.release();
   ctx->d_done.release();
@@ -1404,6 +1408,49 @@ int ebic_support_rows_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t*
   EBIC_CUDA(cudaGetLastError());
   EBIC_CUDA(cudaMemcpyAsync(rows_out, ctx->d_rows.p, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   EBIC_CUDA(cudaStreamSynchronize(s));
+  return EBIC_OK;
+}
+
+int ebic_support_overlap_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
+                               double approx, int negative_trends, uint64_t* sizes_out, uint64_t* inter_out) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(check_approx(approx));
+  if (n_cand > EBIC_OVERLAP_MAX)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "%llu candidates (at most %d per overlap batch)",
+                (unsigned long long)n_cand, EBIC_OVERLAP_MAX);
+  if (n_cand && (!sizes_out || !inter_out)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+  EBIC_TRY(validate_population(ctx, cols, offsets, n_cand));
+  EBIC_TRY(set_device(ctx));
+  if (n_cand == 0) return EBIC_OK;
+  cudaStream_t s = ctx->stream;
+  const uint64_t n_idx = offsets[n_cand];
+  const uint64_t wpc = ctx->ld / 32;  // mask words per candidate
+  const uint64_t nn = n_cand * n_cand;
+  EBIC_TRY(ensure(ctx->d_tmp_cols, n_idx));
+  EBIC_TRY(ensure(ctx->d_tmp_offs, n_cand + 1));
+  EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
+  EBIC_TRY(ensure(ctx->h_tmp_counts, n_cand));
+  EBIC_TRY(ensure(ctx->d_mask, n_cand * wpc));
+  EBIC_TRY(ensure(ctx->d_inter, nn));
+  EBIC_TRY(ensure(ctx->h_inter, nn));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, cols, n_idx * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_offs.p, offsets, (n_cand + 1) * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s));
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_tmp_counts.p, 0, n_cand * sizeof(uint32_t), s));
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_mask.p, 0, n_cand * wpc * sizeof(uint32_t), s));
+  EBIC_TRY(launch_count<true>(ctx, ctx->d_tmp_cols.p, ctx->d_tmp_offs.p, n_cand, approx, negative_trends,
+                              ctx->d_tmp_counts.p, ctx->d_mask.p, s));
+  const dim3 grid((unsigned)n_cand, (unsigned)((n_cand + ebic::kOverlapTile - 1) / ebic::kOverlapTile));
+  ebic::overlap_popc_kernel<<<grid, ebic::kOverlapThreads, 0, s>>>(ctx->d_mask.p, wpc, (ctx->n_rows + 31) / 32,
+                                                                  (uint32_t)n_cand, ctx->d_inter.p);
+  ctx->launches++;
+  EBIC_CUDA(cudaGetLastError());
+  EBIC_CUDA(cudaMemcpyAsync(ctx->h_tmp_counts.p, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s));
+  EBIC_CUDA(cudaMemcpyAsync(ctx->h_inter.p, ctx->d_inter.p, nn * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  EBIC_CUDA(cudaStreamSynchronize(s));
+  for (uint64_t i = 0; i < n_cand; ++i) sizes_out[i] = ctx->h_tmp_counts.p[i];
+  for (uint64_t k = 0; k < nn; ++k) inter_out[k] = ctx->h_inter.p[k];
   return EBIC_OK;
 }
 

@@ -326,6 +326,49 @@ scatter_rows_kernel(const uint32_t* __restrict__ mask, uint64_t words_per_cand, 
 }
 
 // ---------------------------------------------------------------------------
+// overlap_popc_kernel: pairwise row-set intersections of a batch, from its
+// row bitmasks -- the |rows_a n rows_b| of induced_jaccard (evolution.cpp:44-51)
+// without row lists.  CTA (i, t) pairs candidate i with candidates
+// [t*kOverlapTile, +kOverlapTile) at or above the diagonal; each thread ANDs
+// its words of mask i with the tile's masks, then a block reduction.  Both
+// inter[i*n + j] and inter[j*n + i] are written.
+// ---------------------------------------------------------------------------
+constexpr int kOverlapTile = 8;
+constexpr int kOverlapThreads = 256;
+
+__global__ void __launch_bounds__(kOverlapThreads)
+overlap_popc_kernel(const uint32_t* __restrict__ mask, uint64_t words_per_cand, uint64_t n_words_valid,
+                    uint32_t n, uint32_t* __restrict__ inter) {
+  const uint32_t i = blockIdx.x, j0 = blockIdx.y * kOverlapTile;
+  if (j0 + kOverlapTile <= i) return;  // the tile is wholly below the diagonal
+  const uint32_t* mi = mask + (uint64_t)i * words_per_cand;
+  uint32_t c[kOverlapTile] = {};
+  for (uint64_t w = threadIdx.x; w < n_words_valid; w += kOverlapThreads) {
+    const uint32_t a = mi[w];
+#pragma unroll
+    for (int t = 0; t < kOverlapTile; ++t)
+      if (j0 + t < n && j0 + t >= i) c[t] += __popc(a & mask[(uint64_t)(j0 + t) * words_per_cand + w]);
+  }
+  __shared__ uint32_t s_part[kOverlapThreads / 32][kOverlapTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < kOverlapTile; ++t) {
+    const uint32_t v = __reduce_add_sync(kFull, c[t]);
+    if (lane == 0) s_part[warp][t] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kOverlapTile) {
+    const uint32_t j = j0 + threadIdx.x;
+    if (j < n && j >= i) {
+      uint32_t v = 0;
+      for (int w = 0; w < kOverlapThreads / 32; ++w) v += s_part[w][threadIdx.x];
+      inter[(uint64_t)i * n + j] = v;
+      inter[(uint64_t)j * n + i] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // single (row, candidate) predicate with the reference arithmetic
 // ---------------------------------------------------------------------------
 template <typename T>

@@ -320,6 +320,19 @@ class Evaluator:
             break
         return [rows[offs[i]:offs[i + 1]].copy() for i in range(n)]
 
+    def support_overlaps(self, pop, params: TrendParams | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """Row-set sizes and pairwise intersections of a batch without row lists
+        (the |rows_a n rows_b| of induced_jaccard, evolution.cpp:44-51):
+        returns (sizes[n], inter[n, n]) as uint64."""
+        p = params or TrendParams()
+        pop = _as_population(pop)
+        n = len(pop)
+        sizes = np.zeros(n, dtype=np.uint64)
+        inter = np.zeros((n, n), dtype=np.uint64)
+        check(self._L.ebic_support_overlap_batch(self._h, _ptr(pop.cols), _ptr(pop.offsets), n, float(p.approx),
+                                                  int(bool(p.negative_trends)), _ptr(sizes), _ptr(inter)))
+        return sizes, inter
+
     def row_supports(self, row: int, chromosome: Sequence[int], params: TrendParams | None = None) -> bool:
         p = params or TrendParams()
         cols = np.ascontiguousarray(chromosome, dtype=np.uint32)

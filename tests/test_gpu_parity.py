@@ -646,3 +646,58 @@ def test_pair_trend_index_long_vectors_many_candidates(evaluator, neg):
             np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
+
+
+def _overlap_want(m, seqs, approx, neg):
+    rows = [oracle.supporting_rows(m, s, approx, neg) for s in seqs]
+    n = len(seqs)
+    inter = np.zeros((n, n), dtype=np.uint64)
+    for i in range(n):
+        for j in range(n):
+            inter[i, j] = np.intersect1d(rows[i], rows[j], assume_unique=True).size
+    return np.array([r.size for r in rows], dtype=np.uint64), inter
+
+
+@pytest.mark.parametrize("R", [1, 33, 1000, 4099])
+@pytest.mark.parametrize("neg", [False, True])
+def test_support_overlaps_vs_oracle(path_evaluator, R, neg):
+    """ebic_support_overlap_batch: sizes and pairwise |rows_i n rows_j| equal the
+    reference row lists' intersections (evolution.cpp:44-51's counts), on every
+    path; duplicates in the batch, single-column candidates (all rows), and
+    sizes straddling the overlap kernel's 8-candidate tiles."""
+    rng = np.random.default_rng(R)
+    m = rng.standard_normal((R, 40)).astype(np.float32).astype(np.float64)
+    m[:, 5] = m[:, 4]  # ties
+    seqs = [list(rng.choice(40, size=int(rng.integers(2, 7)), replace=False)) for _ in range(17)]
+    seqs += [seqs[3], [7], [4, 5], [5, 4]]
+    path_evaluator.upload(m)
+    approx = 0.03
+    sizes, inter = path_evaluator.support_overlaps(seqs, TrendParams(approx=approx, negative_trends=neg))
+    ws, wi = _overlap_want(m, seqs, approx, neg)
+    np.testing.assert_array_equal(sizes, ws)
+    np.testing.assert_array_equal(inter, wi)
+    counts = path_evaluator.evaluate_population(seqs, TrendParams(approx=approx, negative_trends=neg))
+    np.testing.assert_array_equal(sizes, counts.astype(np.uint64))
+
+
+def test_support_overlaps_edges(evaluator):
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((500, 20)).astype(np.float32)
+    evaluator.upload(m)
+    s, i = evaluator.support_overlaps([])
+    assert s.size == 0 and i.size == 0
+    with pytest.raises(EbicError):
+        evaluator.support_overlaps([[0, 99]])  # column out of range
+    with pytest.raises(EbicError):
+        evaluator.support_overlaps([[0, 1]] * 4097)  # over EBIC_OVERLAP_MAX
+    # the largest batch: a symmetric matrix whose diagonal is the counts
+    pop = synth.random_population(4096, 20, seed=2)
+    sizes, inter = evaluator.support_overlaps(pop)
+    np.testing.assert_array_equal(np.diag(inter), sizes)
+    np.testing.assert_array_equal(inter, inter.T)
+    np.testing.assert_array_equal(sizes, evaluator.evaluate_population(pop).astype(np.uint64))
+    k = [0, 17, 4095]
+    rows = evaluator.supporting_rows_batch(Population.from_sequences([pop.sequence(x) for x in k]))
+    for a in range(3):
+        for b in range(3):
+            assert inter[k[a], k[b]] == np.intersect1d(rows[a], rows[b]).size

@@ -7,6 +7,7 @@ The binaries are built in the build container by oracle/Makefile (`device`)
 from the reference sources and travel to the GPU box prebuilt.
 """
 import json
+import os
 import subprocess
 
 import pytest
@@ -46,22 +47,32 @@ def test_run_config1_byte_identical_to_reference(label):
     assert got["termination"] == golden["termination"]
 
 
+def _archive_env(mode):
+    env = dict(os.environ)
+    env["EBIC_ARCHIVE_ROWS"] = "1" if mode == "lists" else "0"
+    return env
+
+
+@pytest.mark.parametrize("archive", ["overlaps", "lists"])
 @pytest.mark.parametrize("label", ["default", "forced200", "neg_forced60"])
-def test_device_aware_driver_byte_identical_to_reference(label):
+def test_device_aware_driver_byte_identical_to_reference(label, archive):
     """The device-aware evolution driver (csrc/bicseek_run_device.cpp: one upload
-    per run, evaluation overlapped with breeding, batched archive row sets)
-    returns exactly the reference run()'s result on BASELINE config 1."""
+    per run, evaluation overlapped with breeding, batched archive row data --
+    device-side overlap counts by default, host row lists with
+    EBIC_ARCHIVE_ROWS=1) returns exactly the reference run()'s result on
+    BASELINE config 1."""
     exe = _need("run_device_overlap")
     golden = json.loads((GOLDEN / "run_cfg1.json").read_text())[label]
     out = subprocess.run([str(exe), "--engine", "device", *golden["args"]], check=True, capture_output=True,
-                         text=True, timeout=600).stdout
+                         text=True, timeout=600, env=_archive_env(archive)).stdout
     got = json.loads(out)
     assert json.dumps(got["result"], sort_keys=True) == json.dumps(golden["result"], sort_keys=True)
     assert got["generations"] == golden["generations"]
     assert got["termination"] == golden["termination"]
 
 
-def test_device_aware_driver_matches_reference_at_scale():
+@pytest.mark.parametrize("archive", ["overlaps", "lists"])
+def test_device_aware_driver_matches_reference_at_scale(archive):
     """A larger run (10k x 500, P=1024, 15 generations, negatives on): the
     driver's output equals the unchanged reference GA on the device TU."""
     exe_a, exe_b = _need("run_device"), _need("run_device_overlap")
@@ -70,7 +81,7 @@ def test_device_aware_driver_matches_reference_at_scale():
     a = json.loads(subprocess.run([str(exe_a), *args], check=True, capture_output=True, text=True,
                                   timeout=600).stdout)
     b = json.loads(subprocess.run([str(exe_b), "--engine", "device", *args], check=True, capture_output=True,
-                                  text=True, timeout=600).stdout)
+                                  text=True, timeout=600, env=_archive_env(archive)).stdout)
     assert a["result"] == b["result"] and a["generations"] == b["generations"]
 
 
