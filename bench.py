@@ -411,7 +411,9 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     # pair-trend index in use: the kernel streams (L - 1) pair vectors of wp
     # words per candidate (x2 with negatives) -- its PHYSICAL HBM traffic
     index_bytes, index_used = ev.index_info()
-    wp = ((e - b + 31) // 32 + 3) // 4 * 4
+    # words per pair vector as laid out in HBM (the index is C x C vectors)
+    wp = (index_bytes // (4 * cfg["cols"] ** 2) if index_used and index_bytes
+          else ((e - b + 31) // 32 + 3) // 4 * 4)
     n_pairs = [int(dp[3]) - int(dp[2]) for dp in d_pops]
     phys_bytes = [4.0 * wp * npair * (2 if cfg["negative"] else 1) for npair in n_pairs]
     per_step_bytes = [alg_bytes[i % n_pops] for i in range(args.steps)]

@@ -339,6 +339,11 @@ constexpr int kTableNoMemory = -1;  // internal status: the index does not fit (
 // Words per pair vector: a multiple of 4 (uint4 slices); vectors of more than
 // 32 slices are padded to a multiple of 32 slices, so the warp kernel's lanes
 // own exactly J = nv / 32 slices each (unpredicated loads).
+// Words per pair vector: whole uint4 slices, and whole 32-slice groups (128
+// words, 512 B) above 128 words -- the register-load kernels read those with
+// unpredicated loads, and the TMA kernel measured faster on 512-B-aligned
+// vectors than on tight ones (C3: 27.4 us with 640 words vs 28.5 us with 628,
+// 200-step A/B on one box, profiles/r1f_index_padding.txt).
 uint64_t table_wp(const ebic_ctx* ctx) {
   const uint64_t words = (ctx->n_rows + 31) / 32;
   return words > 128 ? (words + 127) / 128 * 128 : (words + 3) / 4 * 4;

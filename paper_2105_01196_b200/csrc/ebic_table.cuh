@@ -582,9 +582,9 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
         if ((uint32_t)q < g) {
 #pragma unroll
           for (int u = 0; u < J; ++u) {
-            // (J == 1: a vector shorter than the warp -- lanes past it re-read
-            // its last slice instead of another slot; their result is dropped)
-            const uint32_t v = J == 1 ? min((uint32_t)lane, nv - 1) : u * 32 + lane;
+            // (the last group of slices: lanes past the vector re-read its
+            // last slice instead of another slot; their result is dropped)
+            const uint32_t v = u == J - 1 ? min((uint32_t)(u * 32 + lane), nv - 1) : u * 32 + lane;
             const uint4 x = lds<uint4>(my + q * slot + v * 16);
             f[u].x &= x.x; f[u].y &= x.y; f[u].z &= x.z; f[u].w &= x.w;
             if (NEG) {

@@ -30,7 +30,7 @@ rng = np.random.default_rng(0)
 ev = Evaluator(0)
 ok = True
 keep = []
-for R, Cn in ((700, 40), (300, 700), (257, 1500), (40000, 12)):
+for R, Cn in ((700, 40), (300, 700), (257, 1500), (5000, 30), (40000, 12)):
     m = rng.standard_normal((R, Cn)).astype(np.float32)
     pop = synth.random_population(200, Cn, 2, min(9, Cn), seed=1)
     paths = (EBIC_PATH_AUTO, EBIC_PATH_TABLE, EBIC_PATH_PLANE, EBIC_PATH_PLANE_U32, EBIC_PATH_VALUE)

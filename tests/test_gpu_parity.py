@@ -506,7 +506,7 @@ def test_zero_copy_host_path(evaluator, layout, path):
 
 
 
-@pytest.mark.parametrize("R", [1, 31, 32, 33, 127, 1000, 1037, 4099])
+@pytest.mark.parametrize("R", [1, 31, 32, 33, 127, 1000, 1037, 4099, 4129, 10000, 20000, 32768, 32800])
 @pytest.mark.parametrize("n_cols", [2, 37, 300])
 def test_pair_trend_index_vs_oracle(evaluator, R, n_cols):
     """The pair-trend index (forced) against the C oracle: ragged row counts
