@@ -125,7 +125,10 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
 
 /* Device pointers, asynchronous on `stream` (NULL = the context's stream).
  * d_counts is overwritten.  Invalid columns / empty candidates are detected on
- * device, counted as 0 and reported by the next ebic_ctx_sync(). */
+ * device, counted as 0 and reported by the next ebic_ctx_sync().  The
+ * context's device scratch is shared by its launches: work of one context
+ * submitted on different streams must not overlap in time (order it, or use
+ * one context per stream). */
 int ebic_eval_counts_device(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
                             uint64_t n_cand, double approx, int negative_trends,
                             uint32_t* d_counts, void* stream);
