@@ -629,23 +629,34 @@ def test_load_tsv_into_device_store(evaluator, tmp_path):
 
 
 @pytest.mark.parametrize("neg", [False, True])
-def test_pair_trend_index_long_vectors_many_candidates(evaluator, neg):
-    """Long pair vectors (40000 rows: 320 uint4 slices) and enough candidates
-    to select the multi-pass warp kernel; ragged last pass; vs the oracle."""
-    rng = np.random.default_rng(40)
-    R, Cn = 40000, 16
-    m = rng.standard_normal((R, Cn)).astype(np.float32)
-    m[:9000] = np.sort(m[:9000], axis=1)
-    pop = Population.from_sequences([rng.choice(Cn, size=int(rng.integers(1, 7)), replace=False)
-                                     for _ in range(5000)])
-    evaluator.upload(m)
-    evaluator.set_path(EBIC_PATH_TABLE)
+def test_pair_trend_index_long_vectors_many_candidates(neg):
+    """Long pair vectors (40000 rows: 1280 words, 320 uint4 slices) and enough
+    candidates to select the multi-pass warp kernel; ragged last pass; vs the
+    oracle.  Counts (twice), row masks, and a bad column (error)."""
+    from paper_2105_01196_b200 import Evaluator
+    ev = Evaluator(0)
     try:
-        for approx in (0.03, 0.0):
+        rng = np.random.default_rng(40)
+        R, Cn = 40000, 16
+        m = rng.standard_normal((R, Cn)).astype(np.float32)
+        m[:9000] = np.sort(m[:9000], axis=1)
+        seqs = [rng.choice(Cn, size=int(rng.integers(1, 7)), replace=False) for _ in range(5000)]
+        pop = Population.from_sequences(seqs)
+        ev.upload(m)
+        ev.set_path(EBIC_PATH_TABLE)
+        for approx in (0.03, 0.0, 0.03):
             want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
-            np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
+            np.testing.assert_array_equal(ev.evaluate_population(pop, TrendParams(approx, neg)), want)
+        rows = ev.supporting_rows_batch(pop, TrendParams(0.03, neg))
+        for j in (0, 1, 2, 4999):
+            np.testing.assert_array_equal(rows[j], oracle.supporting_rows(m, seqs[j], 0.03, neg))
+        bad = seqs[:4900] + [[0, Cn]] + seqs[4900:]
+        with pytest.raises(EbicError):
+            ev.evaluate_population(bad, TrendParams(0.03, neg))
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, neg)
+        np.testing.assert_array_equal(ev.evaluate_population(pop, TrendParams(0.03, neg)), want)
     finally:
-        evaluator.set_path(EBIC_PATH_AUTO)
+        ev.close()
 
 
 def _overlap_want(m, seqs, approx, neg):
