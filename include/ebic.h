@@ -91,6 +91,16 @@ int ebic_matrix_upload_f64(ebic_ctx* ctx, const double* row_major, uint64_t n_ro
 /* Same for row-major float32 input (always exact; stored as float32). */
 int ebic_matrix_upload_f32(ebic_ctx* ctx, const float* row_major, uint64_t n_rows,
                            uint64_t n_cols, uint64_t row_base);
+/* The same two from DEVICE memory on the context's GPU -- e.g. a row-major
+ * buffer an NCCL broadcast filled (the replicated matrix is
+ * uploaded once and broadcast over NVLink).  The buffer is checked and
+ * transposed in place (not modified) and may be freed after the call.  Its
+ * contents must be complete when the call is made (synchronise the stream
+ * that filled it). */
+int ebic_matrix_upload_device_f64(ebic_ctx* ctx, const double* d_row_major, uint64_t n_rows,
+                                  uint64_t n_cols, uint64_t row_base, int store, int* store_out);
+int ebic_matrix_upload_device_f32(ebic_ctx* ctx, const float* d_row_major, uint64_t n_rows,
+                                  uint64_t n_cols, uint64_t row_base);
 /* Shape of the resident matrix.  Any out pointer may be NULL. */
 int ebic_matrix_info(ebic_ctx* ctx, uint64_t* n_rows, uint64_t* n_cols, uint64_t* ld,
                      int* store, uint64_t* row_base);

@@ -38,6 +38,8 @@ SIGNATURES = {
     "ebic_ctx_sync": (C.c_int, [_vp]),
     "ebic_matrix_upload_f64": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_int)]),
     "ebic_matrix_upload_f32": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "ebic_matrix_upload_device_f64": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_int)]),
+    "ebic_matrix_upload_device_f32": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_uint64]),
     "ebic_matrix_info": (C.c_int, [_vp, _u64p, _u64p, _u64p, C.POINTER(C.c_int), _u64p]),
     "ebic_matrix_free": (C.c_int, [_vp]),
     "ebic_eval_counts": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double, C.c_int, _vp]),

@@ -853,9 +853,11 @@ int need_matrix(const ebic_ctx* ctx) {
   return EBIC_OK;
 }
 
+// `src` is host memory, or (src_on_device) a buffer on this context's GPU that
+// is read in place (checked and transposed from it; the caller keeps it).
 template <typename TI>
 int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols, uint64_t row_base,
-                int store, int* store_out) {
+                int store, int* store_out, bool src_on_device = false) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
   if (!host && n_rows * n_cols) return fail(EBIC_ERR_INVALID_ARGUMENT, "null matrix pointer");
   if (n_rows == 0 || n_cols == 0) return fail(EBIC_ERR_INVALID_ARGUMENT, "matrix must be non-empty");
@@ -868,12 +870,28 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   cudaStream_t s = ctx->stream;
   const uint64_t n = n_rows * n_cols;
 
+  if (src_on_device) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, host) != cudaSuccess || a.type != cudaMemoryTypeDevice ||
+        a.device != ctx->device) {
+      cudaGetLastError();
+      return fail(EBIC_ERR_INVALID_ARGUMENT, "matrix pointer is not device memory on device %d", ctx->device);
+    }
+  }
   TI* d_in = nullptr;
-  EBIC_CUDA(cudaMalloc(&d_in, n * sizeof(TI)));
-  cudaError_t ce = cudaMemcpyAsync(d_in, host, n * sizeof(TI), cudaMemcpyHostToDevice, s);
+  cudaError_t ce = cudaSuccess;
+  if (src_on_device) {
+    d_in = const_cast<TI*>(host);
+  } else {
+    EBIC_CUDA(cudaMalloc(&d_in, n * sizeof(TI)));
+    ce = cudaMemcpyAsync(d_in, host, n * sizeof(TI), cudaMemcpyHostToDevice, s);
+  }
+  auto release_in = [&]() {
+    if (!src_on_device) cudaFree(d_in);
+  };
   if (ce == cudaSuccess) ce = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s);
   if (ce != cudaSuccess) {
-    cudaFree(d_in);
+    release_in();
     return fail(EBIC_ERR_CUDA, "matrix upload: %s", cudaGetErrorString(ce));
   }
   {
@@ -885,18 +903,18 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   ce = cudaMemcpyAsync(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
   if (ce != cudaSuccess) {
-    cudaFree(d_in);
+    release_in();
     return fail(EBIC_ERR_CUDA, "matrix check: %s", cudaGetErrorString(ce));
   }
   if (flags & 1) {
-    cudaFree(d_in);
+    release_in();
     return fail(EBIC_ERR_INVALID_ARGUMENT, "ExpressionMatrix: non-finite value");
   }
   const bool exact = !(flags & 2);
   int chosen = store;
   if (chosen == EBIC_STORE_AUTO) chosen = exact ? EBIC_STORE_F32 : EBIC_STORE_F64;
   if (chosen == EBIC_STORE_F32 && !exact) {
-    cudaFree(d_in);
+    release_in();
     return fail(EBIC_ERR_NOT_EXACT, "matrix has values that are not float32-representable");
   }
   const uint64_t ld = (n_rows + ebic::kRowAlign - 1) / ebic::kRowAlign * ebic::kRowAlign;
@@ -904,7 +922,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   void* d_mat = nullptr;
   ce = cudaMalloc(&d_mat, ld * n_cols * esz);
   if (ce != cudaSuccess) {
-    cudaFree(d_in);
+    release_in();
     return fail(EBIC_ERR_CUDA, "matrix store alloc (%llu bytes): %s",
                 (unsigned long long)(ld * n_cols * esz), cudaGetErrorString(ce));
   }
@@ -916,7 +934,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   ctx->launches++;
   ce = cudaGetLastError();
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-  cudaFree(d_in);
+  release_in();
   if (ce != cudaSuccess) {
     cudaFree(d_mat);
     return fail(EBIC_ERR_CUDA, "matrix transpose: %s", cudaGetErrorString(ce));
@@ -1105,6 +1123,16 @@ int ebic_matrix_upload_f64(ebic_ctx* ctx, const double* row_major, uint64_t n_ro
 int ebic_matrix_upload_f32(ebic_ctx* ctx, const float* row_major, uint64_t n_rows, uint64_t n_cols,
                            uint64_t row_base) {
   return upload_impl<float>(ctx, row_major, n_rows, n_cols, row_base, EBIC_STORE_F32, nullptr);
+}
+
+int ebic_matrix_upload_device_f64(ebic_ctx* ctx, const double* d_row_major, uint64_t n_rows, uint64_t n_cols,
+                                  uint64_t row_base, int store, int* store_out) {
+  return upload_impl<double>(ctx, d_row_major, n_rows, n_cols, row_base, store, store_out, true);
+}
+
+int ebic_matrix_upload_device_f32(ebic_ctx* ctx, const float* d_row_major, uint64_t n_rows, uint64_t n_cols,
+                                  uint64_t row_base) {
+  return upload_impl<float>(ctx, d_row_major, n_rows, n_cols, row_base, EBIC_STORE_F32, nullptr, true);
 }
 
 int ebic_matrix_info(ebic_ctx* ctx, uint64_t* n_rows, uint64_t* n_cols, uint64_t* ld, int* store,

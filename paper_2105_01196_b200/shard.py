@@ -9,10 +9,15 @@ for any world size:
            partial uint32 counts are summed with one all_reduce(SUM) (the path's
            only real exchange).  Row lists (supporting_rows) are the per-shard
            ascending lists concatenated in rank order.
-  pop   -- every rank holds the whole matrix (replicated: uploaded per rank, or
-           broadcast from rank 0 with NCCL); rank g evaluates its contiguous
-           slice of the population; no reduction, counts are all-gathered only
-           when every rank needs them.
+  pop   -- every rank holds the whole matrix (replicated); rank g evaluates
+           its contiguous slice of the population; no reduction, counts are
+           all-gathered only when every rank needs them.
+
+Matrix source: every rank passes the host matrix (`source="local"`), or only
+rank 0 does (`source="broadcast"`): the row-major matrix is then broadcast from
+rank 0 -- over NVLink into each GPU's memory with NCCL, where each rank builds
+its store straight from the device buffer (ebic_matrix_upload_device_*), or as
+a CPU tensor with gloo.
 
 The evaluator itself is injected (`local`), so the sharding / exchange logic is
 the same object in production (the CUDA `Evaluator`) and in the CPU gloo tests.
@@ -66,17 +71,58 @@ class ShardedEvaluator:
     `dist` is torch.distributed (already initialised) or None for world 1.
     """
 
-    def __init__(self, local, matrix: np.ndarray, mode: str = "rows", dist=None, group=None):
+    def __init__(self, local, matrix: np.ndarray | None, mode: str = "rows", dist=None, group=None,
+                 source: str = "local"):
         if mode not in ("rows", "pop"):
             raise ValueError("mode must be 'rows' or 'pop'")
+        if source not in ("local", "broadcast"):
+            raise ValueError("source must be 'local' or 'broadcast'")
         self.local = local
         self.dist = dist
         self.group = group
         world = dist.get_world_size(group) if dist is not None else 1
         rank = dist.get_rank(group) if dist is not None else 0
+        if source == "broadcast" and world > 1:
+            self._upload_broadcast(matrix, mode, rank, world)
+            return
+        if matrix is None:
+            raise ValueError("matrix is required with source='local'")
         self.spec = ShardSpec(mode, rank, world, int(matrix.shape[0]), int(matrix.shape[1]))
         b, e = self.spec.rows
         local.upload(np.ascontiguousarray(matrix[b:e]), row_base=b)
+
+    def _upload_broadcast(self, matrix, mode, rank, world):
+        """Rank 0's matrix to every rank (shape and dtype first), then each rank
+        uploads its row block of the broadcast buffer."""
+        import torch
+
+        dist, group = self.dist, self.group
+        dev = _collective_device(dist, group)
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        meta = torch.zeros(3, dtype=torch.int64)
+        if rank == 0:
+            if matrix is None:
+                raise ValueError("rank 0 needs the matrix with source='broadcast'")
+            m = np.asarray(matrix)
+            meta = torch.tensor([m.shape[0], m.shape[1], int(m.dtype != np.float32)], dtype=torch.int64)
+        meta = meta.to(dev)
+        dist.broadcast(meta, src=src, group=group)
+        n_rows, n_cols, f64 = (int(x) for x in meta.tolist())
+        dtype = torch.float64 if f64 else torch.float32
+        if rank == 0:
+            buf = torch.from_numpy(np.ascontiguousarray(matrix, dtype=np.float64 if f64 else np.float32)).to(dev)
+        else:
+            buf = torch.empty((n_rows, n_cols), dtype=dtype, device=dev)
+        dist.broadcast(buf, src=src, group=group)
+        self.spec = ShardSpec(mode, rank, world, n_rows, n_cols)
+        b, e = self.spec.rows
+        block = buf[b:e]  # contiguous rows of a row-major buffer
+        if block.is_cuda and hasattr(self.local, "upload_device"):
+            torch.cuda.current_stream().synchronize()  # the broadcast has landed before the context's stream reads it
+            self.local.upload_device(block.data_ptr(), e - b, n_cols, dtype="f64" if f64 else "f32", row_base=b)
+        else:
+            self.local.upload(block.cpu().numpy(), row_base=b)
+        del buf, block
 
     # -- collectives (torch tensors on CPU for gloo, on CUDA for nccl) -------
     def _all_reduce_sum(self, counts: np.ndarray) -> np.ndarray:

@@ -239,6 +239,22 @@ class Evaluator:
         self._set_shape(m.shape, row_base, out.value)
         return out.value
 
+    def upload_device(self, ptr: int, n_rows: int, n_cols: int, dtype: str = "f32", row_base: int = 0,
+                      store: int = EBIC_STORE_AUTO) -> int:
+        """Upload a row-major matrix already in this context's GPU memory (device
+        pointer `ptr`, e.g. a torch CUDA tensor an NCCL broadcast filled)."""
+        if dtype == "f32":
+            check(self._L.ebic_matrix_upload_device_f32(self._h, int(ptr), int(n_rows), int(n_cols), int(row_base)))
+            self._set_shape((n_rows, n_cols), row_base, EBIC_STORE_F32)
+            return EBIC_STORE_F32
+        if dtype != "f64":
+            raise ValueError("dtype must be 'f32' or 'f64'")
+        out = C.c_int(0)
+        check(self._L.ebic_matrix_upload_device_f64(self._h, int(ptr), int(n_rows), int(n_cols), int(row_base),
+                                                    int(store), C.byref(out)))
+        self._set_shape((n_rows, n_cols), row_base, out.value)
+        return out.value
+
     def _set_shape(self, shape, row_base, store):
         self.n_rows, self.n_cols = int(shape[0]), int(shape[1])
         self.row_base = int(row_base)

@@ -712,3 +712,45 @@ def test_support_overlaps_edges(evaluator):
     for a in range(3):
         for b in range(3):
             assert inter[k[a], k[b]] == np.intersect1d(rows[a], rows[b]).size
+
+
+def test_upload_from_device_memory(evaluator):
+    """ebic_matrix_upload_device_f32/_f64: a row-major matrix already in GPU
+    memory (what an NCCL broadcast fills) builds the same store as the host
+    upload -- f32, f64 that is f32-exact (f32 store), f64 that is not (f64
+    store), a row shard with row_base -- and the counts and rows match the
+    oracle; the source buffer is left unchanged; host pointers are refused."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    m32 = rng.standard_normal((3001, 60)).astype(np.float32)
+    m32[:800] = np.sort(m32[:800], axis=1)
+    pop = synth.random_population(3000, 60, seed=4)
+    tp = TrendParams(approx=0.03, negative_trends=True)
+    want = oracle.evaluate_population(m32.astype(np.float64), pop.cols, pop.offsets, 0.03, True)
+    try:
+        t = torch.from_numpy(m32).cuda()
+        torch.cuda.synchronize()  # (the caller makes sure the buffer has landed)
+        assert evaluator.upload_device(t.data_ptr(), 3001, 60, "f32") == EBIC_STORE_F32
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, tp), want)
+        assert torch.equal(t.cpu(), torch.from_numpy(m32))
+        t64 = torch.from_numpy(m32.astype(np.float64)).cuda()
+        torch.cuda.synchronize()
+        assert evaluator.upload_device(t64.data_ptr(), 3001, 60, "f64") == EBIC_STORE_F32
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, tp), want)
+        m64 = m32.astype(np.float64) + 1e-12
+        t64 = torch.from_numpy(m64).cuda()
+        torch.cuda.synchronize()
+        assert evaluator.upload_device(t64.data_ptr(), 3001, 60, "f64") == EBIC_STORE_F64
+        np.testing.assert_array_equal(evaluator.evaluate_population(pop, tp),
+                                      oracle.evaluate_population(m64, pop.cols, pop.offsets, 0.03, True))
+        # a row shard: rows [1000, 3001) with global row ids
+        sub = t[1000:]
+        evaluator.upload_device(sub.data_ptr(), 2001, 60, "f32", row_base=1000)
+        rows = evaluator.supporting_rows(pop.sequence(0), tp)
+        full = oracle.supporting_rows(m32.astype(np.float64), pop.sequence(0), 0.03, True)
+        np.testing.assert_array_equal(rows, full[full >= 1000])
+        with pytest.raises(EbicError):
+            evaluator.upload_device(m32.ctypes.data, 3001, 60, "f32")  # host memory
+    finally:
+        evaluator.upload(m32)

@@ -49,14 +49,15 @@ def _problem():
     return m, Population.from_sequences(seqs)
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, q, source="local"):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         m, pop = _problem()
-        sev = ShardedEvaluator(OracleLocal(), m, mode=mode, dist=dist)
+        given = m if (source == "local" or rank == 0) else None  # broadcast: only rank 0 has it
+        sev = ShardedEvaluator(OracleLocal(), given, mode=mode, dist=dist, source=source)
         out = {}
         for approx, neg in ((0.03, False), (0.0, True)):
             tp = TrendParams(approx=approx, negative_trends=neg)
@@ -67,8 +68,9 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("source", ["local", "broadcast"])
 @pytest.mark.parametrize("mode", ["rows", "pop"])
-def test_world2_gloo_matches_single_process(mode):
+def test_world2_gloo_matches_single_process(mode, source):
     import torch.multiprocessing as mp
 
     import oracle
@@ -76,7 +78,7 @@ def test_world2_gloo_matches_single_process(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q, source)) for r in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in procs]
