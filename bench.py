@@ -285,6 +285,21 @@ def bench_reference(args, cfg, rank):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def index_kernel_name(wp, n_cand):
+    """The index kernel launch_table picks (ebic_capi.cu) for this vector length
+    and candidate count, with the default EBIC_TABLE_KERNEL."""
+    import torch
+
+    if wp // 4 <= 256:
+        return "table_count_tma_kernel"
+    if not torch.cuda.is_available():
+        return "table_count_warp_multi_kernel / table_count_kernel"
+    n_sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    if wp // 4 <= 256:
+        return "table_count_tma_kernel"
+    return "table_count_warp_multi_kernel" if n_cand >= n_sms * 32 else "table_count_kernel"
+
+
 def bench_ours(args, cfg, rank, world, local_rank, dist):
     import torch
 
@@ -501,7 +516,7 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                    if (world > 1 and args.shard == "rows") else None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.config, world),
-                     "kernel": ("table_count_kernel (pair-trend index)" if index_used else
+                     "kernel": (index_kernel_name(wp, d_pops[0][2]) + " (pair-trend index)" if index_used else
                                 "slab_pair_kernel (packed rank pairs)" if Ccols <= 2048 else "slab_count_kernel (rank plane)")
                      if (args.path != "value" and Ccols <= 8192) else "fitness_count_kernel (value)", "kernel_avg_ms": kern_avg_s * 1e3,
                      "physical": ({"what": "pair-vector bytes streamed from HBM per launch (4 B x wp words x (L-1) pairs "
