@@ -187,6 +187,7 @@ struct ebic_ctx {
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
+  int table_build_a = 2;    // EBIC_TABLE_BUILD_A: a-columns per builder warp (1 or 2)
   int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (TMA warps up to 256 slices; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
@@ -372,9 +373,31 @@ int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
     }
   }
   const uint32_t wp = (uint32_t)table_wp(ctx);
-  const dim3 grid((wp + 31) / 32, (unsigned)((ctx->n_cols + ebic::kTableBuildWarps - 1) / ebic::kTableBuildWarps));
-  ebic::build_pair_table_kernel<<<grid, ebic::kTableBuildWarps * 32, 0, s>>>(
-      ctx->d_plane, ctx->ld, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp, ctx->d_table);
+  // (row block, a tile) CTAs, times z slices of the b columns chosen so the
+  // last wave is as full as possible (C3: 640 tiles = 2.2 waves of 2 CTAs per
+  // SM unsliced; 3 slices = 6.5 waves)
+  const uint64_t tiles = (uint64_t)((wp + 31) / 32) *
+                         ((ctx->n_cols + ebic::kTableBuildWarps - 1) / ebic::kTableBuildWarps);
+  const double slots = 2.0 * ctx->n_sms;  // resident builder CTAs (2 x 512 threads per SM)
+  uint32_t z = 1;
+  double best = 1e30;
+  for (uint32_t zz = 1; zz <= 8 && (zz == 1 || ctx->n_cols / zz >= 64); ++zz) {
+    const double waves = tiles * zz / slots;
+    const double waste = std::ceil(waves) / waves;
+    if (waste < best - 1e-9) {
+      best = waste;
+      z = zz;
+    }
+  }
+  const uint32_t b_per_z = (uint32_t)(((ctx->n_cols + z - 1) / z + 1) / 2 * 2);
+  z = (uint32_t)((ctx->n_cols + b_per_z - 1) / b_per_z);
+  const dim3 grid((wp + 31) / 32, (unsigned)((ctx->n_cols + ebic::kTableBuildWarps - 1) / ebic::kTableBuildWarps), z);
+  if (ctx->table_build_a == 2)
+    ebic::build_pair_table_kernel<2><<<grid, ebic::kTableBuildWarps / 2 * 32, 0, s>>>(
+        ctx->d_plane, ctx->ld, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp, ctx->d_table, b_per_z);
+  else
+    ebic::build_pair_table_kernel<1><<<grid, ebic::kTableBuildWarps * 32, 0, s>>>(
+        ctx->d_plane, ctx->ld, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp, ctx->d_table, b_per_z);
   ctx->launches++;
   EBIC_CUDA(cudaGetLastError());
   ctx->table_valid = true;
@@ -1044,6 +1067,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (tb) ctx->table_budget_user = (uint64_t)std::strtoull(tb, nullptr, 10) << 20;
     const char* hp = std::getenv("EBIC_HOST_PIECES");
     if (hp) ctx->pipeline_pieces = std::max(1, std::min(4, std::atoi(hp)));
+    const char* tba = std::getenv("EBIC_TABLE_BUILD_A");
+    if (tba) ctx->table_build_a = std::atoi(tba) == 1 ? 1 : 2;
     const char* ts = std::getenv("EBIC_TMA_SLOTS");
     if (ts) ctx->tma_slots = std::max(2, std::min(4, std::atoi(ts)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");

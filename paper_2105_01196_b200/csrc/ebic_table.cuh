@@ -69,55 +69,95 @@ __device__ __forceinline__ uint32_t index_to_natural(uint32_t w) {
 // instructions per output word (a ballot-based builder needs 5).  Shared
 // layout: pair j of word l at 16 l + (j ^ ((l >> 1) & 15)) -- conflict-free
 // for the 32 lanes reading pair j of their words at once.
-__global__ void __launch_bounds__(kTableBuildWarps * 32)
+//
+// A = a-columns per warp: with A = 2 a warp keeps the thresholds of columns
+// a and a + 16 (32 packed registers) and every shared-memory read of a column
+// b pair feeds two IADDs, so a CTA of 16 warps still covers 32 columns a.
+template <int A>
+__global__ void __launch_bounds__(kTableBuildWarps / A * 32, A)
 build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_t n_rows, uint32_t n_cols,
-                        uint32_t wp, uint32_t* __restrict__ table) {
-  __shared__ uint32_t s_rg[2][2][kTableRowsPerCta / 2];  // [iteration parity][column of the pair][swizzled pair]
+                        uint32_t wp, uint32_t* __restrict__ table, uint32_t b_per_z) {
+  // blockIdx.z: this CTA's slice [b_begin, b_end) of the columns b (even
+  // length; slices only balance the waves -- every (a, b) is built once)
+  const uint32_t b_begin = blockIdx.z * b_per_z, b_end = min(n_cols, b_begin + b_per_z);
+  constexpr int T = kTableBuildWarps / A * 32;                 // threads
+  constexpr int PAIRS = kTableRowsPerCta / 2;                  // row pairs of the block
+  __shared__ uint32_t s_rg[2][2][PAIRS];  // [iteration parity][column of the pair][swizzled pair]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r0 = blockIdx.x * kTableRowsPerCta;
-  const uint32_t a = blockIdx.y * kTableBuildWarps + warp;
-  const bool a_ok = a < n_cols;
   const uint32_t w0 = r0 / 32;  // first word of this row block
-  // this lane's 32 rows of column a -> 16 negated threshold pairs
-  uint32_t nt[16];
-  {
+  uint32_t ac[A];
+  bool a_ok[A];
+  // this lane's 32 rows of each column a -> 16 negated threshold pairs
+  uint32_t nt[A][16];
+#pragma unroll
+  for (int q = 0; q < A; ++q) {
+    ac[q] = blockIdx.y * kTableBuildWarps + warp + q * (kTableBuildWarps / A);
+    a_ok[q] = ac[q] < n_cols;
     const uint32_t rl = r0 + 32 * lane;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint32_t re = rl + 2 * j;
-      const uint32_t te = (a_ok && re < n_rows) ? (__ldg(plane + (uint64_t)a * ld + re) & 0xFFFFu) : 0u;
-      const uint32_t to = (a_ok && re + 1 < n_rows) ? (__ldg(plane + (uint64_t)a * ld + re + 1) & 0xFFFFu) : 0u;
-      nt[j] = 0u - (te | (to << 16)) - 0x00010001u;
+      const uint32_t te = (a_ok[q] && re < n_rows) ? (__ldg(plane + (uint64_t)ac[q] * ld + re) & 0xFFFFu) : 0u;
+      const uint32_t to = (a_ok[q] && re + 1 < n_rows) ? (__ldg(plane + (uint64_t)ac[q] * ld + re + 1) & 0xFFFFu) : 0u;
+      nt[q][j] = 0u - (te | (to << 16)) - 0x00010001u;
     }
   }
-  const uint32_t valid = a_ok ? index_valid_bits(n_rows, w0 + lane) : 0u;
-  // staging: thread t < 512 packs row pair t of column b, t >= 512 of column b + 1
-  const uint32_t tp = threadIdx.x & 511, th = threadIdx.x >> 9;
-  const uint32_t re = r0 + 2 * tp;
-  const uint32_t sidx = 16 * (tp >> 4) + ((tp & 15) ^ ((tp >> 5) & 15));  // pair j = tp & 15 of word l = tp >> 4
-  auto fetch = [&](uint32_t b) -> uint32_t {
-    if (b >= n_cols) return 0u;
-    const uint32_t we = re < n_rows ? __ldg(plane + (uint64_t)b * ld + re) : 0u;
-    const uint32_t wo = re + 1 < n_rows ? __ldg(plane + (uint64_t)b * ld + re + 1) : 0u;
-    return ((we >> 16) | 0x8000u) | (((wo >> 16) | 0x8000u) << 16);  // guarded ranks Rg of the pair
+  const uint32_t valid = index_valid_bits(n_rows, w0 + lane);
+  // staging: each thread packs PAIRS / T row pairs of columns b and b + 1
+  constexpr int PER = 2 * PAIRS / T;  // values staged per thread per iteration (2 with A = 1, 4 with A = 2)
+  uint32_t nxt[PER];
+  auto fetch = [&](uint32_t b) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t idx = threadIdx.x + k * T;  // 0 .. 2 PAIRS - 1
+      const uint32_t col = b + idx / PAIRS, tp = idx % PAIRS;
+      const uint32_t re = r0 + 2 * tp;
+      uint32_t v = 0u;
+      if (col < n_cols) {
+        const uint32_t we = re < n_rows ? __ldg(plane + (uint64_t)col * ld + re) : 0u;
+        const uint32_t wo = re + 1 < n_rows ? __ldg(plane + (uint64_t)col * ld + re + 1) : 0u;
+        v = ((we >> 16) | 0x8000u) | (((wo >> 16) | 0x8000u) << 16);  // guarded ranks Rg of the pair
+      }
+      nxt[k] = v;
+    }
   };
-  uint32_t nxt = fetch(th);
+  auto stage = [&](int par) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t idx = threadIdx.x + k * T;
+      const uint32_t tp = idx % PAIRS;
+      const uint32_t sidx = 16 * (tp >> 4) + ((tp & 15) ^ ((tp >> 5) & 15));  // pair j = tp & 15 of word tp >> 4
+      s_rg[par][idx / PAIRS][sidx] = nxt[k];
+    }
+  };
+  fetch(b_begin);
   const uint32_t sw = (uint32_t)(lane >> 1) & 15u;
   int par = 0;
-  for (uint32_t b = 0; b < n_cols; b += 2, par ^= 1) {
+  for (uint32_t b = b_begin; b < b_end; b += 2, par ^= 1) {
     // one barrier per two columns: the buffers alternate between iterations,
     // so writing this pair never races the previous pair's readers
-    s_rg[par][th][sidx] = nxt;
+    stage(par);
     __syncthreads();
-    nxt = fetch(b + 2 + th);
+    fetch(b + 2);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if (b + h < n_cols) {
+      if (b + h < b_end) {
         const uint32_t* rg = s_rg[par][h] + 16 * lane;
-        uint32_t word = 0;
+        uint32_t word[A];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) word |= ((rg[j ^ sw] + nt[j]) & 0x80008000u) >> (15 - j);
-        if (a_ok && w0 + lane < wp) table[((uint64_t)a * n_cols + b + h) * wp + w0 + lane] = word & valid;
+        for (int q = 0; q < A; ++q) word[q] = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t x = rg[j ^ sw];
+#pragma unroll
+          for (int q = 0; q < A; ++q) word[q] |= ((x + nt[q][j]) & 0x80008000u) >> (15 - j);
+        }
+        if (w0 + lane < wp) {
+#pragma unroll
+          for (int q = 0; q < A; ++q)
+            if (a_ok[q]) table[((uint64_t)ac[q] * n_cols + b + h) * wp + w0 + lane] = word[q] & valid;
+        }
       }
     }
   }
