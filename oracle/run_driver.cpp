@@ -28,6 +28,7 @@ using namespace bicseek;
 // paper_2105_01196_b200/csrc/bicseek_run_device.cpp: the device-aware driver
 namespace bicseek_device {
 RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device);
+void warm(int device);
 }
 #endif
 
@@ -126,6 +127,9 @@ int main(int argc, char** argv) {
     // (CUDA context creation for the device build) out of run()'s own timer
     const ExpressionMatrix w({1.0, 2.0, 2.0, 1.0}, 2, 2, default_labels('r', 2), default_labels('c', 2));
     (void)evaluate_population(w, {Chromosome({0, 1})}, p.trend, nullptr);
+#ifdef EBIC_DEVICE_RUN
+    if (engine != "reference") bicseek_device::warm(0);  // the driver's own (per-thread) context
+#endif
   }
   RunResult r;
   if (engine == "reference") {

@@ -35,6 +35,7 @@
 #include <tuple>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -96,6 +97,28 @@ std::vector<std::size_t> tally_columns(const std::vector<RankedIndividual>& pop,
 }
 
 // One device context per run: the matrix, the plane and the marshaller ring.
+// Contexts are kept per thread and device across runs (stream, pinned staging
+// slots and scratch survive; the matrix does not): creating one costs
+// milliseconds to, on some boxes, a large fraction of a second.
+struct ThreadContexts {
+  std::vector<std::pair<int, ebic_ctx*>> ctx;
+  ebic_ctx* get(int device) {
+    for (auto& c : ctx)
+      if (c.first == device) return c.second;
+    ebic_ctx* x = nullptr;
+    check(ebic_ctx_create(device, &x), "context");
+    ctx.emplace_back(device, x);
+    return x;
+  }
+  ~ThreadContexts() {
+    for (auto& c : ctx) ebic_ctx_destroy(c.second);
+  }
+};
+ebic_ctx* thread_context(int device) {
+  thread_local ThreadContexts pool;
+  return pool.get(device);
+}
+
 struct Device {
   ebic_ctx* ctx = nullptr;
   double approx = 0.0;
@@ -103,7 +126,7 @@ struct Device {
   uint64_t launches0 = 0;
 
   Device(const ExpressionMatrix& m, const TrendParams& tp, int device) {
-    check(ebic_ctx_create(device, &ctx), "context");
+    ctx = thread_context(device);
     check(ebic_matrix_upload_f64(ctx, m.values().data(), m.rows(), m.cols(), 0, EBIC_STORE_AUTO, nullptr),
           "matrix upload");
     approx = tp.approx;
@@ -111,7 +134,9 @@ struct Device {
     check(ebic_matrix_prepare(ctx, approx), "rank plane");
   }
   ~Device() {
-    if (ctx) ebic_ctx_destroy(ctx);
+    // the context, and the matrix with its index, stay for this thread's next
+    // run (whose upload replaces the matrix and reuses the index allocation)
+    if (ctx) ebic_ctx_sync(ctx);
   }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;
@@ -417,13 +442,25 @@ Chromosome breed_child(State& st, const EvolutionParams& p, std::size_t num_cols
 
 }  // namespace
 
+// Create this thread's context for `device` ahead of the first run (a
+// harness can keep the start-up out of run()'s timer, as it does for the
+// drop-in TU with one tiny evaluation).
+void warm(int device = 0) { (void)thread_context(device); }
+
 // evolution.cpp:305-333 with the device evaluator on the caller side.
 RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 0) {
   p.validate();
   if (m.rows() == 0 || m.cols() < 2) throw std::invalid_argument("run: matrix too small");
   const auto t0 = std::chrono::steady_clock::now();
 
+  // EBIC_DRIVER_TRACE=1: phase times on stderr (setup, per-generation breed+eval / archive)
+  const char* trace_env = std::getenv("EBIC_DRIVER_TRACE");
+  const bool trace = trace_env && std::atoi(trace_env);
+  auto since = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   Device dev(m, p.trend, device);
+  if (trace) std::fprintf(stderr, "[driver] device setup %.2f ms\n", since(t0));
   const std::size_t chunk = std::max<std::size_t>(256, p.population_size / 4);
   const char* lists_env = std::getenv("EBIC_ARCHIVE_ROWS");
   const bool lists = (lists_env && std::atoi(lists_env)) || p.top_rank_capacity() + 64 > EBIC_OVERLAP_MAX;
@@ -442,6 +479,7 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
     st.column_usage = tally_columns(st.population, m.cols());
   }
 
+  if (trace) std::fprintf(stderr, "[driver] init_state done at %.2f ms\n", since(t0));
   std::string reason = "budget";
   while (st.generation < p.max_iterations) {
     if (st.tabu.hit_count >= p.effective_tabu_threshold()) {
@@ -449,6 +487,7 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
       break;
     }
     // step_generation (evolution.cpp:248-303)
+    const auto t_gen = std::chrono::steady_clock::now();
     const std::size_t num_cols = m.cols();
     std::vector<RankedIndividual> next;
     next.reserve(p.population_size);
@@ -464,7 +503,11 @@ RunResult run(const ExpressionMatrix& m, const EvolutionParams& p, int device = 
       ev.add(offspring);  // overlap: the GPU counts this chunk while the next is bred
     }
     const std::vector<std::size_t> counts = ev.finish(offspring);
+    const auto t_ins = std::chrono::steady_clock::now();
     const bool improved = rank_and_insert(std::move(offspring), counts, st, p, rows, next);
+    if (trace)
+      std::fprintf(stderr, "[driver] gen %zu: breed+eval %.2f ms, archive %.2f ms\n", st.generation,
+                   std::chrono::duration<double, std::milli>(t_ins - t_gen).count(), since(t_ins));
     if (improved) st.tabu.hit_count = 0;
     st.population = std::move(next);
     st.column_usage = tally_columns(st.population, num_cols);

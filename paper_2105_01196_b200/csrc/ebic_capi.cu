@@ -187,6 +187,7 @@ struct ebic_ctx {
   size_t smem_optin = 227 * 1024;
   int prefetch = -1;  // -1 auto, 0 off, 1 on (EBIC_PREFETCH)
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
+  uint64_t table_cap = 0;   // bytes allocated at d_table (kept across uploads for reuse)
   int table_build_a = 2;    // EBIC_TABLE_BUILD_A: a-columns per builder warp (1 or 2)
   int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (TMA warps up to 256 slices; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA (A/B)
@@ -364,6 +365,11 @@ int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
   if (ctx->table_valid && std::memcmp(&ctx->table_approx, &approx, sizeof(double)) == 0) return EBIC_OK;
   EBIC_TRY(ensure_plane(ctx, approx, s));
   ctx->table_valid = false;
+  if (ctx->d_table && ctx->table_cap < table_bytes(ctx)) {  // a kept allocation too small for this matrix
+    cudaFree(ctx->d_table);
+    ctx->d_table = nullptr;
+    ctx->table_cap = 0;
+  }
   if (!ctx->d_table) {
     if (cudaMalloc(&ctx->d_table, table_bytes(ctx)) != cudaSuccess) {
       cudaGetLastError();
@@ -371,6 +377,7 @@ int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
       ctx->table_failed = true;
       return kTableNoMemory;
     }
+    ctx->table_cap = table_bytes(ctx);
   }
   const uint32_t wp = (uint32_t)table_wp(ctx);
   // (row block, a tile) CTAs, times z slices of the b columns chosen so the
@@ -876,6 +883,29 @@ int need_matrix(const ebic_ctx* ctx) {
   return EBIC_OK;
 }
 
+// Drop the resident matrix and what derives from it.  `keep_index_alloc`
+// (a new upload follows): the pair-trend index allocation is kept for reuse --
+// allocating gigabytes costs tens to hundreds of milliseconds per upload.
+void drop_matrix(ebic_ctx* ctx, bool keep_index_alloc) {
+  if (ctx->d_mat) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_mat);
+  }
+  if (ctx->d_plane) cudaFree(ctx->d_plane);
+  ctx->d_plane = nullptr;
+  ctx->plane_valid = false;
+  if (ctx->d_table && !keep_index_alloc) {
+    cudaFree(ctx->d_table);
+    ctx->d_table = nullptr;
+    ctx->table_cap = 0;
+  }
+  ctx->table_valid = ctx->table_failed = false;
+  ctx->d_mat = nullptr;
+  ctx->store = 0;
+  ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
+}
+
 // `src` is host memory, or (src_on_device) a buffer on this context's GPU that
 // is read in place (checked and transposed from it; the caller keeps it).
 template <typename TI>
@@ -889,7 +919,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   if (store < EBIC_STORE_AUTO || store > EBIC_STORE_F64)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "bad store mode %d", store);
   EBIC_TRY(set_device(ctx));
-  ebic_matrix_free(ctx);
+  drop_matrix(ctx, /*keep_index_alloc=*/true);
   cudaStream_t s = ctx->stream;
   const uint64_t n = n_rows * n_cols;
 
@@ -975,7 +1005,15 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
       cudaGetLastError();
       fr = 0;
     }
-    ctx->table_budget = std::min<uint64_t>(ctx->table_budget_user, index_headroom(fr));
+    ctx->table_budget = std::min<uint64_t>(ctx->table_budget_user, index_headroom(fr + ctx->table_cap));
+    // a kept index allocation: reused if this matrix's index fits it and
+    // is allowed, otherwise (or if it is more than twice the need) released
+    if (ctx->d_table && (!table_allowed(ctx) || ctx->table_cap < table_bytes(ctx) ||
+                         ctx->table_cap > 2 * table_bytes(ctx))) {
+      cudaFree(ctx->d_table);
+      ctx->d_table = nullptr;
+      ctx->table_cap = 0;
+    }
   }
   if (store_out) *store_out = chosen;
   return EBIC_OK;
@@ -1173,20 +1211,7 @@ int ebic_matrix_info(ebic_ctx* ctx, uint64_t* n_rows, uint64_t* n_cols, uint64_t
 
 int ebic_matrix_free(ebic_ctx* ctx) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
-  if (ctx->d_mat) {
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    cudaFree(ctx->d_mat);
-  }
-  if (ctx->d_plane) cudaFree(ctx->d_plane);
-  ctx->d_plane = nullptr;
-  ctx->plane_valid = false;
-  if (ctx->d_table) cudaFree(ctx->d_table);
-  ctx->d_table = nullptr;
-  ctx->table_valid = ctx->table_failed = false;
-  ctx->d_mat = nullptr;
-  ctx->store = 0;
-  ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
+  drop_matrix(ctx, false);
   return EBIC_OK;
 }
 
