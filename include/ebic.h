@@ -85,7 +85,10 @@ int ebic_ctx_sync(ebic_ctx* ctx);
  * shard [row_base, row_base + n_rows) of a larger one).  Transposes on device
  * to column-major with rows padded to a multiple of 32.  Non-finite values
  * are rejected (matrix.cpp:41-42).  *store_out (optional) receives the chosen
- * EBIC_STORE_F32 / EBIC_STORE_F64.  Replaces any previous matrix. */
+ * EBIC_STORE_F32 / EBIC_STORE_F64.  Replaces any previous matrix; the previous
+ * pair-trend index ALLOCATION is kept and reused when the new index fits it
+ * (at most twice the need), else released -- ebic_matrix_free releases
+ * everything. */
 int ebic_matrix_upload_f64(ebic_ctx* ctx, const double* row_major, uint64_t n_rows,
                            uint64_t n_cols, uint64_t row_base, int store, int* store_out);
 /* Same for row-major float32 input (always exact; stored as float32). */
