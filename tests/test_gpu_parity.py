@@ -754,3 +754,20 @@ def test_upload_from_device_memory(evaluator):
             evaluator.upload_device(m32.ctypes.data, 3001, 60, "f32")  # host memory
     finally:
         evaluator.upload(m32)
+
+
+def test_index_allocation_kept_across_uploads(evaluator):
+    """A new upload reuses the previous pair-trend index allocation when the
+    new index fits it (same shape; smaller but at least half) and reallocates
+    otherwise (larger; much smaller); the index is rebuilt for every matrix
+    and the counts follow the current matrix."""
+    rng = np.random.default_rng(21)
+    for R, C in ((5000, 120), (5000, 120), (4000, 110), (9000, 150), (600, 30), (5000, 120)):
+        m = rng.standard_normal((R, C)).astype(np.float32)
+        m[: R // 4] = np.sort(m[: R // 4], axis=1)
+        pop = synth.random_population(1500, C, seed=R + C)
+        evaluator.upload(m)
+        for approx, neg in ((0.03, False), (0.0, True)):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
+        assert evaluator.index_info()[1]
