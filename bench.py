@@ -2,7 +2,8 @@
 """Benchmark: batched bicluster-fitness evaluation on B200 (EBIC hot path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c3|c2|c4|c5] [--shard rows|pop]
+                    [--config c3|c2|c4|c5|spec] [--shard rows|pop|replica]
+                    [--l2 auto|stream|flush]
 
 A STEP is one pass of the hot path over one batch: evaluate_population of P
 candidates against all R rows (trend.cpp:56-72), i.e. P fitness evals and P*R
@@ -12,33 +13,48 @@ reported alongside), % of the HBM roofline.
 Default workload = BASELINE configs[2] ("c3"): 20k x 1000 planted-trend float32
 matrix, P = 16384 (L uniform in [3,5]), approx 0.03.  BASELINE's metric and both
 of its numeric targets (>= 60% HBM roofline at 20k x 1000; >= 6x at 8 GPUs
-row-sharded) are quoted on this configuration; configs[1] is the bit-exact
-parity case (tests/test_gpu_parity.py::test_config2_bit_exact).
+row-sharded) are quoted on this configuration.
 
-N > 1 (torchrun, one process per GPU), --shard:
-  replica (default) -- candidates are independent, so the units are partitioned
-           with no data-path collective: every rank evaluates its own P-candidate
-           population against the replicated matrix (weak scaling; value = the
-           whole job's N*P evals per step / the slowest rank's step time).
-  rows     -- matrix rows sharded; every rank evaluates the whole population on
-           its shard and the partial counts are summed with one NCCL all_reduce
-           per step (strong scaling; for matrices too large to replicate).
+--gpus N > 1 without WORLD_SIZE in the environment re-launches this script
+under torch.distributed.run with N ranks (one per GPU; it fails unless N GPUs
+are visible, or --share-gpu lets the ranks share GPUs for testing).  Under
+torchrun WORLD_SIZE must equal N.  N > 1, --shard:
+  rows (default) -- BASELINE config 3: the matrix rows are sharded, every rank
+           evaluates the whole population on its shard and the partial counts
+           are summed over NVLink peer memory (ebic_xchg.cuh; --exchange nccl:
+           an NCCL all_reduce).  Steps are pipelined: step k's exchange runs on
+           the exchange stream while step k+1's count kernel runs.  Strong
+           scaling: the whole job evaluates P candidates per step.
   pop      -- one population split across ranks, counts all-gathered (strong).
+  replica  -- every rank evaluates its own P-candidate population against the
+           replicated matrix, no collective (weak scaling; secondary mode).
 
-value    : device-resident inputs (population CSR already in HBM), per-step CUDA
-           events on the launching stream around kernel + all_reduce; L2 is
-           flushed (512 MiB read, untimed) before every timed step.
-e2e      : the same metric through the public host API (ebic_eval_counts via
-           Evaluator.evaluate_population / ShardedEvaluator): host CSR copied to
-           pinned staging and H2D, counts D2H, every step inside the timed region.
-roofline : algorithmic bytes 4*L*R per eval / average fitness-kernel
-           time (CUDA events), vs the measured HBM copy bandwidth.
+Timing (--l2): `stream` (default when the per-rank index is larger than twice
+the 126 MB L2) -- K steps issued back to back, populations cycled from a pool
+whose pair vectors cover more than twice the L2, so no step finds its inputs
+in L2 and nothing is flushed; `flush` -- a 512 MiB device read before every
+step (outside the step's events).  Both are CUDA events on the launching
+stream, max over ranks.
+
+value    : device-resident populations, whole job's evals / step time.
+e2e      : the same metric through the public host API (ebic_eval_counts,
+           or ShardedEvaluator for N > 1): host arrays in, counts out, every
+           step's H2D / D2H inside the timed region.
+roofline : the count kernel's PHYSICAL HBM bytes (pair vectors it must stream:
+           4 B x wp words x (L-1) pairs per candidate, x2 with negatives) over
+           its measured time (sum bytes / sum time), vs the measured HBM peak.
+           SURVEY 8(d)'s 4*L*R algorithmic bytes are reported separately as
+           `effective_algorithmic` (the index kernel never reads the matrix).
+amortized: the one-time upload + rank plane + index build spread over the
+           timed steps and over a declared GA run.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -52,6 +68,8 @@ REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 METRIC = "candidate fitness evals/s & row-checks/s at 1/2/4/8 B200; % of HBM roofline"
+L2_BYTES = 126 * 1024 * 1024
+GA_GENERATIONS = 200  # the declared GA run of the amortized fields: BASELINE config 1's iteration count
 
 CONFIGS = {
     # name: rows, cols, population, len range, approx, negative, planted (rows, cols)
@@ -65,6 +83,12 @@ CONFIGS = {
     "c5": dict(rows=1_000_000, cols=64, pop=1024, len_min=16, len_max=16, approx=0.03, negative=False,
                bic=(10_000, 16),
                label="c5 microbench point: 1M x 64 f32, P=1024, L=16, approx 0.03"),
+    # SPEC.md:593's performance shape at the reference's own GA batch size
+    # (P=400, evolution.hpp:21; 392 offspring per generation, evolution.cpp:291)
+    "spec": dict(rows=20_000, cols=250, pop=392, len_min=3, len_max=5, approx=0.03, negative=False,
+                 bic=(500, 20),
+                 label="spec: 20k x 250 planted-trend f32 matrix, P=392 (one GA generation at the reference "
+                       "defaults), L in [3,5], approx 0.03"),
 }
 
 
@@ -268,10 +292,13 @@ def bench_reference(args, cfg, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "row_checks_per_s": value * cfg["rows"],
+        "higher_is_better": True, "scaling": "weak" if args.shard == "replica" else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (planted-trend f32 matrix, random populations; no dataset)",
+        "row_checks_per_s": value * cfg["rows"],
         "config": {"workload": cfg["label"], "rows": cfg["rows"], "cols": cfg["cols"], "population": cfg["pop"],
-                   "parallelism": "cpu"},
+                   "parallelism": f"cpu: the reference's WorkerPool on {cores} host threads (rank 0 only)",
+                   "shard": args.shard},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": kind,
                          "sample": f"{n_step} of {cfg['pop']} candidates x all {cfg['rows']} rows per step "
                                    f"(reference evaluate_population on WorkerPool({cores}))" if kind == "reference"
@@ -285,285 +312,386 @@ def bench_reference(args, cfg, rank):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def index_kernel_name(wp, n_cand):
+def index_kernel_name(wp, n_cand, n_sms=148):
     """The index kernel launch_table picks (ebic_capi.cu) for this vector length
     and candidate count, with the default EBIC_TABLE_KERNEL."""
-    import torch
-
-    if wp // 4 <= 256:
-        return "table_count_tma_kernel"
-    if not torch.cuda.is_available():
-        return "table_count_warp_multi_kernel / table_count_kernel"
-    n_sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     if wp // 4 <= 256:
         return "table_count_tma_kernel"
     return "table_count_warp_multi_kernel" if n_cand >= n_sms * 32 else "table_count_kernel"
 
 
+def table_wp(rows: int) -> int:
+    """Words per pair vector (ebic_capi.cu table_wp)."""
+    words = (rows + 31) // 32
+    return (words + 127) // 128 * 128 if words > 128 else (words + 3) // 4 * 4
+
+
+def pool_size(cfg, rows_rank: int, want_bytes: float) -> int:
+    """Populations to cycle so the distinct pair vectors they touch cover
+    `want_bytes` (expected over random draws of the C^2 ordered pairs)."""
+    c2 = cfg["cols"] ** 2
+    pairs = cfg["pop"] * ((cfg["len_min"] + cfg["len_max"]) / 2 - 1)
+    vec = 4 * table_wp(rows_rank)
+    for n in range(4, 65):
+        if c2 * vec * (1 - math.exp(-n * pairs / c2)) >= want_bytes:
+            return n
+    return 64
+
+
+class Collective:
+    """Barrier / max / sum over ranks on whatever device the backend needs."""
+
+    def __init__(self, dist, dev):
+        self.dist = dist
+        self.dev = dev if (dist is not None and dist.get_backend() == "nccl") else "cpu"
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_reduce_sum_(self, t):
+        if self.dist is None:
+            return t
+        if self.dev == "cpu":
+            c = t.cpu()
+            self.dist.all_reduce(c, op=self.dist.ReduceOp.SUM)
+            t.copy_(c)
+        else:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return t
+
+
 def bench_ours(args, cfg, rank, world, local_rank, dist):
     import torch
 
-    from paper_2105_01196_b200 import Evaluator, TrendParams
-    from paper_2105_01196_b200.shard import ShardedEvaluator, row_range
+    from paper_2105_01196_b200 import Evaluator, Population, TrendParams
+    from paper_2105_01196_b200.shard import ShardedEvaluator, pop_range, row_range, slice_population
 
-    local_rank = local_rank % max(torch.cuda.device_count(), 1)  # gloo test mode: ranks may share a GPU
+    n_dev = max(torch.cuda.device_count(), 1)
+    local_rank = local_rank % n_dev  # --share-gpu: ranks may share a GPU
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    coll = Collective(dist, dev)
     tp = TrendParams(approx=cfg["approx"], negative_trends=cfg["negative"])
-    n_pops = 4
-    # replica mode: every rank evaluates its OWN populations (different seeds)
-    replica = args.shard == "replica" and world > 1
-    m, pops = make_inputs(cfg, n_pops, seed0=42 + (1000 * rank if replica else 0))
+    shard = args.shard
     R, Ccols, P = cfg["rows"], cfg["cols"], cfg["pop"]
-    b, e = row_range(R, rank, world) if args.shard == "rows" else (0, R)
+    b, e = row_range(R, rank, world) if shard == "rows" else (0, R)
+    replica = shard == "replica"
+    p2p = shard == "rows" and args.exchange == "p2p"
+    neg_factor = 2 if cfg["negative"] else 1
 
+    # ---- populations: a pool large enough that the stream mode never finds
+    # a step's pair vectors in L2 (see pool_size)
+    want = 2.0 * L2_BYTES
+    n_pops = args.pops or pool_size(cfg, e - b, want)
+    m, pops = make_inputs(cfg, n_pops, seed0=42 + (1000 * rank if replica else 0))
+    if shard == "pop":
+        pops_local = [slice_population(pp, *pop_range(P, rank, world)) for pp in pops]
+    else:
+        pops_local = pops
+
+    # ---- one-time: upload + (matrix, approx) index --------------------------
     ev = Evaluator(local_rank)
     ev.set_path({"auto": 0, "value": 1, "plane": 2, "table": 4}[args.path])
+    if args.index_budget_gb is not None:
+        ev.set_table_budget(int(args.index_budget_gb * (1 << 30)))
     t0 = time.perf_counter()
     ev.upload(np.ascontiguousarray(m[b:e]), row_base=b)
     upload_ms = (time.perf_counter() - t0) * 1e3
-    # per-(matrix, approx) index: the exact rank plane (built once per GA run; outside the steps)
     t0 = time.perf_counter()
     ev.prepare(cfg["approx"])
     prepare_ms = (time.perf_counter() - t0) * 1e3
-    # rows mode over peer memory: every rank's exchange window mapped into every
-    # rank (CUDA IPC handles exchanged once through the process group)
-    p2p = world > 1 and args.shard == "rows" and args.exchange == "p2p"
+    build = ev.build_info()
+    index_bytes, index_used = ev.index_info()
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ev.set_stream(stream.cuda_stream)
     if p2p:
         h = ev.xchg_create(world, rank, P)
         handles = [None] * world
         dist.all_gather_object(handles, h)
         ev.xchg_open(handles)
-    # a dedicated (non-default) stream: kernels, NCCL and the timing events all run on it
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    ev.set_stream(stream.cuda_stream)
 
-    # device-resident populations
-    d_pops = []
-    for pop in pops:
-        if args.shard == "pop":
-            from paper_2105_01196_b200.shard import pop_range, slice_population
+    d_pops = [(torch.from_numpy(pp.cols.view(np.int32)).to(dev), torch.from_numpy(pp.offsets.view(np.int32)).to(dev),
+               len(pp), int(pp.cols.size)) for pp in pops_local]
+    n_local = d_pops[0][2]
+    counts = torch.zeros(P, dtype=torch.int32, device=dev)
 
-            pb, pe = pop_range(len(pop), rank, world)
-            pop = slice_population(pop, pb, pe)
-        d_pops.append((torch.from_numpy(pop.cols.view(np.int32)).to(dev),
-                       torch.from_numpy(pop.offsets.view(np.int32)).to(dev), len(pop), int(pop.cols.size)))
-    counts_full = torch.zeros(P, dtype=torch.int32, device=dev)
-    # L2 flush by READING 512 MiB (4x the 126 MB L2): evicts every line and leaves
-    # the L2 clean, so the timed kernel does not pay for write-backs of a
-    # write-based flush's dirty lines
-    flush = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # L2 mode
+    wp = (index_bytes // (4 * Ccols ** 2)) if (index_used and index_bytes) else table_wp(e - b)
+    per_rank_index = index_bytes if index_used else 0
+    l2_mode = args.l2
+    if l2_mode == "auto":
+        l2_mode = "stream" if (index_used and per_rank_index > 2 * L2_BYTES) else "flush"
+    flush = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if l2_mode == "flush" else None
     flush_sink = torch.empty((), dtype=torch.float32, device=dev)
 
     def flush_l2():
-        if os.environ.get("EBIC_BENCH_NO_FLUSH"):  # experiments only (L2-warm inputs)
-            return
-        torch.sum(flush, dim=0, out=flush_sink)
+        if flush is not None:
+            torch.sum(flush, dim=0, out=flush_sink)
 
-    def step(i, ev_k0=None, ev_k1=None):
+    def step(i, pipelined=True):
         dc, do, n, _ = d_pops[i % n_pops]
-        out = counts_full[:n] if args.shard == "pop" else counts_full
-        if ev_k0 is not None:
-            ev_k0.record(stream)
-        if p2p:  # count kernel + the fused peer-memory sum (one call, two kernels)
-            ev.evaluate_population_rows_sum_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp,
-                                                   stream=stream.cuda_stream)
-        else:
-            ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp,
-                                          stream=stream.cuda_stream)
-        if ev_k1 is not None:
-            ev_k1.record(stream)
-        if world > 1 and not replica and not p2p:
-            if args.shard == "rows":
-                dist.all_reduce(counts_full, op=dist.ReduceOp.SUM)
+        if p2p:
+            if pipelined:
+                ev.evaluate_population_rows_sum_async(dc.data_ptr(), do.data_ptr(), n, counts.data_ptr(), tp,
+                                                      stream=stream.cuda_stream)
             else:
-                gathered = [torch.empty_like(counts_full[:n]) for _ in range(world)]
-                dist.all_gather(gathered, counts_full[:n])
+                ev.evaluate_population_rows_sum_device(dc.data_ptr(), do.data_ptr(), n, counts.data_ptr(), tp,
+                                                       stream=stream.cuda_stream)
+            return
+        out = counts[:n]
+        ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, out.data_ptr(), tp, stream=stream.cuda_stream)
+        if world > 1 and shard == "rows":  # --exchange nccl
+            coll.all_reduce_sum_(counts)
+        elif world > 1 and shard == "pop":
+            gathered = [torch.empty_like(out) for _ in range(world)]
+            dist.all_gather(gathered, out)
 
-    # warmup
+    def finish():
+        if p2p:
+            ev.xchg_fence(stream.cuda_stream)
+
+    # ---- warmup -------------------------------------------------------------
     for i in range(max(args.warmup, 3)):
         step(i)
+    finish()
     torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
+    ev.sync()
+    coll.barrier()
 
-    # a step that is exactly one kernel launch (one GPU, or independent
-    # replicas) is timed by its own two events only: two more event records
-    # inside it would add ~5 us of GPU time per step to what is measured
-    kernel_only = (world == 1 or replica) and not p2p
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # ---- timed region ---------------------------------------------------------
     launches0 = ev.launch_count()
     clocks = ClockSampler(local_rank)
-    if dist is not None:
-        dist.barrier()
     torch.cuda.synchronize()
+    coll.barrier()
     with clocks:
         w0 = time.perf_counter()
-        for i in range(args.steps):
-            flush_l2()  # L2 flush (untimed: outside the step events)
-            starts[i].record(stream)
-            if kernel_only:  # the step IS the one count launch: its events are the kernel's
+        if l2_mode == "stream":
+            t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t_start.record(stream)
+            for i in range(args.steps):
                 step(i)
-            else:
-                step(i, k0[i], k1[i])
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
+            finish()
+            t_end.record(stream)
+            torch.cuda.synchronize()
+            total_ms = t_start.elapsed_time(t_end)
+        else:
+            starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush_l2()  # outside the step events
+                starts[i].record(stream)
+                step(i, pipelined=False)
+                ends[i].record(stream)
+            torch.cuda.synchronize()
+            total_ms = sum(s.elapsed_time(t) for s, t in zip(starts, ends))
+        coll.barrier()
         wall = time.perf_counter() - w0
     launches = ev.launch_count() - launches0
-    step_ms = [s.elapsed_time(t) for s, t in zip(starts, ends)]
-    kern_ms = step_ms if kernel_only else [s.elapsed_time(t) for s, t in zip(k0, k1)]
-    total_ms = sum(step_ms)
-    if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    ev.sync()  # raises on any device-side error of the timed steps (bad column, exchange timeout / poison)
+    total_ms = coll.max(total_ms)
     ms_per_step = total_ms / args.steps
-    p_total = P * world if replica else P  # candidates evaluated per step by the whole job
+    p_total = P * world if replica else P
     value = p_total / (ms_per_step / 1e3)
 
-    # roofline of the fitness kernel on this rank
-    sum_len = [int(dp[3]) for dp in d_pops]
-    alg_bytes = [4.0 * (e - b) * sl for sl in sum_len]
-    # pair-trend index in use: the kernel streams (L - 1) pair vectors of wp
-    # words per candidate (x2 with negatives) -- its PHYSICAL HBM traffic
-    index_bytes, index_used = ev.index_info()
-    # words per pair vector as laid out in HBM (the index is C x C vectors)
-    wp = (index_bytes // (4 * cfg["cols"] ** 2) if index_used and index_bytes
-          else ((e - b + 31) // 32 + 3) // 4 * 4)
+    # ---- kernel pass: the count kernel alone, events around every launch ----
+    k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kout = torch.zeros(P, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        if l2_mode == "flush":
+            flush_l2()
+        dc, do, n, _ = d_pops[i % n_pops]
+        k0[i].record(stream)
+        ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, kout.data_ptr(), tp, stream=stream.cuda_stream)
+        k1[i].record(stream)
+    torch.cuda.synchronize()
+    kern_ms = [a.elapsed_time(z) for a, z in zip(k0, k1)]
+    per_rank = None
+    if p2p:
+        # unpipelined steps: count + exchange, serialised (exchange = the difference)
+        s0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        s1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        coll.barrier()
+        for i in range(args.steps):
+            s0[i].record(stream)
+            step(i, pipelined=False)
+            s1[i].record(stream)
+        torch.cuda.synchronize()
+        ser = statistics.mean(a.elapsed_time(z) for a, z in zip(s0, s1))
+        per_rank = {"rank": rank, "rows": [b, e], "kernel_us": 1e3 * statistics.mean(kern_ms),
+                    "step_unpipelined_us": 1e3 * ser, "exchange_us": 1e3 * max(0.0, ser - statistics.mean(kern_ms)),
+                    "step_pipelined_us": 1e3 * ms_per_step}
+    ev.sync()
+
+    # roofline of the count kernel on this rank
     n_pairs = [int(dp[3]) - int(dp[2]) for dp in d_pops]
-    phys_bytes = [4.0 * wp * npair * (2 if cfg["negative"] else 1) for npair in n_pairs]
-    per_step_bytes = [alg_bytes[i % n_pops] for i in range(args.steps)]
-    kern_avg_s = statistics.mean(kern_ms) / 1e3
-    achieved = statistics.mean(bb / (km / 1e3) for bb, km in zip(per_step_bytes, kern_ms)) / 1e9
+    phys = [4.0 * wp * npair * neg_factor for npair in n_pairs]
+    alg = [4.0 * (e - b) * int(dp[3]) for dp in d_pops]
+    kb = [phys[i % n_pops] for i in range(args.steps)]
+    ka = [alg[i % n_pops] for i in range(args.steps)]
+    ksum_s = sum(kern_ms) / 1e3
     peak, peak_src = measured_peak()
+    phys_gbs = sum(kb) / ksum_s / 1e9
+    alg_gbs = sum(ka) / ksum_s / 1e9
+    kernel = ((index_kernel_name(wp, n_local) + " (pair-trend index)") if index_used else
+              "slab_pair_kernel (packed rank pairs)" if Ccols <= 2048 else "slab_count_kernel (rank plane)") \
+        if (args.path != "value" and Ccols <= 8192) else "fitness_count_kernel (value)"
+    if not index_used:  # the slab / value kernels re-read the plane or the store from L2: no fixed physical bytes
+        phys_gbs = None
 
-    # ---- e2e through the public host API -----------------------------------
-    e2e_ms = []
+    # ---- e2e through the public host API -------------------------------------
+    ev.set_stream(None)
+    torch.cuda.set_stream(torch.cuda.default_stream(dev))
+    keep = []
+
+    def pinned(a):
+        t = torch.empty(a.size, dtype=torch.int32, pin_memory=True)
+        keep.append(t)
+        v = t.numpy().view(np.uint32)
+        v[:] = a
+        return v
+
+    def pinned_csr(pp):  # one page-locked block [offsets | cols]: the library DMAs it in one copy
+        buf = pinned(np.concatenate([pp.offsets, pp.cols]))
+        n1 = pp.offsets.size
+        return Population(buf[n1:], buf[:n1])
+
+    n_e2e = min(n_pops, 8)
     if world > 1 and not replica:
-        sev = ShardedEvaluator(ev, m, mode=args.shard, dist=dist)
+        # the context already holds this rank's shard and its exchange window
+        sev = ShardedEvaluator.attach(ev, R, Ccols, mode=shard, dist=dist,
+                                      exchange="p2p" if p2p else "collective", max_cand=P)
+        e2e_pops = pops[:n_e2e]
         call = sev.evaluate_population
+        api = f"ShardedEvaluator({shard}, exchange={sev.exchange}).evaluate_population"
     else:
-        # inputs and result in pinned host memory (the contract's e2e), DMA'd
-        # directly by ebic_eval_counts
-        from paper_2105_01196_b200 import Population
-
-        keep = []
-
-        def pinned(a):
-            t = torch.empty(a.size, dtype=torch.int32, pin_memory=True)
-            keep.append(t)
-            v = t.numpy().view(np.uint32)
-            v[:] = a
-            return v
-
-        def pinned_csr(pp):
-            # one page-locked block [offsets | cols]: the library DMAs it in one copy
-            buf = pinned(np.concatenate([pp.offsets, pp.cols]))
-            n1 = pp.offsets.size
-            return Population(buf[n1:], buf[:n1])
-
-        pops = [pinned_csr(pp) for pp in pops]
+        e2e_pops = [pinned_csr(pp) for pp in pops_local[:n_e2e]]
         out_pinned = pinned(np.zeros(P, dtype=np.uint32))
 
         def call(pop, params):
-            # the counts land in the page-locked out_pinned (the step's D2H); no extra copy
             return ev.evaluate_population(pop, params, out=out_pinned)
-    ev.set_stream(None)
+        api = "ebic_eval_counts (Evaluator.evaluate_population), pinned host arrays"
     for i in range(max(args.warmup, 8)):  # >= 2x the marshaller ring: every pinned slot allocated
-        call(pops[i % n_pops], tp)
+        call(e2e_pops[i % n_e2e], tp)
+    e2e_ms = []
     for i in range(args.steps):
-        flush_l2()
+        if l2_mode == "flush":
+            flush_l2()
         torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
+        coll.barrier()
         t0 = time.perf_counter()
-        host_counts = call(pops[i % n_pops], tp)
+        call(e2e_pops[i % n_e2e], tp)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_tot = sum(e2e_ms)
-    if dist is not None:
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_tot = float(t.item())
-    e2e_value = p_total / (e2e_tot / args.steps / 1e3)
-    pop0 = pops[0]
+    e2e_tot = coll.max(sum(e2e_ms))
+    e2e_step = e2e_tot / args.steps
+    e2e_value = p_total / (e2e_step / 1e3)
+    pop0 = e2e_pops[0]
     h2d = int(pop0.cols.nbytes + pop0.offsets.nbytes)
-    d2h = 4 * P
+    d2h = 4 * (P if not (shard == "pop") else n_local)
 
-    # parity spot-check of the device-resident result against the host-API result
-    ev.set_stream(stream.cuda_stream)
-    step(0)
-    torch.cuda.synchronize()
-    dev_counts = counts_full.cpu().numpy().view(np.uint32)
-    ev.set_stream(None)
-    host0 = np.array(call(pops[0], tp), copy=True)
-    parity_dev_vs_host = (bool(np.array_equal(dev_counts[:len(host0)], host0))
-                          if (world == 1 or args.shard == "rows" or replica) else None)
+    # ---- parity spot checks (no oracle here: two independent device paths) ---
+    host0 = np.array(call(e2e_pops[0], tp), copy=True)
+    dc, do, n, _ = d_pops[0]
+    ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, kout.data_ptr(), tp)
+    ev.sync()
+    local0 = kout[:n].clone()
+    if world > 1 and shard == "rows":
+        coll.all_reduce_sum_(local0)  # the partial counts summed by the process group, not the exchange windows
+    parity = bool(np.array_equal(local0.cpu().numpy().view(np.uint32)[:len(host0)], host0)) \
+        if shard != "pop" else None
 
+    # ---- one-time costs, amortized ---------------------------------------------
+    one_time_ms = coll.max(upload_ms + prepare_ms)
+    k = args.steps
+    amort = {
+        "one_time_ms": {"total": one_time_ms, "upload": upload_ms, "prepare": prepare_ms,
+                        "index_alloc": build["alloc_ms"], "plane": build["plane_ms"], "index": build["index_ms"],
+                        "note": "upload = H2D + finiteness/exactness check + transpose (host clock); prepare = "
+                                "index allocation (host clock) + rank plane + pair-trend index (CUDA events); "
+                                "max over ranks"},
+        "value_amortized": p_total * k / ((total_ms + one_time_ms) / 1e3),
+        "e2e_amortized": p_total * k / ((e2e_tot + one_time_ms) / 1e3),
+        "over_timed_steps": k,
+        "ga_run": {"generations": GA_GENERATIONS, "population": p_total,
+                   "value": p_total * GA_GENERATIONS / ((GA_GENERATIONS * ms_per_step + one_time_ms) / 1e3),
+                   "e2e": p_total * GA_GENERATIONS / ((GA_GENERATIONS * e2e_step + one_time_ms) / 1e3),
+                   "note": f"{GA_GENERATIONS} generations (BASELINE config 1's iteration count) of this "
+                           f"step's population, one upload + index build"},
+    }
+
+    parallelism = ("1 GPU" if world == 1 else
+                   f"rows-sharded x{world}: every rank holds R/{world} rows and evaluates the whole population; "
+                   + ("partial counts summed over NVLink peer memory (exchange windows, pipelined)" if p2p
+                      else "partial counts summed with an NCCL all_reduce") if shard == "rows" else
+                   f"population split x{world}, counts all-gathered" if shard == "pop" else
+                   f"replicas x{world}: every rank evaluates its own {P}-candidate population, no collective")
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak" if args.shard in ("replica", "pop") else "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "scaling": "weak" if replica else "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (planted-trend f32 matrix, random populations; no dataset)",
         "row_checks_per_s": value * R,
         "config": {"workload": cfg["label"], "rows": R, "cols": Ccols, "population": P,
-                   "population_per_step_total": p_total,
-                   "parallelism": ("1 GPU" if world == 1 else
-                                   f"population-sharded x{world}: every rank evaluates its own {P}-candidate "
-                                   f"population against the replicated matrix, no collective (weak)" if replica
-                                   else f"{args.shard}-sharded x{world}"),
-                   "l2": "flushed before every timed step (512 MiB device read, outside the step events)",
-                   "shard": args.shard, "path": args.path,
-                   "exchange": ("peer memory (fused sum kernel)" if p2p else "NCCL all_reduce")
-                   if (world > 1 and args.shard == "rows") else None},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                   "population_per_step_total": p_total, "parallelism": parallelism, "shard": shard,
+                   "path": args.path, "exchange": ("p2p" if p2p else "nccl") if shard == "rows" and world > 1 else None,
+                   "l2": ("stream: no flush; the per-rank pair-trend index (%.0f MB) exceeds 2x the 126 MB L2 and "
+                          "populations are cycled from a pool of %d whose pair vectors cover >= %.0f MB, "
+                          "steps issued back to back" % (per_rank_index / 1e6, n_pops, want / 1e6))
+                   if l2_mode == "stream" else
+                   "flushed before every timed step (512 MiB device read, outside the step events)",
+                   "populations_cycled": n_pops},
+        "roofline": {"bound": "hbm",
+                     "achieved": phys_gbs if phys_gbs is not None else alg_gbs,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": (phys_gbs if phys_gbs is not None else alg_gbs) / peak,
                      "traffic": ncu_traffic(args.config, world),
-                     "kernel": (index_kernel_name(wp, d_pops[0][2]) + " (pair-trend index)" if index_used else
-                                "slab_pair_kernel (packed rank pairs)" if Ccols <= 2048 else "slab_count_kernel (rank plane)")
-                     if (args.path != "value" and Ccols <= 8192) else "fitness_count_kernel (value)", "kernel_avg_ms": kern_avg_s * 1e3,
-                     "physical": ({"what": "pair-vector bytes streamed from HBM per launch (4 B x wp words x (L-1) pairs "
-                                          "per candidate) / kernel time, vs the same peak",
-                                  "bytes_per_launch": statistics.mean(phys_bytes),
-                                  "gbs": statistics.mean(pb / (km / 1e3) for pb, km in
-                                                         zip([phys_bytes[i % n_pops] for i in range(args.steps)],
-                                                             kern_ms)) / 1e9,
-                                  } if index_used else None),
-                     "algorithmic_bytes_per_launch": statistics.mean(alg_bytes),
+                     "kernel": kernel, "kernel_avg_ms": statistics.mean(kern_ms),
+                     "bytes_per_launch": statistics.mean(phys) if phys_gbs is not None else None,
+                     "bytes": ("physical: pair-vector bytes the kernel must stream from HBM, 4 B x %d words x "
+                               "(L-1) pairs per candidate%s; achieved = sum(bytes) / sum(kernel time) over the "
+                               "kernel pass (CUDA events around each launch on its stream)"
+                               % (wp, " x 2 (negatives)" if neg_factor == 2 else ""))
+                     if phys_gbs is not None else
+                     "algorithmic 4 B x L x R per eval (no index: the slab/value kernel re-reads the matrix "
+                     "from L2/shared memory, so this can exceed HBM)",
                      "peak_source": peak_src,
-                     "note": ("algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once, "
-                              "SURVEY 8(d)); the pair-trend index kernel never reads the matrix -- it streams "
-                              "(L-1) x R/8 index bytes per eval -- so achieved/frac exceed the HBM peak; "
-                              "roofline.physical is that kernel's real HBM traffic over the same time "
-                              "(and roofline.traffic the ncu DRAM bytes per launch)") if index_used else
-                             ("algorithmic bytes = 4 B x L x R per eval (each referenced f32 element once); "
-                              "the matrix is re-read from L2/shared memory by many candidates, so achieved can "
-                              "exceed the HBM peak")},
+                     "effective_algorithmic": {"bytes_per_launch": statistics.mean(alg), "gbs": alg_gbs,
+                                               "x_of_peak": alg_gbs / peak,
+                                               "what": "SURVEY 8(d) algorithmic bytes (4 B x L x R per eval, each "
+                                                       "referenced f32 element once) over the same kernel time: "
+                                                       "the bandwidth a matrix-reading kernel would need to match "
+                                                       "this one; not a roofline fraction"}},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_tot / args.steps,
-                "api": "ebic_eval_counts (Evaluator.evaluate_population), pinned host arrays" if (world == 1 or replica)
-                       else f"ShardedEvaluator({args.shard}) over ebic_eval_counts + NCCL"},
+                "ms_per_step": e2e_step, "api": api},
+        "amortized": amort,
         "gpu_launches": int(launches),
         "store": {"upload_ms": upload_ms, "index_build_ms": prepare_ms,
-                  "pair_trend_index_bytes": index_bytes if index_used else 0,
-                  "note": "one-time per matrix (upload+transpose) and per (matrix, approx) (rank plane + "
-                          "pair-trend index: every pair test of the matrix as row bitsets, independent of the "
-                          "candidates); not part of a step, like the reference's matrix construction"},
+                  "pair_trend_index_bytes": per_rank_index,
+                  "index_budget_gb": args.index_budget_gb},
         "wall_ms_timed_region": wall * 1e3,
-        "parity_device_vs_host_api": parity_dev_vs_host,
+        "parity_device_vs_host_api": parity,
     }
-    if line["roofline"]["physical"]:
-        line["roofline"]["physical"]["frac"] = line["roofline"]["physical"]["gbs"] / peak
-    with_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
-    if with_cpu:
+    if per_rank is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank)
+        line["per_rank"] = gathered
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         CUR_APPROX[0], CUR_NEG[0] = cfg["approx"], cfg["negative"]
         run, kind, cores = cpu_eval_setup(m)
         n, t, cpu_counts = cpu_sample(run, pops, float(os.environ.get("EBIC_CPU_BUDGET_S", "12")))
-        gpu_counts = call(pops[0], tp)
+        gpu_counts = call(e2e_pops[0], tp)
         line["cpu_baseline"] = {
             "value": n / t, "unit": "evals/s", "cores": cores, "kind": kind,
             "sample": f"{n} candidates (whole {P}-candidate populations, cycled) x all {R} rows, {t:.1f} s "
@@ -578,6 +706,27 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     return 0
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """--gpus N without torchrun: re-launch this script with N ranks, one per GPU."""
+    import torch
+
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus and not args.share_gpu:
+        log(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n_dev} "
+            f"(--share-gpu runs the ranks on fewer GPUs, for testing only)")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, cwd=str(REPO))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -585,38 +734,53 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--shard", choices=["replica", "rows", "pop"], default="replica",
-                    help="N > 1: replica = every rank evaluates its own population on the replicated matrix, "
-                         "no collective (weak scaling, the default: candidates are independent); rows = matrix "
-                         "rows sharded, NCCL all_reduce of the partial counts (strong); pop = one population "
-                         "split across ranks + all_gather (strong)")
+    ap.add_argument("--shard", choices=["rows", "pop", "replica"], default=None,
+                    help="N > 1: rows (default; BASELINE config 3: row-sharded strong scaling with the pipelined "
+                         "peer-memory exchange), pop (population split + all_gather) or replica (independent "
+                         "populations, no collective; weak scaling)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
-                    help="rows mode: sum the partial counts over peer memory (exchange windows mapped with "
-                         "CUDA IPC, one fused kernel) or with an NCCL all_reduce")
+                    help="rows mode: sum the partial counts over peer memory (default) or with an NCCL all_reduce")
+    ap.add_argument("--l2", choices=["auto", "stream", "flush"], default="auto")
+    ap.add_argument("--pops", type=int, default=0, help="populations cycled (0 = enough to exceed 2x L2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
-                    help="collective backend for N > 1 (gloo lets N ranks share one GPU to test the sharded path)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default=None,
+                    help="process-group backend for N > 1 (default nccl; gloo with --share-gpu)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="allow N ranks on fewer than N GPUs (tests the sharded path on a 1-GPU box; not scaling data)")
+    ap.add_argument("--index-budget-gb", type=float, default=None,
+                    help="pair-trend index budget (default: the library's, 40%% of free HBM)")
     ap.add_argument("--path", choices=["auto", "value", "plane", "table"], default="auto",
                     help="evaluation kernel: rank-plane slab kernel (auto for <= 8192 cols) or float value kernel")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.shard is None:
+        args.shard = "rows" if args.gpus > 1 else "none"
 
     if args.impl == "reference":
         return bench_reference(args, cfg, rank)
 
+    if env_world is None and args.gpus > 1:
+        return self_launch(args)
+    world = int(env_world or "1")
+    if world != args.gpus:
+        log(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return 2
     dist = None
     if world > 1:
         import torch
         import torch.distributed as tdist
 
         n_dev = torch.cuda.device_count()
+        if n_dev < world and not args.share_gpu:
+            log(f"bench.py: {world} ranks need {world} visible GPUs, found {n_dev}")
+            return 2
         dev_idx = local_rank % max(n_dev, 1)
         torch.cuda.set_device(dev_idx)
-        if args.backend == "nccl":
+        backend = args.backend or ("gloo" if n_dev < world else "nccl")
+        if backend == "nccl":
             tdist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
         else:
             tdist.init_process_group("gloo")

@@ -228,13 +228,22 @@ int ebic_ctx_set_path(ebic_ctx* ctx, int path);
  * benchmarking. */
 int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_per_warp);
 
-/* Memory budget of the pair-trend index (bytes; default 128 GiB, env
- * EBIC_TABLE_BUDGET_MB); AUTO uses the index only if it needs <= min(budget,
- * free device memory at upload minus a reserve of max(8 GiB, 10%)). */
+/* Memory budget of the pair-trend index (bytes; env EBIC_TABLE_BUDGET_MB).
+ * Default (bytes = 0): 40% of the device memory free at upload, so one
+ * context never takes most of a shared GPU.  An explicit budget replaces the
+ * fraction and is capped at the free memory minus a reserve of
+ * max(8 GiB, 10%); use it to opt in to very large indexes (a 200k x 2000
+ * matrix needs 100 GB).  AUTO uses the index only if it fits the budget. */
 int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes);
 /* Bytes the pair-trend index of the resident matrix needs (0 if the matrix is
  * too wide for the rank plane) and whether it is built. */
 int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use);
+
+/* One-time costs of the last (matrix, approx) preparation, in milliseconds:
+ * the index allocation (host clock; 0 when a kept allocation was reused), the
+ * rank-plane build and the pair-trend index build (CUDA events on the
+ * context's stream).  0 for a step that was not run.  Waits for the builds. */
+int ebic_matrix_build_info(ebic_ctx* ctx, double* alloc_ms, double* plane_ms, double* index_ms);
 
 /* Build (or reuse) the rank plane of the resident matrix for `approx` now,
  * instead of lazily on the first evaluation with that approx.  The plane is a
@@ -252,7 +261,7 @@ int ebic_matrix_prepare(ebic_ctx* ctx, double approx);
  * ebic_eval_counts_rows_sum (all ranks, same order).  ebic_xchg_open_local
  * maps windows of contexts in the SAME process instead (device pointers from
  * ebic_xchg_window).  A rank that never arrives makes the kernel give up after
- * ~2 s; the next ebic_ctx_sync reports it.  Ranks sharing one GPU (tests) must
+ * EBIC_XCHG_TIMEOUT_MS; the next ebic_ctx_sync reports it.  Ranks sharing one GPU (tests) must
  * build their index first (ebic_matrix_prepare): a device allocation inside a
  * step can wait for the device to go idle, i.e. for a peer's spinning kernel. */
 #define EBIC_IPC_HANDLE_BYTES 64
@@ -263,10 +272,29 @@ int ebic_xchg_open_local(ebic_ctx* ctx, void* const* windows /* world device poi
 int ebic_xchg_window(ebic_ctx* ctx, void** window_out);
 int ebic_xchg_destroy(ebic_ctx* ctx);
 /* Device pointers, asynchronous on `stream`: counts of this rank's row shard,
- * summed over all ranks, land in d_counts on every rank. */
+ * summed over all ranks, land in d_counts on every rank (ordered on `stream`).
+ * Every window must have been created with the same world and max_cand
+ * (checked when the windows are opened).  If this rank's count fails, the
+ * exchange still runs -- it pushes zeros and poisons every rank's window --
+ * so no rank falls an epoch behind; every rank's counts of that step and all
+ * later ones are then 0xFFFFFFFF and ebic_ctx_sync reports the failure.  A
+ * rank that does not arrive within EBIC_XCHG_TIMEOUT_MS (default 10000)
+ * makes the waiting ranks write 0xFFFFFFFF and report a timeout. */
 int ebic_eval_counts_rows_sum(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
                               uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
                               void* stream);
+/* Pipelined variant (overlap step k's exchange with step
+ * k+1's count).  The count runs on `stream`; the exchange runs on the
+ * context's own exchange stream as soon as the count is done, so the next
+ * call's count kernel does not wait for it.  d_counts is complete only once a
+ * stream has passed ebic_xchg_fence (or after ebic_ctx_sync); d_cols and
+ * d_offsets may be reused as soon as `stream` passes the call. */
+int ebic_eval_counts_rows_sum_async(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
+                                    uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
+                                    void* stream);
+/* Make `stream` (NULL = the context's stream) wait for every exchange issued
+ * so far by this context. */
+int ebic_xchg_fence(ebic_ctx* ctx, void* stream);
 
 #ifdef __cplusplus
 }

@@ -66,7 +66,11 @@ SIGNATURES = {
     "ebic_xchg_window": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
     "ebic_xchg_destroy": (C.c_int, [_vp]),
     "ebic_eval_counts_rows_sum": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double, C.c_int, _vp, _vp]),
+    "ebic_eval_counts_rows_sum_async": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double, C.c_int, _vp, _vp]),
+    "ebic_xchg_fence": (C.c_int, [_vp, _vp]),
     "ebic_matrix_prepare": (C.c_int, [_vp, C.c_double]),
+    "ebic_matrix_build_info": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
 }
 
 EBIC_PATH_AUTO = 0

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -162,7 +163,17 @@ struct ebic_ctx {
   bool xchg_ipc_opened[ebic::kMaxRanks] = {};      // peer windows opened through CUDA IPC
   int xchg_world = 0, xchg_rank = 0;
   uint64_t xchg_max = 0, xchg_epoch = 0;
-  DevBuf<uint32_t> d_xchg_local;                   // this rank's partial counts
+  uint64_t xchg_timeout_ns = 10'000'000'000ull;    // EBIC_XCHG_TIMEOUT_MS (default 10 s)
+  // Pipelining: step k counts into local[k % kXchgDepth] on the caller's
+  // stream; its exchange runs on xchg_stream once the count has finished, so
+  // step k+1's count overlaps step k's exchange.  cdone[s]: the count of the
+  // step in ring slot s is done; xdone[s]: its exchange is done (the slot's
+  // local buffer may be refilled).
+  static constexpr int kXchgDepth = 2;
+  cudaStream_t xchg_stream = nullptr;
+  cudaEvent_t xchg_cdone[kXchgDepth] = {}, xchg_xdone[kXchgDepth] = {};
+  bool xchg_xdone_armed[kXchgDepth] = {};
+  DevBuf<uint32_t> d_xchg_local[kXchgDepth];       // this rank's partial counts, per ring slot
   int pipeline_pieces = 1;       // EBIC_HOST_PIECES (1 = no pipelining; measured faster on B200 at 16K candidates)
   Slot slots[EBIC_MARSHAL_SLOTS];
   uint64_t next_ticket = 1;
@@ -174,13 +185,16 @@ struct ebic_ctx {
   uint32_t* d_plane = nullptr;
   bool plane_valid = false;
   // pair-trend index (ebic_table.cuh), per matrix x approx; used when it fits
-  // table_budget bytes (EBIC_TABLE_BUDGET_MB; default min(24 GB, free HBM / 2)
-  // at upload time)
+  // table_budget bytes.  Default budget: kDefaultBudgetFrac of the device
+  // memory free at upload (counting a kept index allocation as free), so the
+  // library never takes most of a shared GPU by itself; an explicit budget
+  // (ebic_ctx_set_table_budget / EBIC_TABLE_BUDGET_MB) replaces the fraction
+  // and is capped at the free memory minus a reserve of max(8 GiB, 10%).
   uint32_t* d_table = nullptr;
   bool table_valid = false, table_failed = false;
   double table_approx = 0.0;
   uint64_t table_budget = 0;
-  uint64_t table_budget_user = 128ull << 30;  // ebic_ctx_set_table_budget / EBIC_TABLE_BUDGET_MB
+  uint64_t table_budget_user = 0;  // 0 = the default fraction
   double plane_approx = 0.0;
   int path = EBIC_PATH_AUTO;
   int n_sms = 148;
@@ -192,6 +206,12 @@ struct ebic_ctx {
   int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (TMA warps up to 256 slices; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
+  // one-time build costs of the last (matrix, approx) preparation
+  // (ebic_matrix_build_info): events around the plane and index kernels, host
+  // clock around the index allocation (cudaMalloc is synchronous)
+  cudaEvent_t ev_build[4] = {};  // plane start / plane end / index start / index end
+  bool plane_timed = false, index_timed = false;
+  double index_alloc_ms = 0.0;
 };
 
 namespace {
@@ -239,6 +259,17 @@ void launch_count_t(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_off
   ctx->launches++;
 }
 
+// ---- one-time build timing (ebic_matrix_build_info) --------------------------
+int build_event(ebic_ctx* ctx, int k, cudaStream_t s) {
+  if (!ctx->ev_build[k]) EBIC_CUDA(cudaEventCreate(&ctx->ev_build[k]));
+  EBIC_CUDA(cudaEventRecord(ctx->ev_build[k], s));
+  return EBIC_OK;
+}
+
+double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 // ---- rank plane ------------------------------------------------------------
 bool plane_fits(const ebic_ctx* ctx) { return ctx->n_cols >= 1 && ctx->n_cols <= ebic::kPlaneMaxCols; }
 
@@ -249,6 +280,7 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   if (!ctx->d_plane) {
     EBIC_CUDA(cudaMalloc(&ctx->d_plane, ctx->ld * ctx->n_cols * sizeof(uint32_t)));
   }
+  EBIC_TRY(build_event(ctx, 0, s));
   EBIC_CUDA(cudaMemsetAsync(ctx->d_plane, 0, ctx->ld * ctx->n_cols * sizeof(uint32_t), s));
   uint32_t pow2 = 1;
   while (pow2 < ctx->n_cols) pow2 <<= 1;
@@ -290,6 +322,8 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   }
   ctx->launches++;
   EBIC_CUDA(cudaGetLastError());
+  EBIC_TRY(build_event(ctx, 1, s));
+  ctx->plane_timed = true;
   ctx->plane_valid = true;
   ctx->plane_approx = approx;
   return EBIC_OK;
@@ -336,6 +370,16 @@ uint64_t index_headroom(uint64_t free_bytes) {
   return free_bytes > reserve ? free_bytes - reserve : 0;
 }
 
+// The index budget for `avail` bytes of device memory (free memory plus a kept
+// index allocation): the explicit budget if one was set, else
+// kDefaultBudgetFrac of avail; never more than the headroom.
+constexpr double kDefaultBudgetFrac = 0.4;
+uint64_t index_budget(const ebic_ctx* ctx, uint64_t avail) {
+  const uint64_t head = index_headroom(avail);
+  if (ctx->table_budget_user) return std::min<uint64_t>(ctx->table_budget_user, head);
+  return std::min<uint64_t>(head, (uint64_t)((double)avail * kDefaultBudgetFrac));
+}
+
 constexpr int kTableNoMemory = -1;  // internal status: the index does not fit (fall back)
 
 // Words per pair vector: a multiple of 4 (uint4 slices); vectors of more than
@@ -370,15 +414,19 @@ int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
     ctx->d_table = nullptr;
     ctx->table_cap = 0;
   }
+  ctx->index_alloc_ms = 0.0;
   if (!ctx->d_table) {
+    const double t0 = host_ms();
     if (cudaMalloc(&ctx->d_table, table_bytes(ctx)) != cudaSuccess) {
       cudaGetLastError();
       ctx->d_table = nullptr;
       ctx->table_failed = true;
       return kTableNoMemory;
     }
+    ctx->index_alloc_ms = host_ms() - t0;
     ctx->table_cap = table_bytes(ctx);
   }
+  EBIC_TRY(build_event(ctx, 2, s));
   const uint32_t wp = (uint32_t)table_wp(ctx);
   // (row block, a tile) CTAs, times z slices of the b columns chosen so the
   // last wave is as full as possible (C3: 640 tiles = 2.2 waves of 2 CTAs per
@@ -407,6 +455,8 @@ int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
         ctx->d_plane, ctx->ld, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp, ctx->d_table, b_per_z);
   ctx->launches++;
   EBIC_CUDA(cudaGetLastError());
+  EBIC_TRY(build_event(ctx, 3, s));
+  ctx->index_timed = true;
   ctx->table_valid = true;
   ctx->table_approx = approx;
   return EBIC_OK;
@@ -901,6 +951,7 @@ void drop_matrix(ebic_ctx* ctx, bool keep_index_alloc) {
     ctx->table_cap = 0;
   }
   ctx->table_valid = ctx->table_failed = false;
+  ctx->plane_timed = ctx->index_timed = false;
   ctx->d_mat = nullptr;
   ctx->store = 0;
   ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
@@ -999,13 +1050,13 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   ctx->ld = ld;
   ctx->row_base = row_base;
   {
-    // pair-trend index budget: the user cap, at most half of the free HBM
+    // pair-trend index budget (index_budget): measured against the memory free now
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
       cudaGetLastError();
       fr = 0;
     }
-    ctx->table_budget = std::min<uint64_t>(ctx->table_budget_user, index_headroom(fr + ctx->table_cap));
+    ctx->table_budget = index_budget(ctx, fr + ctx->table_cap);
     // a kept index allocation: reused if this matrix's index fits it and
     // is allowed, otherwise (or if it is more than twice the need) released
     if (ctx->d_table && (!table_allowed(ctx) || ctx->table_cap < table_bytes(ctx) ||
@@ -1111,6 +1162,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (ts) ctx->tma_slots = std::max(2, std::min(4, std::atoi(ts)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");
     if (tk) ctx->table_kernel = std::atoi(tk);
+    const char* xt = std::getenv("EBIC_XCHG_TIMEOUT_MS");
+    if (xt && std::atoll(xt) > 0) ctx->xchg_timeout_ns = (uint64_t)std::atoll(xt) * 1000000ull;
     const char* sc = std::getenv("EBIC_PAIR_LAYOUT");
     int fp = 0, fs = 0;
     if (sc && std::sscanf(sc, "%d,%d", &fp, &fs) == 2) ctx->simd_force = fp * 16 + fs;
@@ -1150,6 +1203,13 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   for (cudaEvent_t& e : ctx->piece_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (int i = 0; i < ebic_ctx::kXchgDepth; ++i) {
+    if (ctx->xchg_cdone[i]) cudaEventDestroy(ctx->xchg_cdone[i]);
+    if (ctx->xchg_xdone[i]) cudaEventDestroy(ctx->xchg_xdone[i]);
+  }
+  if (ctx->xchg_stream) cudaStreamDestroy(ctx->xchg_stream);
+  for (cudaEvent_t& e : ctx->ev_build)
+    if (e) cudaEventDestroy(e);
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -1166,12 +1226,15 @@ int ebic_ctx_sync(ebic_ctx* ctx) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
   EBIC_TRY(set_device(ctx));
   EBIC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->xchg_stream) EBIC_CUDA(cudaStreamSynchronize(ctx->xchg_stream));
   EBIC_CUDA(cudaDeviceSynchronize());
   int err = 0;
   EBIC_CUDA(cudaMemcpy(&err, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err) {
     EBIC_CUDA(cudaMemset(ctx->d_err, 0, sizeof(int)));
-    if (err == 4) return fail(EBIC_ERR_CUDA, "peer exchange timed out: a rank did not arrive");
+    if (err == 4) return fail(EBIC_ERR_CUDA, "peer exchange timed out: a rank did not arrive (counts set to 0xFFFFFFFF)");
+    if (err == 5)
+      return fail(EBIC_ERR_CUDA, "peer exchange poisoned: a rank's count failed (counts set to 0xFFFFFFFF)");
     return fail(EBIC_ERR_INVALID_ARGUMENT,
                 "device detected an empty candidate or an out-of-range column index");
   }
@@ -1621,7 +1684,7 @@ int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes) {
       cudaGetLastError();
       fr = 0;
     }
-    ctx->table_budget = std::min<uint64_t>(bytes, index_headroom(fr + (ctx->d_table ? table_bytes(ctx) : 0)));
+    ctx->table_budget = index_budget(ctx, fr + ctx->table_cap);
   }
   return EBIC_OK;
 }
@@ -1630,6 +1693,24 @@ int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use) {
   EBIC_TRY(need_matrix(ctx));
   if (bytes_needed) *bytes_needed = plane_fits(ctx) ? table_bytes(ctx) : 0;
   if (in_use) *in_use = ctx->table_valid ? 1 : 0;
+  return EBIC_OK;
+}
+
+int ebic_matrix_build_info(ebic_ctx* ctx, double* alloc_ms, double* plane_ms, double* index_ms) {
+  EBIC_TRY(need_matrix(ctx));
+  EBIC_TRY(set_device(ctx));
+  float pm = 0.f, im = 0.f;
+  if (ctx->plane_timed) {
+    EBIC_CUDA(cudaEventSynchronize(ctx->ev_build[1]));
+    EBIC_CUDA(cudaEventElapsedTime(&pm, ctx->ev_build[0], ctx->ev_build[1]));
+  }
+  if (ctx->index_timed) {
+    EBIC_CUDA(cudaEventSynchronize(ctx->ev_build[3]));
+    EBIC_CUDA(cudaEventElapsedTime(&im, ctx->ev_build[2], ctx->ev_build[3]));
+  }
+  if (alloc_ms) *alloc_ms = ctx->index_timed ? ctx->index_alloc_ms : 0.0;
+  if (plane_ms) *plane_ms = pm;
+  if (index_ms) *index_ms = im;
   return EBIC_OK;
 }
 
@@ -1684,20 +1765,107 @@ int ebic_matrix_load_tsv(ebic_ctx* ctx, const char* path, int n_threads, int sto
 
 // ---- row-shard exchange over peer memory ----------------------------------
 
+}  // extern "C"
+
+namespace {
+
+// Every peer's window header must match ours: same world size and inbox size
+// (a push into a smaller peer's inbox would write past its window).
+int check_peer_header(ebic_ctx* ctx, int g) {
+  ebic::XchgHeader h{};
+  EBIC_CUDA(cudaMemcpy(&h, ctx->xchg_peer[g], sizeof(h), cudaMemcpyDefault));
+  if (h.magic != ebic::kXchgMagic)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "peer window %d is not an exchange window", g);
+  if ((int)h.world != ctx->xchg_world || h.max_cand != (uint32_t)ctx->xchg_max)
+    return fail(EBIC_ERR_INVALID_ARGUMENT,
+                "peer window %d was created with world=%u max_cand=%u; this rank has world=%d max_cand=%llu", g,
+                h.world, h.max_cand, ctx->xchg_world, (unsigned long long)ctx->xchg_max);
+  return EBIC_OK;
+}
+
+int xchg_ready(ebic_ctx* ctx, uint64_t n_cand, const void* d_cols, const void* d_offsets, const void* d_counts) {
+  EBIC_TRY(need_matrix(ctx));
+  if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
+  for (int g = 0; g < ctx->xchg_world; ++g)
+    if (!ctx->xchg_peer[g]) return fail(EBIC_ERR_INVALID_ARGUMENT, "peer window %d not opened", g);
+  if (n_cand > ctx->xchg_max)
+    return fail(EBIC_ERR_CAPACITY, "%llu candidates exceed the exchange window (%llu)", (unsigned long long)n_cand,
+                (unsigned long long)ctx->xchg_max);
+  if (n_cand && (!d_cols || !d_offsets || !d_counts)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null device pointer");
+  return EBIC_OK;
+}
+
+// One pipelined row-sharded step (see ctx->kXchgDepth): count on `s` into the
+// ring slot's local buffer, exchange on the context's exchange stream.  Every
+// rank runs the same sequence of steps, so the epochs agree -- including when
+// this rank's count fails: the exchange still runs (pushing zeros and
+// poisoning the peers' windows), so no rank is left an epoch behind, and the
+// count's error is returned afterwards.
+int rows_sum_step(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets, uint64_t n_cand, double approx,
+                  int neg, uint32_t* d_counts, cudaStream_t s) {
+  const uint64_t k = ctx->xchg_epoch;  // steps issued so far
+  const int slot = (int)(k % ebic_ctx::kXchgDepth);
+  cudaStream_t xs = ctx->xchg_stream;
+  // the slot's buffer was last read by the exchange of step k - depth
+  if (ctx->xchg_xdone_armed[slot]) EBIC_CUDA(cudaStreamWaitEvent(s, ctx->xchg_xdone[slot], 0));
+  int st = check_approx(approx);
+  if (st == EBIC_OK && n_cand)
+    st = count_into(ctx, d_cols, d_offsets, n_cand, approx, neg, ctx->d_xchg_local[slot].p, nullptr, s);
+  const std::string count_error = st == EBIC_OK ? std::string() : g_last_error;
+  EBIC_CUDA(cudaEventRecord(ctx->xchg_cdone[slot], s));
+  EBIC_CUDA(cudaStreamWaitEvent(xs, ctx->xchg_cdone[slot], 0));
+  const uint64_t epoch = k + 1;
+  ebic::XchgPeers peers;
+  for (int g = 0; g < ebic::kMaxRanks; ++g) peers.win[g] = ctx->xchg_peer[g];
+  ebic::xchg_sum_kernel<<<ebic::kXchgCtas, 256, 0, xs>>>(ctx->d_xchg_local[slot].p, (uint32_t)n_cand, peers,
+                                                          ctx->xchg_world, ctx->xchg_rank, epoch,
+                                                          (uint32_t)ctx->xchg_max, d_counts, ctx->d_err,
+                                                          st == EBIC_OK ? 0 : 1, ctx->xchg_timeout_ns);
+  ctx->launches++;
+  const cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess)  // the exchange never launched: the epoch did not advance
+    return fail(EBIC_ERR_CUDA, "exchange kernel launch: %s", cudaGetErrorString(le));
+  ctx->xchg_epoch = epoch;  // only once the exchange is in the stream
+  EBIC_CUDA(cudaEventRecord(ctx->xchg_xdone[slot], xs));
+  ctx->xchg_xdone_armed[slot] = true;
+  if (st != EBIC_OK) return fail(st, "%s (the exchange ran with zeros and poisoned the peers)", count_error.c_str());
+  return EBIC_OK;
+}
+
+int xchg_fence(ebic_ctx* ctx, cudaStream_t s) {
+  if (!ctx->xchg_stream) return EBIC_OK;
+  const uint64_t k = ctx->xchg_epoch;
+  if (k == 0) return EBIC_OK;
+  const int last = (int)((k - 1) % ebic_ctx::kXchgDepth);  // the exchanges are serialised on xchg_stream
+  EBIC_CUDA(cudaStreamWaitEvent(s, ctx->xchg_xdone[last], 0));
+  return EBIC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ebic_xchg_create(ebic_ctx* ctx, int world, int rank, uint64_t max_cand, void* handle_out) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
   if (world < 1 || world > ebic::kMaxRanks || rank < 0 || rank >= world)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "bad world/rank (%d, %d); at most %d ranks", world, rank, ebic::kMaxRanks);
-  if (max_cand == 0 || max_cand > 0xffffffffull) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad max_cand");
+  if (max_cand == 0 || max_cand > 0x7fffffffull) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad max_cand");
   EBIC_TRY(set_device(ctx));
   EBIC_TRY(ebic_xchg_destroy(ctx));
-  const size_t bytes = ebic::kMaxRanks * ebic::kXchgFlagStride * sizeof(uint64_t) +
-                       2ull * ebic::kMaxRanks * max_cand * sizeof(uint32_t);
+  const size_t bytes = ebic::xchg_window_bytes((uint32_t)max_cand);
   EBIC_CUDA(cudaMalloc(&ctx->xchg_win, bytes));
   EBIC_CUDA(cudaMemset(ctx->xchg_win, 0, bytes));
+  const ebic::XchgHeader h{ebic::kXchgMagic, (uint32_t)world, (uint32_t)max_cand, 0u};
+  EBIC_CUDA(cudaMemcpy(ctx->xchg_win, &h, sizeof(h), cudaMemcpyHostToDevice));
   // the step must not allocate: a device allocation can wait for an idle
   // device, i.e. for another rank's exchange kernel on a shared GPU
-  EBIC_TRY(ensure(ctx->d_xchg_local, max_cand));
+  for (auto& b : ctx->d_xchg_local) EBIC_TRY(ensure(b, max_cand));
+  if (!ctx->xchg_stream) EBIC_CUDA(cudaStreamCreateWithFlags(&ctx->xchg_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < ebic_ctx::kXchgDepth; ++i) {
+    if (!ctx->xchg_cdone[i]) EBIC_CUDA(cudaEventCreateWithFlags(&ctx->xchg_cdone[i], cudaEventDisableTiming));
+    if (!ctx->xchg_xdone[i]) EBIC_CUDA(cudaEventCreateWithFlags(&ctx->xchg_xdone[i], cudaEventDisableTiming));
+    ctx->xchg_xdone_armed[i] = false;
+  }
   ctx->xchg_world = world;
   ctx->xchg_rank = rank;
   ctx->xchg_max = max_cand;
@@ -1705,9 +1873,9 @@ int ebic_xchg_create(ebic_ctx* ctx, int world, int rank, uint64_t max_cand, void
   for (auto& p : ctx->xchg_peer) p = nullptr;
   ctx->xchg_peer[rank] = ctx->xchg_win;
   if (handle_out) {
-    cudaIpcMemHandle_t h;
-    EBIC_CUDA(cudaIpcGetMemHandle(&h, ctx->xchg_win));
-    std::memcpy(handle_out, &h, sizeof(h));
+    cudaIpcMemHandle_t ih;
+    EBIC_CUDA(cudaIpcGetMemHandle(&ih, ctx->xchg_win));
+    std::memcpy(handle_out, &ih, sizeof(ih));
   }
   return EBIC_OK;
 }
@@ -1731,6 +1899,7 @@ int ebic_xchg_open(ebic_ctx* ctx, const void* handles) {
     EBIC_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     ctx->xchg_peer[g] = static_cast<unsigned char*>(p);
     ctx->xchg_ipc_opened[g] = true;
+    EBIC_TRY(check_peer_header(ctx, g));
   }
   return EBIC_OK;
 }
@@ -1738,14 +1907,24 @@ int ebic_xchg_open(ebic_ctx* ctx, const void* handles) {
 int ebic_xchg_open_local(ebic_ctx* ctx, void* const* windows) {
   if (!ctx || !windows) return fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
   if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
-  for (int g = 0; g < ctx->xchg_world; ++g)
-    if (g != ctx->xchg_rank) ctx->xchg_peer[g] = static_cast<unsigned char*>(windows[g]);
+  EBIC_TRY(set_device(ctx));
+  for (int g = 0; g < ctx->xchg_world; ++g) {
+    if (g == ctx->xchg_rank) continue;
+    if (!windows[g]) return fail(EBIC_ERR_INVALID_ARGUMENT, "null window for rank %d", g);
+    ctx->xchg_peer[g] = static_cast<unsigned char*>(windows[g]);
+    const int st = check_peer_header(ctx, g);
+    if (st != EBIC_OK) {
+      ctx->xchg_peer[g] = nullptr;
+      return st;
+    }
+  }
   return EBIC_OK;
 }
 
 int ebic_xchg_destroy(ebic_ctx* ctx) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
   cudaSetDevice(ctx->device);
+  if (ctx->xchg_stream) cudaStreamSynchronize(ctx->xchg_stream);
   for (int g = 0; g < ebic::kMaxRanks; ++g) {
     if (ctx->xchg_ipc_opened[g] && ctx->xchg_peer[g]) cudaIpcCloseMemHandle(ctx->xchg_peer[g]);
     ctx->xchg_ipc_opened[g] = false;
@@ -1754,35 +1933,35 @@ int ebic_xchg_destroy(ebic_ctx* ctx) {
   if (ctx->xchg_win) cudaFree(ctx->xchg_win);
   ctx->xchg_win = nullptr;
   ctx->xchg_world = 0;
-  ctx->d_xchg_local.release();
+  ctx->xchg_epoch = 0;
+  for (auto& b : ctx->d_xchg_local) b.release();
+  for (bool& a : ctx->xchg_xdone_armed) a = false;
   return EBIC_OK;
+}
+
+int ebic_eval_counts_rows_sum_async(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
+                                    uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
+                                    void* stream) {
+  EBIC_TRY(xchg_ready(ctx, n_cand, d_cols, d_offsets, d_counts));
+  EBIC_TRY(set_device(ctx));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return rows_sum_step(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, d_counts, s);
+}
+
+int ebic_xchg_fence(ebic_ctx* ctx, void* stream) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  EBIC_TRY(set_device(ctx));
+  return xchg_fence(ctx, stream ? static_cast<cudaStream_t>(stream) : ctx->stream);
 }
 
 int ebic_eval_counts_rows_sum(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets, uint64_t n_cand,
                               double approx, int negative_trends, uint32_t* d_counts, void* stream) {
-  EBIC_TRY(need_matrix(ctx));
-  EBIC_TRY(check_approx(approx));
-  if (!ctx->xchg_win) return fail(EBIC_ERR_INVALID_ARGUMENT, "no exchange window (ebic_xchg_create)");
-  for (int g = 0; g < ctx->xchg_world; ++g)
-    if (!ctx->xchg_peer[g]) return fail(EBIC_ERR_INVALID_ARGUMENT, "peer window %d not opened", g);
-  if (n_cand > ctx->xchg_max)
-    return fail(EBIC_ERR_CAPACITY, "%llu candidates exceed the exchange window (%llu)",
-                (unsigned long long)n_cand, (unsigned long long)ctx->xchg_max);
-  if (n_cand && (!d_cols || !d_offsets || !d_counts)) return fail(EBIC_ERR_INVALID_ARGUMENT, "null device pointer");
+  EBIC_TRY(xchg_ready(ctx, n_cand, d_cols, d_offsets, d_counts));
   EBIC_TRY(set_device(ctx));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  // every rank runs the same sequence of steps, so the epochs agree
-  const uint64_t epoch = ++ctx->xchg_epoch;
-  EBIC_TRY(ensure(ctx->d_xchg_local, std::max<uint64_t>(n_cand, 1)));
-  EBIC_TRY(count_into(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, ctx->d_xchg_local.p, nullptr, s));
-  ebic::XchgPeers peers;
-  for (int g = 0; g < ebic::kMaxRanks; ++g) peers.win[g] = ctx->xchg_peer[g];
-  ebic::xchg_sum_kernel<<<ebic::kXchgCtas, 256, 0, s>>>(ctx->d_xchg_local.p, (uint32_t)n_cand, peers,
-                                                         ctx->xchg_world, ctx->xchg_rank, epoch,
-                                                         (uint32_t)ctx->xchg_max, d_counts, ctx->d_err);
-  ctx->launches++;
-  EBIC_CUDA(cudaGetLastError());
-  return EBIC_OK;
+  const int st = rows_sum_step(ctx, d_cols, d_offsets, n_cand, approx, negative_trends, d_counts, s);
+  EBIC_TRY(xchg_fence(ctx, s));  // the summed counts are ordered on `stream`
+  return st;
 }
 
 }  // extern "C"

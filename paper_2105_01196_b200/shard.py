@@ -19,6 +19,12 @@ rank 0 -- over NVLink into each GPU's memory with NCCL, where each rank builds
 its store straight from the device buffer (ebic_matrix_upload_device_*), or as
 a CPU tensor with gloo.
 
+Exchange of the rows layout: `exchange="collective"` sums the partial counts
+with one all_reduce of the process group (NCCL over NVLink, or gloo);
+`exchange="p2p"` sums them on the device through the exchange windows of
+ebic_xchg.cuh (every rank's window mapped into every rank with CUDA IPC, one
+fused push/wait/sum kernel, no collective call per step).
+
 The evaluator itself is injected (`local`), so the sharding / exchange logic is
 the same object in production (the CUDA `Evaluator`) and in the CPU gloo tests.
 """
@@ -72,24 +78,95 @@ class ShardedEvaluator:
     """
 
     def __init__(self, local, matrix: np.ndarray | None, mode: str = "rows", dist=None, group=None,
-                 source: str = "local"):
+                 source: str = "local", exchange: str = "collective", max_cand: int = 0):
         if mode not in ("rows", "pop"):
             raise ValueError("mode must be 'rows' or 'pop'")
         if source not in ("local", "broadcast"):
             raise ValueError("source must be 'local' or 'broadcast'")
+        if exchange not in ("collective", "p2p"):
+            raise ValueError("exchange must be 'collective' or 'p2p'")
         self.local = local
         self.dist = dist
         self.group = group
+        self.exchange = exchange if mode == "rows" else "collective"
         world = dist.get_world_size(group) if dist is not None else 1
         rank = dist.get_rank(group) if dist is not None else 0
         if source == "broadcast" and world > 1:
             self._upload_broadcast(matrix, mode, rank, world)
-            return
-        if matrix is None:
-            raise ValueError("matrix is required with source='local'")
-        self.spec = ShardSpec(mode, rank, world, int(matrix.shape[0]), int(matrix.shape[1]))
-        b, e = self.spec.rows
-        local.upload(np.ascontiguousarray(matrix[b:e]), row_base=b)
+        else:
+            if matrix is None:
+                raise ValueError("matrix is required with source='local'")
+            self.spec = ShardSpec(mode, rank, world, int(matrix.shape[0]), int(matrix.shape[1]))
+            b, e = self.spec.rows
+            local.upload(np.ascontiguousarray(matrix[b:e]), row_base=b)
+        if self.exchange == "p2p":
+            if max_cand <= 0:
+                raise ValueError("exchange='p2p' needs max_cand (the largest population per call)")
+            self._setup_p2p(int(max_cand))
+
+    @classmethod
+    def attach(cls, local, n_rows: int, n_cols: int, mode: str = "rows", dist=None, group=None,
+               exchange: str = "collective", max_cand: int = 0) -> "ShardedEvaluator":
+        """Wrap a context that already holds this rank's shard (uploaded with
+        row_base = row_range(...)[0]) and, for exchange='p2p', an opened
+        exchange window of at least max_cand candidates."""
+        self = cls.__new__(cls)
+        self.local, self.dist, self.group = local, dist, group
+        world = dist.get_world_size(group) if dist is not None else 1
+        rank = dist.get_rank(group) if dist is not None else 0
+        self.spec = ShardSpec(mode, rank, world, int(n_rows), int(n_cols))
+        self.exchange = exchange if mode == "rows" else "collective"
+        if self.exchange == "p2p":
+            self._setup_p2p(int(max_cand), window_open=True)
+        return self
+
+    def _setup_p2p(self, max_cand: int, window_open: bool = False) -> None:
+        """Create this rank's exchange window and map every peer's (IPC handles
+        all-gathered once through the process group)."""
+        import torch
+
+        if not window_open:
+            handle = self.local.xchg_create(self.spec.world, self.spec.rank, max_cand)
+            handles = [handle]
+            if self.dist is not None and self.spec.world > 1:
+                handles = [None] * self.spec.world
+                self.dist.all_gather_object(handles, handle, group=self.group)
+            self.local.xchg_open(handles)
+        self.max_cand = max_cand
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._dev = dev
+        self._stream = torch.cuda.Stream(dev)
+        self._h_counts = torch.empty(max_cand, dtype=torch.int32, pin_memory=True)
+        self._d_counts = torch.empty(max_cand, dtype=torch.int32, device=dev)
+        self._pinned = {}
+
+    def _pin(self, key: str, a: np.ndarray):
+        """Page-locked staging copy of a host array (grown on demand)."""
+        import torch
+
+        buf = self._pinned.get(key)
+        if buf is None or buf.numel() < a.size:
+            buf = torch.empty(max(a.size, 1024), dtype=torch.int32, pin_memory=True)
+            self._pinned[key] = buf
+        buf.numpy().view(np.uint32)[:a.size] = a
+        return buf[:a.size]
+
+    def _rows_sum_p2p(self, pop: Population, p: TrendParams) -> np.ndarray:
+        import torch
+
+        n = len(pop)
+        if n > self.max_cand:
+            raise ValueError(f"{n} candidates exceed the exchange window ({self.max_cand})")
+        with torch.cuda.stream(self._stream):
+            d_cols = self._pin("cols", pop.cols).to(self._dev, non_blocking=True)
+            d_offs = self._pin("offs", pop.offsets).to(self._dev, non_blocking=True)
+            self.local.evaluate_population_rows_sum_device(d_cols.data_ptr(), d_offs.data_ptr(), n,
+                                                           self._d_counts.data_ptr(), p,
+                                                           stream=self._stream.cuda_stream)
+            self._h_counts[:n].copy_(self._d_counts[:n], non_blocking=True)
+        self._stream.synchronize()
+        self.local.sync()  # raises on a device-side error (bad column, exchange timeout / poison)
+        return self._h_counts[:n].numpy().view(np.uint32).copy()
 
     def _upload_broadcast(self, matrix, mode, rank, world):
         """Rank 0's matrix to every rank (shape and dtype first), then each rank
@@ -147,6 +224,8 @@ class ShardedEvaluator:
     def evaluate_population(self, pop: Population, p: TrendParams | None = None) -> np.ndarray:
         p = p or TrendParams()
         if self.spec.mode == "rows":
+            if self.exchange == "p2p":
+                return self._rows_sum_p2p(pop, p)
             return self._all_reduce_sum(self.local.evaluate_population(pop, p))
         b, e = pop_range(len(pop), self.spec.rank, self.spec.world)
         mine = self.local.evaluate_population(slice_population(pop, b, e), p)

@@ -205,6 +205,19 @@ class Evaluator:
                                                 float(p.approx), int(bool(p.negative_trends)),
                                                 C.c_void_p(d_counts), C.c_void_p(stream or 0)))
 
+    def evaluate_population_rows_sum_async(self, d_cols: int, d_offsets: int, n_cand: int, d_counts: int,
+                                           params: TrendParams | None = None, stream: int | None = None) -> None:
+        """Pipelined row-sharded step: the count runs on `stream`, the exchange on the
+        context's exchange stream; d_counts is complete after xchg_fence(stream) / sync()."""
+        p = params or TrendParams()
+        check(self._L.ebic_eval_counts_rows_sum_async(self._h, C.c_void_p(d_cols), C.c_void_p(d_offsets),
+                                                      int(n_cand), float(p.approx), int(bool(p.negative_trends)),
+                                                      C.c_void_p(d_counts), C.c_void_p(stream or 0)))
+
+    def xchg_fence(self, stream: int | None = None) -> None:
+        """Order `stream` after every exchange issued so far."""
+        check(self._L.ebic_xchg_fence(self._h, C.c_void_p(stream or 0)))
+
     def load_tsv(self, path, threads: int = 0, store: int = EBIC_STORE_AUTO) -> tuple[int, int, int]:
         """Parse a reference-format TSV matrix (io.cpp:78-111) on all host threads
         straight into page-locked memory and upload it; returns (rows, cols, store)."""
@@ -217,6 +230,12 @@ class Evaluator:
     def prepare(self, approx: float) -> None:
         """Build the rank plane for `approx` now (otherwise built on first use)."""
         check(self._L.ebic_matrix_prepare(self._h, float(approx)))
+
+    def build_info(self) -> dict:
+        """One-time costs (ms) of the last preparation: index allocation, rank plane, pair-trend index."""
+        a, pl, ix = C.c_double(0), C.c_double(0), C.c_double(0)
+        check(self._L.ebic_matrix_build_info(self._h, C.byref(a), C.byref(pl), C.byref(ix)))
+        return {"alloc_ms": a.value, "plane_ms": pl.value, "index_ms": ix.value}
 
     # -- matrix store ------------------------------------------------------
     def upload(self, matrix: np.ndarray, row_base: int = 0, store: int = EBIC_STORE_AUTO) -> int:
