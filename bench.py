@@ -667,6 +667,13 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                      "algorithmic 4 B x L x R per eval (no index: the slab/value kernel re-reads the matrix "
                      "from L2/shared memory, so this can exceed HBM)",
                      "peak_source": peak_src,
+                     "stream": ({"gbs": statistics.mean(phys) / (ms_per_step / 1e3) / 1e9,
+                                 "frac": statistics.mean(phys) / (ms_per_step / 1e3) / 1e9 / peak,
+                                 "what": "the same physical bytes over the timed region's step time: batches "
+                                         "issued back to back overlap one kernel's tail with the next one's start "
+                                         "(programmatic dependent launch), which the per-launch events of the "
+                                         "kernel pass (and ncu, which serialises launches) exclude"}
+                                if (phys_gbs is not None and l2_mode == "stream" and world == 1) else None),
                      "effective_algorithmic": {"bytes_per_launch": statistics.mean(alg), "gbs": alg_gbs,
                                                "x_of_peak": alg_gbs / peak,
                                                "what": "SURVEY 8(d) algorithmic bytes (4 B x L x R per eval, each "

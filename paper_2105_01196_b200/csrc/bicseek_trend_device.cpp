@@ -18,20 +18,30 @@
 // call (trend.hpp:43-45).  The first call uploads it (float32 store when every
 // value is float32-representable, else float64 -- bit-exact either way); later
 // calls reuse the resident copy when the pointer, shape AND contents match
-// (contents are compared against a host shadow copy, so a different matrix
-// that happens to reuse a freed buffer is never mistaken for the cached one).
+// (contents are compared against a host shadow copy, so a matrix mutated in
+// place, or a different matrix that reuses a freed buffer, is never mistaken
+// for the cached one).  The comparison -- and the shadow copy at upload --
+// runs on a persistent pool of host threads in 4-MB chunks with an early exit
+// (HostPool below): 160 MB at 20k x 1000 is a few milliseconds on 16 cores
+// instead of a single-threaded memcmp of the whole matrix per call.
 // EBIC_SHIM_TRUST_POINTER=1 skips the content comparison for very large
-// matrices whose identity the caller guarantees (e.g. one run()).
+// matrices whose identity the caller guarantees (e.g. one run());
+// EBIC_SHIM_THREADS=<n> sizes the pool (default: all hardware threads).
 // EBIC_DEVICE=<n> pins the CUDA device; by default each thread's context goes
 // to the next visible device round-robin.  State is thread_local, so
 // concurrent run()s on different threads (bench.cpp:103-121) get independent
 // contexts and streams -- on different GPUs when there are several.
+#include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "bicseek/trend.hpp"
@@ -48,6 +58,111 @@ void TrendParams::validate() const {
 }
 
 namespace {
+
+// Persistent host thread pool for chunked byte-range work (compare / copy of
+// the matrix shadow).  One job at a time; the calling thread takes chunks too.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  // fn(begin, end) over [0, n) in chunks of `chunk`; stops handing out chunks
+  // once `stop` is set (by fn)
+  void run(std::size_t n, std::size_t chunk, const std::function<void(std::size_t, std::size_t)>& fn,
+           const std::atomic<bool>* stop = nullptr) {
+    std::lock_guard<std::mutex> job_lock(job_mu_);
+    const std::size_t n_chunks = (n + chunk - 1) / chunk;
+    if (workers_.empty() || n_chunks <= 1) {
+      for (std::size_t c = 0; c < n_chunks && !(stop && stop->load()); ++c) fn(c * chunk, std::min(n, (c + 1) * chunk));
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      fn_ = &fn;
+      stop_ = stop;
+      n_ = n;
+      chunk_ = chunk;
+      next_.store(0);
+      active_ = workers_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> l(mu_);
+    done_cv_.wait(l, [&] { return active_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    unsigned n = std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("EBIC_SHIM_THREADS")) n = (unsigned)std::max(1, std::atoi(e));
+    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      quit_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void drain() {
+    const std::size_t n_chunks = (n_ + chunk_ - 1) / chunk_;
+    for (;;) {
+      if (stop_ && stop_->load()) return;
+      const std::size_t c = next_.fetch_add(1);
+      if (c >= n_chunks) return;
+      (*fn_)(c * chunk_, std::min(n_, (c + 1) * chunk_));
+    }
+  }
+  void loop() {
+    std::uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return quit_ || gen_ != seen; });
+        if (quit_) return;
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> l(mu_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(std::size_t, std::size_t)>* fn_ = nullptr;
+  const std::atomic<bool>* stop_ = nullptr;
+  std::size_t n_ = 0, chunk_ = 1;
+  std::atomic<std::size_t> next_{0};
+  std::size_t active_ = 0;
+  std::uint64_t gen_ = 0;
+  bool quit_ = false;
+};
+
+constexpr std::size_t kChunkBytes = 4u << 20;
+
+bool same_bytes(const void* a, const void* b, std::size_t bytes) {
+  std::atomic<bool> differs{false};
+  const auto* pa = static_cast<const unsigned char*>(a);
+  const auto* pb = static_cast<const unsigned char*>(b);
+  HostPool::get().run(
+      bytes, kChunkBytes,
+      [&](std::size_t lo, std::size_t hi) {
+        if (std::memcmp(pa + lo, pb + lo, hi - lo) != 0) differs.store(true);
+      },
+      &differs);
+  return !differs.load();
+}
+
+void copy_bytes(void* dst, const void* src, std::size_t bytes) {
+  auto* d = static_cast<unsigned char*>(dst);
+  const auto* s = static_cast<const unsigned char*>(src);
+  HostPool::get().run(bytes, kChunkBytes, [&](std::size_t lo, std::size_t hi) { std::memcpy(d + lo, s + lo, hi - lo); });
+}
 
 struct DeviceState {
   ebic_ctx* ctx = nullptr;
@@ -91,8 +206,7 @@ ebic_ctx* bind(const ExpressionMatrix& m) {
   const std::vector<double>& v = m.values();
   const bool same = s.key == v.data() && s.rows == m.rows() && s.cols == m.cols() &&
                     (trust_pointer() ||
-                     (s.shadow.size() == v.size() &&
-                      std::memcmp(s.shadow.data(), v.data(), v.size() * sizeof(double)) == 0));
+                     (s.shadow.size() == v.size() && same_bytes(s.shadow.data(), v.data(), v.size() * sizeof(double))));
   if (!same) {
     s.key = nullptr;
     check(ebic_matrix_upload_f64(s.ctx, v.data(), m.rows(), m.cols(), 0, EBIC_STORE_AUTO, nullptr),
@@ -100,7 +214,10 @@ ebic_ctx* bind(const ExpressionMatrix& m) {
     s.key = v.data();
     s.rows = m.rows();
     s.cols = m.cols();
-    if (!trust_pointer()) s.shadow = v;
+    if (!trust_pointer()) {
+      s.shadow.resize(v.size());
+      copy_bytes(s.shadow.data(), v.data(), v.size() * sizeof(double));
+    }
   }
   return s.ctx;
 }

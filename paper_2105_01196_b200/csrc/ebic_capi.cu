@@ -206,6 +206,7 @@ struct ebic_ctx {
   int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (TMA warps up to 256 slices; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
+  bool pdl = true;         // programmatic dependent launch of the count kernels (EBIC_PDL=0 disables)
   // one-time build costs of the last (matrix, approx) preparation
   // (ebic_matrix_build_info): events around the plane and index kernels, host
   // clock around the index allocation (cudaMalloc is synchronous)
@@ -327,6 +328,23 @@ int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
   ctx->plane_valid = true;
   ctx->plane_approx = approx;
   return EBIC_OK;
+}
+
+// Launch with the programmatic-stream-serialization attribute (PDL) when `pdl`.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 // Raise a kernel's dynamic shared-memory limit to the opt-in maximum, once per
@@ -527,10 +545,12 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
       const uint64_t per_sm = (uint64_t)resident_ctas(reinterpret_cast<const void*>(kern), ebic::kTmaWarps * 32, smem);
       const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + ebic::kTmaWarps - 1) / ebic::kTmaWarps,
                                                          std::max<uint64_t>(1, per_sm) * ctx->n_sms);
-      kern<<<grid, ebic::kTmaWarps * 32, smem, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
-                                                   (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand,
-                                                   (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,
-                                                   ctx->ld / 32);
+      // programmatic dependent launch (ebic_table.cuh pdl_trigger / pdl_wait):
+      // back-to-back batches overlap one kernel's tail with the next one's start
+      EBIC_CUDA(launch_pdl(kern, dim3(grid), dim3(ebic::kTmaWarps * 32), smem, s, ctx->pdl,
+                           (const uint32_t*)ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
+                           (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out,
+                           err_out ? err_out : ctx->d_err, d_mask, (uint64_t)(ctx->ld / 32)));
       return EBIC_OK;
     };
     auto pickj = [&](auto negc, auto sc) -> int {
@@ -1162,6 +1182,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (ts) ctx->tma_slots = std::max(2, std::min(4, std::atoi(ts)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");
     if (tk) ctx->table_kernel = std::atoi(tk);
+    const char* pd = std::getenv("EBIC_PDL");
+    if (pd) ctx->pdl = std::atoi(pd) != 0;
     const char* xt = std::getenv("EBIC_XCHG_TIMEOUT_MS");
     if (xt && std::atoll(xt) > 0) ctx->xchg_timeout_ns = (uint64_t)std::atoll(xt) * 1000000ull;
     const char* sc = std::getenv("EBIC_PAIR_LAYOUT");

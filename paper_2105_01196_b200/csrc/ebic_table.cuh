@@ -522,6 +522,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                : "memory");
 }
 
+// Programmatic dependent launch (PDL).  The count kernels let the next kernel
+// of their stream launch as soon as they start (their CTAs are persistent, so
+// the next grid's CTAs only fill SM slots as this grid's CTAs retire: the
+// tail of batch k overlaps the start of batch k+1), and wait for the previous
+// grid before their first global store (a back-to-back batch may write the
+// same output buffer).  The count kernels read nothing an earlier count
+// kernel writes; kernels whose output they do read (the index builders, the
+// lazy pair builder) never trigger early, so the count kernel starts after
+// them as usual.  Both instructions are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int J, int S, bool NEG, bool MASK>
 __global__ void __launch_bounds__(kTmaWarps * 32)
 table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
@@ -541,6 +553,14 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
     mbar_init(empty, 32);
   }
   __syncwarp();
+  pdl_trigger();
+  bool dep_done = false;  // griddepcontrol.wait issued (before this warp's first store)
+  auto before_store = [&]() {
+    if (!dep_done) {
+      pdl_wait();
+      dep_done = true;
+    }
+  };
   uint32_t phase = 0, ephase = 0;
   // Persistent warps, software-pipelined over candidates: the next candidate's
   // offsets are loaded at the top of an iteration and its columns once the
@@ -575,6 +595,7 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
     bool badc = lane < L && c_lane >= n_cols;
     for (uint32_t k = b + 32 + lane; k < b + L; k += 32) badc |= __ldg(cols + k) >= n_cols;
     if (__any_sync(kFull, bad_offs || badc)) {
+      before_store();
       if (lane == 0) {
         out[i] = 0;
         *err_out = bad_offs ? 2 : 1;
@@ -582,6 +603,7 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
       break;
     }
     if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
+      before_store();
       if (lane == 0) out[i] = n_rows;
       if (MASK)
         for (uint32_t w = lane; w < mask_wpc; w += 32)
@@ -646,6 +668,7 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
       __syncwarp();
     }
     uint32_t n = 0;
+    before_store();
 #pragma unroll
     for (int u = 0; u < J; ++u) {
       const uint32_t v = u * 32 + lane;

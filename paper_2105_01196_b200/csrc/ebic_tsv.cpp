@@ -9,8 +9,10 @@
 // messages -- the same library call parses every cell, so the values are
 // bit-identical -- but finds the lines and parses the rows on all host
 // threads, straight into page-locked memory that the device store is uploaded
-// from (ebic_matrix_load_tsv).  Row/column labels are not kept: the device path
-// needs only the values.
+// from (ebic_matrix_load_tsv).  Row/column labels are not kept (the device path
+// needs only the values), but they are checked like the ExpressionMatrix the
+// reference parser constructs (matrix.cpp:43-49): a duplicate row label, then
+// a duplicate column label, is an error with the reference's message.
 #include <charconv>
 #include <cmath>
 #include <cstdarg>
@@ -18,7 +20,9 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <string_view>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 #include "ebic.h"
@@ -168,6 +172,45 @@ Error parse_all(const std::string& text, const std::vector<std::pair<size_t, siz
   return Error{};
 }
 
+// ExpressionMatrix::validate's label rules (matrix.cpp:43-49), run after the
+// values parsed (the reference constructs the matrix -- and validates it --
+// only once every cell has parsed, io.cpp:108-109): the first label, in row
+// order, that repeats an earlier one; then the same over the column labels.
+Error check_labels(const std::string& text, const std::vector<std::pair<size_t, size_t>>& lines, const Shape& sh) {
+  Error err;
+  auto dup = [&](const char* what, std::string_view l) {
+    err.code = EBIC_ERR_INVALID_ARGUMENT;
+    err.msg = std::string("ExpressionMatrix: duplicate ") + what + " label '" + std::string(l) + "'";
+    return err;
+  };
+  std::unordered_set<std::string_view> seen;
+  seen.reserve(sh.rows * 2);
+  for (uint64_t r = 0; r < sh.rows; ++r) {
+    const char* b = text.data() + lines[r + 1].first;
+    const char* e = text.data() + lines[r + 1].second;
+    const char* t = static_cast<const char*>(std::memchr(b, '\t', (size_t)(e - b)));
+    if (!seen.insert(std::string_view(b, (size_t)((t ? t : e) - b))).second)
+      return dup("row", std::string_view(b, (size_t)((t ? t : e) - b)));
+  }
+  // header labels (io.cpp:85-90: a leading corner cell is dropped)
+  std::vector<std::string_view> cols;
+  {
+    const char* b = text.data() + lines[0].first;
+    const char* e = text.data() + lines[0].second;
+    for (const char* p = b;;) {
+      const char* t = static_cast<const char*>(std::memchr(p, '\t', (size_t)(e - p)));
+      cols.emplace_back(p, (size_t)((t ? t : e) - p));
+      if (!t) break;
+      p = t + 1;
+    }
+    if (cols.size() == sh.cols + 1) cols.erase(cols.begin());
+  }
+  seen.clear();
+  for (const auto& l : cols)
+    if (!seen.insert(l).second) return dup("column", l);
+  return err;
+}
+
 int clamp_threads(int n) {
   if (n <= 0) n = (int)std::thread::hardware_concurrency();
   return n < 1 ? 1 : (n > 256 ? 256 : n);
@@ -195,6 +238,8 @@ extern "C" int ebic_tsv_read(const char* path, int n_threads, double* values_out
   if (!values_out || cap < sh.rows * sh.cols)
     return ebic_internal_fail(EBIC_ERR_CAPACITY, "values buffer too small for the matrix");
   e = parse_all(text, lines, path, sh, values_out, threads);
+  if (e.code) return ebic_internal_fail(e.code, e.msg.c_str());
+  e = check_labels(text, lines, sh);
   if (e.code) return ebic_internal_fail(e.code, e.msg.c_str());
   return EBIC_OK;
 }

@@ -771,3 +771,44 @@ def test_index_allocation_kept_across_uploads(evaluator):
             want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
             np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
         assert evaluator.index_info()[1]
+
+
+@pytest.mark.parametrize("R", [5000, 20000, 70000])
+@pytest.mark.parametrize("neg", [False, True])
+def test_back_to_back_launches_programmatic_dependent(evaluator, R, neg):
+    """Count kernels issued back to back on one stream overlap (programmatic
+    dependent launch: kernel k+1 starts while kernel k drains).  Every launch's
+    counts must still be exact, and a buffer written by several launches must
+    hold the LAST one's counts (kernel k+1 waits for kernel k before storing)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(R)
+    m = rng.standard_normal((R, 300)).astype(np.float32)
+    m[: R // 4] = np.sort(m[: R // 4], axis=1)
+    evaluator.upload(m)
+    tp = TrendParams(0.03, neg)
+    pops = [synth.random_population(3000 + 500 * k, 300, 1 if k == 2 else 2, 7, seed=50 + k) for k in range(4)]
+    want = [oracle.evaluate_population(m, p.cols, p.offsets, 0.03, neg) for p in pops]
+    dev = [(torch.from_numpy(p.cols.view(np.int32)).cuda(), torch.from_numpy(p.offsets.view(np.int32)).cuda())
+           for p in pops]
+    n_max = max(len(p) for p in pops)
+    shared = torch.full((n_max,), -1, dtype=torch.int32, device="cuda")
+    outs = [torch.full((len(pops[i % 4]),), -1, dtype=torch.int32, device="cuda") for i in range(24)]
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for i in range(24):
+        dc, do = dev[i % 4]
+        n = len(pops[i % 4])
+        evaluator.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, outs[i].data_ptr(), tp,
+                                             stream=s.cuda_stream)
+        evaluator.evaluate_population_device(dc.data_ptr(), do.data_ptr(), n, shared.data_ptr(), tp,
+                                             stream=s.cuda_stream)
+    s.synchronize()
+    evaluator.sync()
+    for i in range(24):
+        np.testing.assert_array_equal(outs[i].cpu().numpy().view(np.uint32), want[i % 4], err_msg=f"launch {i}")
+    last = want[23 % 4]
+    got = shared.cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(got[:len(last)], last)
+    # positions past the last population were last written by a longer one
+    longest = max(range(4), key=lambda k: (len(pops[k]), -k))
+    np.testing.assert_array_equal(got[len(last):], want[longest][len(last):])

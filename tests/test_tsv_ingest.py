@@ -69,6 +69,15 @@ CASES = {
     "no_values": "\tc0\nr0\nr1\n",
     "empty_file": "",
     "error_order": "\tc0\tc1\nr0\t1\t2\nr1\tx\t2\nr2\t1\n",
+    # ExpressionMatrix::validate's label rules (matrix.cpp:43-49)
+    "dup_row_label": "\tc0\tc1\nr0\t1\t2\nr1\t3\t4\nr0\t5\t6\n",
+    "dup_col_label": "\tc0\tc0\nr0\t1\t2\nr1\t3\t4\n",
+    "dup_col_label_no_corner": "c1\tc1\nr0\t1\t2\n",
+    "dup_row_before_col": "\tc0\tc0\nr0\t1\t2\nr0\t3\t4\n",
+    "dup_first_repeat_wins": "\tc0\nb\t1\na\t2\na\t3\nb\t4\n",
+    "dup_empty_labels": "\tc0\n\t1\n\t2\n",
+    "parse_error_before_dup": "\tc0\nr0\t1\nr0\tx\n",
+    "corner_equals_label": "c0\tc0\tc1\nr0\t1\t2\n",
 }
 
 
