@@ -707,8 +707,169 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
             "parity_with_gpu": bool(np.array_equal(cpu_counts, gpu_counts[:len(cpu_counts)])),
         }
     line["clocks"] = clocks.summary()
+    line["index"] = ev.index_stats()
+    if world == 1 and args.path == "auto":
+        line["cold_start"] = cold_start(cfg, m, pops[0], tp, local_rank)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    ev.close()
+    return 0
+
+
+def cold_start(cfg, m, pop, tp, device):
+    """First-call latency on a fresh context with the library's default policy
+    (no prepare(): AUTO picks the lazy index when the full one is large),
+    host API with host arrays, then the next calls of the same population."""
+    from paper_2105_01196_b200 import Evaluator
+
+    import torch
+
+    # the first batch's device work alone (device API, CUDA events): the
+    # lazy index builds the population's pair vectors inside the count kernel.
+    # Process-cold (first launch of the lazy kernel in this process: CUDA's
+    # lazy module loading) is measured first on a tiny matrix, then a fresh
+    # matrix in a fresh context (matrix-cold).
+    from paper_2105_01196_b200 import synth
+    from paper_2105_01196_b200._lib import EBIC_PATH_LAZY
+
+    ev = Evaluator(device)
+    try:
+        ev.set_path(EBIC_PATH_LAZY)
+        ev.upload(np.ascontiguousarray(m[:256, :64]))
+        tiny = synth.random_population(64, 64, 3, 5, seed=3)
+        t0 = time.perf_counter()
+        ev.evaluate_population(tiny, tp)
+        process_cold_ms = (time.perf_counter() - t0) * 1e3
+    finally:
+        ev.close()
+    ev = Evaluator(device)
+    try:
+        ev.upload(m)
+        dc = torch.from_numpy(pop.cols.view(np.int32)).cuda(device)
+        do = torch.from_numpy(pop.offsets.view(np.int32)).cuda(device)
+        out = torch.empty(len(pop), dtype=torch.int32, device=f"cuda:{device}")
+        s = torch.cuda.Stream()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        for k in range(3):
+            e[k].record(s)
+            ev.evaluate_population_device(dc.data_ptr(), do.data_ptr(), len(pop), out.data_ptr(), tp,
+                                          stream=s.cuda_stream)
+        e[3].record(s)
+        torch.cuda.synchronize()
+        ev.sync()
+        dev_ms = [e[k].elapsed_time(e[k + 1]) for k in range(3)]
+    finally:
+        ev.close()
+    ev = Evaluator(device)
+    try:
+        t0 = time.perf_counter()
+        ev.upload(m)
+        upload_ms = (time.perf_counter() - t0) * 1e3
+        calls = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            ev.evaluate_population(pop, tp)
+            calls.append((time.perf_counter() - t0) * 1e3)
+        st = ev.index_stats()
+        return {"upload_ms": upload_ms, "first_call_ms": calls[0], "second_call_ms": calls[1],
+                "third_call_ms": calls[2], "device_first_batch_ms": dev_ms[0], "device_next_batches_ms": dev_ms[1:],
+                "process_cold_tiny_call_ms": process_cold_ms,
+                "index": st["mode"], "lazy_vectors": st["lazy_slots_used"],
+                "index_bytes": st["lazy_bytes"] if st["mode"] == "lazy" else st["full_bytes"],
+                "what": "fresh context, upload, then evaluate_population of one population three times through "
+                        "the host API (the first call builds what the default policy needs: with the lazy index "
+                        "only the population's own pair vectors)"}
+    finally:
+        ev.close()
+
+
+# ---------------------------------------------------------------------------
+# config 5: the fitness-kernel microbench sweep (BASELINE configs[4])
+# ---------------------------------------------------------------------------
+SWEEP_L = [2, 3, 4, 5, 8, 12, 16, 24, 32, 50]
+SWEEP_R = [1_000, 4_000, 16_000, 64_000, 256_000, 1_000_000]
+SWEEP_APPROX = [0.0, 0.03]
+SWEEP_COLS = 64
+
+
+def measured_l2():
+    p = REPO / "profiles" / "measured_l2.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["l2_gbs"]), "measured (profiles/measured_l2.json, scripts/microbench/l2_bw.cu)"
+        except Exception:
+            pass
+    return None, None
+
+
+def bench_sweep(args):
+    """One JSON line per (R, approx, L): the index count kernel on an N(0,1)
+    background of R x 64 (datagen.cpp:64-70 shape, float32), exactly-L random
+    distinct columns, P = ceil(1 GiB / (4 L R)) candidates (>= 1 GiB of
+    algorithmic bytes per launch), full pair-trend index.  The fraction is
+    against the L2 read roofline when the whole index fits in L2 (every launch
+    touches nearly all 64 x 63 pairs), else against HBM."""
+    import torch
+
+    from paper_2105_01196_b200 import Evaluator, TrendParams, synth
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    hbm, hbm_src = measured_peak()
+    l2, l2_src = measured_l2()
+    ev = Evaluator(0)
+    stream = torch.cuda.Stream(dev)
+    Ls = [int(x) for x in args.sweep_l.split(",")] if args.sweep_l else SWEEP_L
+    Rs = [int(x) for x in args.sweep_r.split(",")] if args.sweep_r else SWEEP_R
+    for R in Rs:
+        rng = np.random.default_rng(7)
+        m = rng.standard_normal((R, SWEEP_COLS), dtype=np.float32)
+        ev.upload(m)
+        for approx in SWEEP_APPROX:
+            ev.prepare(approx)
+            index_bytes, used = ev.index_info()
+            wp = index_bytes // (4 * SWEEP_COLS ** 2)
+            tp = TrendParams(approx=approx)
+            for L in Ls:
+                if args.sweep_sizing == "algorithmic":  # SURVEY 8(d): 4 L R P >= 1 GiB
+                    P = min(2_000_000, -(-(1 << 30) // (4 * L * R)))
+                else:  # >= 512 MB of pair vectors per launch: a throughput, not a launch-latency, measurement
+                    P = min(2_000_000, -(-(512 << 20) // (4 * wp * (L - 1))))
+                pops = [synth.exact_len_population(P, SWEEP_COLS, L, seed=1000 * L + k) for k in range(2)]
+                d = [(torch.from_numpy(pp.cols.view(np.int32)).to(dev), torch.from_numpy(pp.offsets.view(np.int32)).to(dev))
+                     for pp in pops]
+                out = torch.empty(P, dtype=torch.int32, device=dev)
+                ev.set_stream(stream.cuda_stream)
+                for i in range(3):
+                    ev.evaluate_population_device(d[i % 2][0].data_ptr(), d[i % 2][1].data_ptr(), P, out.data_ptr(), tp,
+                                                  stream=stream.cuda_stream)
+                ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+                ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+                torch.cuda.synchronize()
+                for i in range(args.steps):
+                    ev0[i].record(stream)
+                    ev.evaluate_population_device(d[i % 2][0].data_ptr(), d[i % 2][1].data_ptr(), P, out.data_ptr(), tp,
+                                                  stream=stream.cuda_stream)
+                    ev1[i].record(stream)
+                torch.cuda.synchronize()
+                ev.sync()
+                ev.set_stream(None)
+                ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+                phys = 4.0 * wp * P * (L - 1)
+                alg = 4.0 * L * R * P
+                regime = "l2" if (l2 is not None and index_bytes <= 0.75 * L2_BYTES) else "hbm"
+                peak = l2 if regime == "l2" else hbm
+                line = {"sweep": "c5", "sizing": args.sweep_sizing, "rows": R, "cols": SWEEP_COLS, "L": L,
+                        "approx": approx, "population": P,
+                        "kernel": index_kernel_name(wp, P), "kernel_ms": ms, "evals_per_s": P / (ms / 1e3),
+                        "row_checks_per_s": P * R / (ms / 1e3), "index_bytes": index_bytes, "wp": int(wp),
+                        "physical_bytes": phys, "physical_gbs": phys / (ms / 1e3) / 1e9, "regime": regime,
+                        "peak_gbs": peak, "peak_source": l2_src if regime == "l2" else hbm_src,
+                        "frac": phys / (ms / 1e3) / 1e9 / peak,
+                        "effective_algorithmic_gbs": alg / (ms / 1e3) / 1e9}
+                print(json.dumps(line), flush=True)
+                del d, out
     ev.close()
     return 0
 
@@ -758,8 +919,17 @@ def main():
                     help="pair-trend index budget (default: the library's, 40%% of free HBM)")
     ap.add_argument("--path", choices=["auto", "value", "plane", "table"], default="auto",
                     help="evaluation kernel: rank-plane slab kernel (auto for <= 8192 cols) or float value kernel")
+    ap.add_argument("--sweep", action="store_true",
+                    help="config 5: one JSON line per (rows, approx, L) point of the fitness-kernel microbench sweep")
+    ap.add_argument("--sweep-l", default="", help="comma-separated L values (default: the BASELINE sweep)")
+    ap.add_argument("--sweep-r", default="", help="comma-separated row counts (default: the BASELINE sweep)")
+    ap.add_argument("--sweep-sizing", choices=["physical", "algorithmic"], default="physical",
+                    help="population per point: >= 512 MB of pair vectors per launch (default), or SURVEY 8(d)'s "
+                         ">= 1 GiB of algorithmic bytes (4 L R P), which the index compresses ~32x into 10-30 us launches")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.sweep:
+        return bench_sweep(args)
     env_world = os.environ.get("WORLD_SIZE")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -202,9 +202,13 @@ int ebic_ctx_launch_count(ebic_ctx* ctx, uint64_t* n_out);
 /* Tuning knob for the value-path kernel: rows per CTA slab (0 = auto). */
 int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
 
-/* Evaluation path.  AUTO: the pair-trend index (every consecutive-pair test
- * of the matrix as row bitsets, built once per matrix x approx; C^2 x R/8
- * bytes) when it fits the context's budget, else the rank-plane slab kernels
+/* Evaluation path.  AUTO: a pair-trend index -- the full one (every
+ * consecutive-pair test of the matrix as row bitsets, built once per matrix x
+ * approx; C^2 x R/8 bytes) when it is small (<= 1 GiB), requested
+ * (ebic_matrix_prepare) or paid for (ski rental: once the lazy index has built
+ * half of the C^2 pairs), or else the LAZY one (only the pairs the batches
+ * use, built on first use; <= 32K rows per shard) -- within the context's
+ * budget, else the rank-plane slab kernels
  * whenever the matrix has <= 8192 columns (packed 16-bit rank pairs when a
  * 32-row slab fits in shared memory, else 32-bit plane words), otherwise the
  * value kernel.  TABLE, VALUE, PLANE (slab kernels, no index) and PLANE_U32
@@ -217,7 +221,21 @@ int ebic_ctx_set_slab_rows(ebic_ctx* ctx, uint32_t slab_rows);
 #define EBIC_PATH_PLANE 2
 #define EBIC_PATH_PLANE_U32 3
 #define EBIC_PATH_TABLE 4
+#define EBIC_PATH_LAZY 5
 int ebic_ctx_set_path(ebic_ctx* ctx, int path);
+
+/* Which index served the last counting launch and what it holds.  *mode: 0
+ * none (slab / value kernels), 1 the full pair-trend index, 2 the lazy index
+ * (pair vectors built by the count kernel the first time a candidate needs
+ * them, kept in a pool for later batches; ebic_lazy.cuh).  full_bytes: the
+ * built full index (0 if none); lazy_slots_used / lazy_slots_cap: pair
+ * vectors in the pool as last reported by the device / its capacity;
+ * lazy_bytes: pool + pair map; lazy_built: vectors built lazily over the
+ * matrix's lifetime (the ski-rental count); lazy_resets: times a full pool was
+ * started over.  Any out pointer may be NULL. */
+int ebic_matrix_index_stats(ebic_ctx* ctx, int* mode, uint64_t* full_bytes, uint64_t* lazy_slots_used,
+                            uint64_t* lazy_slots_cap, uint64_t* lazy_bytes, uint64_t* lazy_built,
+                            uint64_t* lazy_resets);
 
 /* Packed-pair layout of the hot kernel: `rows_per_lane_pairs` (1 or 2) 16-bit
  * row pairs per lane and `cands_per_warp` (1, 2 or 4) candidates per warp
@@ -245,9 +263,11 @@ int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use);
  * context's stream).  0 for a step that was not run.  Waits for the builds. */
 int ebic_matrix_build_info(ebic_ctx* ctx, double* alloc_ms, double* plane_ms, double* index_ms);
 
-/* Build (or reuse) the rank plane of the resident matrix for `approx` now,
- * instead of lazily on the first evaluation with that approx.  The plane is a
- * per-(matrix, approx) index: a GA run uses one approx for all generations. */
+/* Build (or reuse) the full pair-trend index of the resident matrix for
+ * `approx` now (if it fits the budget; else the rank plane the slab kernels
+ * use), instead of choosing an index on the first evaluation with that approx.
+ * Both are per-(matrix, approx): a GA run uses one approx for all
+ * generations. */
 int ebic_matrix_prepare(ebic_ctx* ctx, double approx);
 
 /* ---- row-sharded step: count reduction over peer memory -----------------

@@ -84,6 +84,19 @@ int main(int argc, char** argv) {
     else if (k == "--warm") warm = std::atoi(v) != 0;
     else if (k == "--engine") engine = v;
     else if (k == "--jobs") jobs = std::atoi(v);
+    // non-default GA parameters (evolution.hpp:20-39)
+    else if (k == "--overlap") p.overlap_threshold = std::strtod(v, nullptr);
+    else if (k == "--tournament") p.tournament_size = std::strtoull(v, nullptr, 10);
+    else if (k == "--biclusters") p.num_biclusters = std::strtoull(v, nullptr, 10);
+    else if (k == "--elite") p.elite_count = std::strtoull(v, nullptr, 10);
+    else if (k == "--penalty") p.penalty_base = std::strtod(v, nullptr);
+    else if (k == "--weights") {  // five comma-separated operator weights
+      char* e = const_cast<char*>(v);
+      for (double& w : p.operator_weights) {
+        w = std::strtod(e, &e);
+        if (*e == ',') ++e;
+      }
+    }
     else {
       std::fprintf(stderr, "unknown option %s\n", k.c_str());
       return 2;

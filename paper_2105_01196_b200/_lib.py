@@ -54,6 +54,7 @@ SIGNATURES = {
     "ebic_ctx_launch_count": (C.c_int, [_vp, _u64p]),
     "ebic_ctx_set_slab_rows": (C.c_int, [_vp, C.c_uint32]),
     "ebic_ctx_set_path": (C.c_int, [_vp, C.c_int]),
+    "ebic_matrix_index_stats": (C.c_int, [_vp, C.POINTER(C.c_int)] + [C.POINTER(C.c_uint64)] * 6),
     "ebic_ctx_set_pair_layout": (C.c_int, [_vp, C.c_int, C.c_int]),
     "ebic_ctx_set_table_budget": (C.c_int, [_vp, C.c_uint64]),
     "ebic_matrix_index_info": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
@@ -78,6 +79,7 @@ EBIC_PATH_VALUE = 1
 EBIC_PATH_PLANE = 2
 EBIC_PATH_PLANE_U32 = 3
 EBIC_PATH_TABLE = 4
+EBIC_PATH_LAZY = 5
 EBIC_IPC_HANDLE_BYTES = 64
 
 

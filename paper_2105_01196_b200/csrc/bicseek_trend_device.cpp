@@ -16,26 +16,30 @@
 //
 // Device matrix cache: the reference passes the matrix by const& on every
 // call (trend.hpp:43-45).  The first call uploads it (float32 store when every
-// value is float32-representable, else float64 -- bit-exact either way); later
-// calls reuse the resident copy when the pointer, shape AND contents match
-// (contents are compared against a host shadow copy, so a matrix mutated in
-// place, or a different matrix that reuses a freed buffer, is never mistaken
-// for the cached one).  The comparison -- and the shadow copy at upload --
-// runs on a persistent pool of host threads in 4-MB chunks with an early exit
-// (HostPool below): 160 MB at 20k x 1000 is a few milliseconds on 16 cores
-// instead of a single-threaded memcmp of the whole matrix per call.
-// EBIC_SHIM_TRUST_POINTER=1 skips the content comparison for very large
-// matrices whose identity the caller guarantees (e.g. one run());
-// EBIC_SHIM_THREADS=<n> sizes the pool (default: all hardware threads).
-// EBIC_DEVICE=<n> pins the CUDA device; by default each thread's context goes
-// to the next visible device round-robin.  State is thread_local, so
-// concurrent run()s on different threads (bench.cpp:103-121) get independent
-// contexts and streams -- on different GPUs when there are several.
+// value is float32-representable, else float64 -- bit-exact either way) and
+// keeps a host shadow copy.  A later call reuses the resident copy when the
+// pointer and shape match AND the values the call depends on are identical to
+// the shadow: a call reads only the columns of its chromosomes, and every
+// device structure derived from the matrix (rank plane, pair-trend index,
+// lazy pair vectors) answers a pair test from the two columns' own values, so
+// unchanged referenced columns give the reference's result even if some other
+// column was mutated in place.  So:
+//   row_supports       -- compares the candidate's L values of that row;
+//   supporting_rows    -- compares the candidate's columns over all rows (a
+//                         strided compare of L x R values, not the matrix);
+//   evaluate_population-- compares the columns the population references, or
+//                         the whole matrix when it references most of them.
+// Any difference re-uploads the whole matrix and refreshes the shadow.  The
+// compares run on a persistent pool of host threads (HostPool) with an early
+// exit.  EBIC_SHIM_TRUST_POINTER=1 skips them for callers that guarantee the
+// matrix is immutable; EBIC_SHIM_THREADS=<n> sizes the pool (default: all
+// hardware threads).
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
+#include <climits>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -200,13 +204,54 @@ int pick_device() {
   return static_cast<int>(next.fetch_add(1) % static_cast<unsigned>(n));
 }
 
-ebic_ctx* bind(const ExpressionMatrix& m) {
+// Are the values at `cols` (all rows) identical to the shadow?  Strided
+// compare over row blocks on the pool.
+bool same_columns(const double* a, const double* b, std::size_t rows, std::size_t n_cols,
+                  const std::vector<uint32_t>& cols) {
+  std::atomic<bool> differs{false};
+  const std::size_t block = std::max<std::size_t>(1, (256u << 10) / std::max<std::size_t>(1, cols.size() * 64));
+  HostPool::get().run(
+      rows, block,
+      [&](std::size_t r0, std::size_t r1) {
+        for (std::size_t r = r0; r < r1; ++r) {
+          const double* ra = a + r * n_cols;
+          const double* rb = b + r * n_cols;
+          for (uint32_t c : cols)
+            if (std::memcmp(ra + c, rb + c, sizeof(double)) != 0) {
+              differs.store(true);
+              return;
+            }
+        }
+      },
+      &differs);
+  return !differs.load();
+}
+
+// What a call depends on: every value (nullptr), some columns, or one row's cells.
+struct Deps {
+  const std::vector<uint32_t>* cols = nullptr;  // distinct columns referenced (nullptr: the whole matrix)
+  std::size_t row = SIZE_MAX;                   // row_supports: only this row's cells of `cols`
+};
+
+bool unchanged(const DeviceState& s, const std::vector<double>& v, std::size_t n_cols, const Deps& d) {
+  if (s.shadow.size() != v.size()) return false;
+  if (d.cols && d.row != SIZE_MAX) {
+    for (uint32_t c : *d.cols)
+      if (std::memcmp(&s.shadow[d.row * n_cols + c], &v[d.row * n_cols + c], sizeof(double)) != 0) return false;
+    return true;
+  }
+  // a strided compare touches a cache line per value: cheaper than the whole
+  // matrix only for a small fraction of the columns
+  if (d.cols && d.cols->size() * 8 < n_cols) return same_columns(s.shadow.data(), v.data(), v.size() / n_cols, n_cols, *d.cols);
+  return same_bytes(s.shadow.data(), v.data(), v.size() * sizeof(double));
+}
+
+ebic_ctx* bind(const ExpressionMatrix& m, const Deps& deps = Deps{}) {
   DeviceState& s = g_dev;
   if (!s.ctx) check(ebic_ctx_create(pick_device(), &s.ctx), "context");
   const std::vector<double>& v = m.values();
   const bool same = s.key == v.data() && s.rows == m.rows() && s.cols == m.cols() &&
-                    (trust_pointer() ||
-                     (s.shadow.size() == v.size() && same_bytes(s.shadow.data(), v.data(), v.size() * sizeof(double))));
+                    (trust_pointer() || unchanged(s, v, m.cols(), deps));
   if (!same) {
     s.key = nullptr;
     check(ebic_matrix_upload_f64(s.ctx, v.data(), m.rows(), m.cols(), 0, EBIC_STORE_AUTO, nullptr),
@@ -220,6 +265,18 @@ ebic_ctx* bind(const ExpressionMatrix& m) {
     }
   }
   return s.ctx;
+}
+
+// Distinct columns of one or more chromosomes (indices already range-checked).
+std::vector<uint32_t> distinct_columns(const std::vector<uint32_t>& cols, std::size_t n_cols) {
+  std::vector<uint32_t> out;
+  std::vector<unsigned char> seen(n_cols, 0);
+  for (uint32_t c : cols)
+    if (!seen[c]) {
+      seen[c] = 1;
+      out.push_back(c);
+    }
+  return out;
 }
 
 std::vector<uint32_t> to_u32(const std::vector<std::size_t>& cols, std::size_t n_cols) {
@@ -237,8 +294,11 @@ std::vector<uint32_t> to_u32(const std::vector<std::size_t>& cols, std::size_t n
 bool row_supports(const ExpressionMatrix& m, std::size_t row, const Chromosome& c,
                   const TrendParams& p) {
   if (row >= m.rows()) throw std::out_of_range("row_supports: row out of range");
-  ebic_ctx* ctx = bind(m);
   const std::vector<uint32_t> cols = to_u32(c.columns, m.cols());
+  Deps deps;
+  deps.cols = &cols;
+  deps.row = row;
+  ebic_ctx* ctx = bind(m, deps);
   int out = 0;
   check(ebic_row_supports(ctx, row, cols.data(), static_cast<uint32_t>(cols.size()), p.approx,
                           p.negative_trends ? 1 : 0, &out),
@@ -249,8 +309,11 @@ bool row_supports(const ExpressionMatrix& m, std::size_t row, const Chromosome& 
 std::vector<std::size_t> supporting_rows(const ExpressionMatrix& m, const Chromosome& c,
                                          const TrendParams& p) {
   if (m.rows() == 0) return {};
-  ebic_ctx* ctx = bind(m);
   const std::vector<uint32_t> cols = to_u32(c.columns, m.cols());
+  const std::vector<uint32_t> used = distinct_columns(cols, m.cols());
+  Deps deps;
+  deps.cols = &used;
+  ebic_ctx* ctx = bind(m, deps);
   std::vector<uint32_t> rows(m.rows());
   uint64_t n = 0;
   check(ebic_support_rows(ctx, cols.data(), static_cast<uint32_t>(cols.size()), p.approx,
@@ -266,7 +329,6 @@ std::vector<std::size_t> evaluate_population(const ExpressionMatrix& m,
   // the device grid replaces it, so it is accepted and ignored.
   std::vector<std::size_t> counts(pop.size(), 0);
   if (pop.empty() || m.rows() == 0) return counts;
-  ebic_ctx* ctx = bind(m);
   std::vector<uint32_t> cols, offs;
   offs.reserve(pop.size() + 1);
   offs.push_back(0);
@@ -278,6 +340,10 @@ std::vector<std::size_t> evaluate_population(const ExpressionMatrix& m,
     }
     offs.push_back(static_cast<uint32_t>(cols.size()));
   }
+  const std::vector<uint32_t> used = distinct_columns(cols, m.cols());
+  Deps deps;
+  deps.cols = &used;
+  ebic_ctx* ctx = bind(m, deps);
   std::vector<uint32_t> out(pop.size());
   check(ebic_eval_counts(ctx, cols.data(), offs.data(), pop.size(), p.approx,
                          p.negative_trends ? 1 : 0, out.data()),

@@ -195,6 +195,24 @@ struct ebic_ctx {
   double table_approx = 0.0;
   uint64_t table_budget = 0;
   uint64_t table_budget_user = 0;  // 0 = the default fraction
+  bool full_requested = false;      // ebic_matrix_prepare asked for the full index
+  // lazy pair-trend index (ebic_lazy.cuh), per matrix x approx: built pair by
+  // pair inside the count kernel, kept in a pool that grows (stream-ordered
+  // allocations) up to the budget and starts over when full
+  uint32_t* d_lmap = nullptr;       // C x C slot per ordered pair
+  uint32_t* d_lpool = nullptr;      // lcap x wp words
+  uint32_t* d_lcount = nullptr;     // slots handed out (device)
+  uint64_t lcap = 0;                // pool capacity (slots)
+  HostBuf<uint32_t> h_lmirror;      // page-locked, mapped: {count at a lazy kernel's start, its batch sequence}
+  uint32_t* h_lmirror_dev = nullptr;
+  bool lazy_valid = false;
+  double lazy_approx = 0.0;
+  uint32_t lazy_seq = 0, lazy_epoch_seq = 1;  // batch sequence; first batch of the current map epoch
+  std::vector<std::pair<uint32_t, uint64_t>> lazy_inflight;  // (seq, worst-case new pairs) not yet seen by the mirror
+  uint64_t lazy_built = 0;          // slots filled over all epochs of this (matrix, approx) (ski-rental rent)
+  uint64_t lazy_epoch_seen = 0;     // slots of the current epoch already added to lazy_built
+  uint64_t lazy_resets = 0;
+  int index_mode = 0;               // index used by the last counting launch (IndexMode)
   double plane_approx = 0.0;
   int path = EBIC_PATH_AUTO;
   int n_sms = 148;
@@ -480,25 +498,168 @@ int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
   return EBIC_OK;
 }
 
-// Use the index for this evaluation?  Builds it on first use; false if it is
-// not allowed or cannot be allocated.
-int use_table(ebic_ctx* ctx, double approx, cudaStream_t s, bool* yes) {
-  *yes = false;
-  if (!table_allowed(ctx)) {
-    if (ctx->path == EBIC_PATH_TABLE)
-      return fail(EBIC_ERR_INVALID_ARGUMENT, "pair-trend index unavailable for this matrix (%llu columns)",
-                  (unsigned long long)ctx->n_cols);
+// ---- index policy: full pair-trend index, lazy index, or none ---------------
+enum IndexMode { kIndexNone = 0, kIndexFull = 1, kIndexLazy = 2 };
+constexpr uint64_t kLazyMaxCols = 8192;              // map of C^2 slots <= 256 MB
+constexpr uint64_t kSmallFullIndex = 1ull << 30;     // a full index this small is built outright (ms)
+constexpr double kLazyRentFrac = 0.5;                // ski rental: buy the full index once this share of
+                                                     // the C^2 pairs has been built lazily
+
+// The lazy index runs in the TMA kernel (vectors of <= 256 uint4 slices, i.e.
+// <= 32K rows per shard).
+bool lazy_allowed(const ebic_ctx* ctx) {
+  if (!(ctx->path == EBIC_PATH_AUTO || ctx->path == EBIC_PATH_LAZY)) return false;
+  const uint64_t C = ctx->n_cols;
+  return C >= 1 && C <= kLazyMaxCols && table_wp(ctx) / 4 <= 256 && ctx->table_kernel != 1 && ctx->table_kernel != 2;
+}
+
+uint64_t lazy_map_bytes(const ebic_ctx* ctx) { return ctx->n_cols * ctx->n_cols * sizeof(uint32_t); }
+
+void lazy_release(ebic_ctx* ctx, cudaStream_t s) {
+  if (ctx->d_lpool) cudaFreeAsync(ctx->d_lpool, s);
+  ctx->d_lpool = nullptr;
+  ctx->lcap = 0;
+  ctx->lazy_valid = false;
+  ctx->lazy_inflight.clear();
+}
+
+// Start a new map epoch (first use, new approx, or a full pool): every pair
+// is unbuilt again.  Stream-ordered, so in-flight batches keep their vectors.
+int lazy_new_epoch(ebic_ctx* ctx, cudaStream_t s) {
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_lmap, 0xFF, lazy_map_bytes(ctx), s));
+  EBIC_CUDA(cudaMemsetAsync(ctx->d_lcount, 0, sizeof(uint32_t), s));
+  ctx->lazy_epoch_seq = ctx->lazy_seq + 1;
+  ctx->lazy_epoch_seen = 0;
+  ctx->lazy_inflight.clear();
+  return EBIC_OK;
+}
+
+// Make room for a batch that may need `worst` new vectors, without a host
+// sync: the mirror tells how full the pool was when some earlier batch
+// started; every batch issued since may have added its worst case.  Grows the
+// pool (cudaMallocAsync + copy + cudaFreeAsync on the stream) up to the
+// budget, or starts a new epoch when it cannot grow.  An underestimate is
+// still exact: a warp that finds no free slot builds a private copy.
+int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, ebic::LazyArgs* la) {
+  const uint64_t vec_bytes = table_wp(ctx) * sizeof(uint32_t);
+  if (!ctx->d_lmap) {
+    EBIC_CUDA(cudaMalloc(&ctx->d_lmap, lazy_map_bytes(ctx)));
+    ctx->lazy_valid = false;
+  }
+  if (!ctx->d_lcount) EBIC_CUDA(cudaMalloc(&ctx->d_lcount, sizeof(uint32_t)));
+  if (!ctx->h_lmirror.p) {
+    EBIC_TRY(ensure(ctx->h_lmirror, 2));
+    ctx->h_lmirror.p[0] = ctx->h_lmirror.p[1] = 0;
+    ctx->h_lmirror_dev = static_cast<uint32_t*>(dev_alias(ctx->h_lmirror.p));
+  }
+  if (!ctx->lazy_valid || std::memcmp(&ctx->lazy_approx, &approx, sizeof(double)) != 0) {
+    EBIC_TRY(lazy_new_epoch(ctx, s));
+    ctx->lazy_valid = true;
+    ctx->lazy_approx = approx;
+    ctx->lazy_built = 0;
+  }
+  // lagged fill of the pool
+  const uint32_t m_count = *(volatile uint32_t*)&ctx->h_lmirror.p[0];
+  const uint32_t m_seq = *(volatile uint32_t*)&ctx->h_lmirror.p[1];
+  uint64_t used = 0;
+  if (m_seq >= ctx->lazy_epoch_seq && m_seq <= ctx->lazy_seq) {
+    used = std::min<uint64_t>(m_count, ctx->lcap);
+    if (used > ctx->lazy_epoch_seen) {
+      ctx->lazy_built += used - ctx->lazy_epoch_seen;
+      ctx->lazy_epoch_seen = used;
+    }
+    auto& f = ctx->lazy_inflight;
+    f.erase(std::remove_if(f.begin(), f.end(), [&](const std::pair<uint32_t, uint64_t>& x) { return x.first < m_seq; }),
+            f.end());
+  }
+  uint64_t pending = 0;
+  for (const auto& x : ctx->lazy_inflight) pending += x.second;
+  const uint64_t c2 = ctx->n_cols * ctx->n_cols;
+  const uint64_t budget = ctx->table_budget > lazy_map_bytes(ctx) ? ctx->table_budget - lazy_map_bytes(ctx) : 0;
+  const uint64_t max_slots = std::max<uint64_t>(1, std::min<uint64_t>({c2, budget / vec_bytes, 0x7fffffffull}));
+  const uint64_t need_raw = used + pending + worst;
+  const uint64_t need = std::min<uint64_t>(need_raw, max_slots);
+  if (need_raw > ctx->lcap) {
+    if (ctx->lcap < max_slots) {
+      // room for ~3 batches of this size: the mirror lags by a batch or two,
+      // so a pool sized for one batch would grow again on the next call
+      const uint64_t cap = std::min<uint64_t>(max_slots, std::max<uint64_t>({need + 2 * worst, 2 * ctx->lcap, 4096}));
+      uint32_t* np = nullptr;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&np), cap * vec_bytes, s) != cudaSuccess) {
+        cudaGetLastError();  // cannot grow: stay at this capacity (warps build private copies)
+      } else {
+        if (ctx->d_lpool) {
+          EBIC_CUDA(cudaMemcpyAsync(np, ctx->d_lpool, ctx->lcap * vec_bytes, cudaMemcpyDeviceToDevice, s));
+          EBIC_CUDA(cudaFreeAsync(ctx->d_lpool, s));
+        }
+        ctx->d_lpool = np;
+        ctx->lcap = cap;
+      }
+    } else if (ctx->lcap < c2 && used + pending >= ctx->lcap / 2) {
+      ++ctx->lazy_resets;  // the pool cannot grow and is filling up: start over (a pool of all C^2 never is)
+      EBIC_TRY(lazy_new_epoch(ctx, s));
+    }
+  }
+  const uint32_t seq = ++ctx->lazy_seq;
+  ctx->lazy_inflight.emplace_back(seq, worst);
+  if (ctx->lazy_inflight.size() > 256) ctx->lazy_inflight.erase(ctx->lazy_inflight.begin());
+  la->map = ctx->d_lmap;
+  la->pool = ctx->d_lpool;
+  la->count = ctx->d_lcount;
+  la->count_out = ctx->h_lmirror_dev;
+  la->cap = (uint32_t)ctx->lcap;
+  la->seq = seq;
+  la->mat = ctx->d_mat;
+  la->ld = ctx->ld;
+  la->f64 = ctx->store == EBIC_STORE_F64 ? 1 : 0;
+  la->approx = approx;
+  return EBIC_OK;
+}
+
+// Which index serves this evaluation (IndexMode in *mode; kIndexNone: the
+// slab / value kernels).  The full index is built on first use when the path
+// forces it, when it is small (<= 1 GiB: milliseconds), when
+// ebic_matrix_prepare asked for it, when the lazy index cannot serve the
+// matrix, or -- ski rental -- once the lazy index has built kLazyRentFrac of
+// all C^2 pairs (the work already spent is then about what the full build
+// costs, and every later batch saves the lazy lookups); always within the
+// budget.  Otherwise the lazy index (ebic_lazy.cuh) builds just the pairs the
+// batches use.  `worst` bounds the new pairs this batch can need.
+int use_index(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, int* mode, ebic::LazyArgs* la) {
+  *mode = kIndexNone;
+  if (ctx->path == EBIC_PATH_TABLE && !table_allowed(ctx))
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "pair-trend index unavailable for this matrix (%llu columns)",
+                (unsigned long long)ctx->n_cols);
+  const bool lazy_ok = lazy_allowed(ctx);
+  if (table_allowed(ctx)) {
+    const bool have = ctx->table_valid && std::memcmp(&ctx->table_approx, &approx, sizeof(double)) == 0;
+    const bool rent_paid = ctx->lazy_valid && std::memcmp(&ctx->lazy_approx, &approx, sizeof(double)) == 0 &&
+                           (double)ctx->lazy_built >= kLazyRentFrac * (double)(ctx->n_cols * ctx->n_cols);
+    if (have || ctx->path == EBIC_PATH_TABLE || !lazy_ok || table_bytes(ctx) <= kSmallFullIndex ||
+        ctx->full_requested || rent_paid) {
+      const int st = ensure_table(ctx, approx, s);
+      if (st == EBIC_OK) {
+        if (ctx->d_lpool) lazy_release(ctx, s);  // the full index replaces the pool
+        *mode = kIndexFull;
+        ctx->index_mode = kIndexFull;
+        return EBIC_OK;
+      }
+      if (st != kTableNoMemory) return st;
+      if (ctx->path == EBIC_PATH_TABLE)
+        return fail(EBIC_ERR_CUDA, "pair-trend index (%llu bytes) does not fit in device memory",
+                    (unsigned long long)table_bytes(ctx));
+    }
+  }
+  if (lazy_ok && !(ctx->d_mat && ctx->n_rows == 0)) {
+    EBIC_TRY(lazy_reserve(ctx, approx, worst, s, la));
+    *mode = kIndexLazy;
+    ctx->index_mode = kIndexLazy;
     return EBIC_OK;
   }
-  const int st = ensure_table(ctx, approx, s);
-  if (st == kTableNoMemory) {
-    if (ctx->path == EBIC_PATH_TABLE)
-      return fail(EBIC_ERR_CUDA, "pair-trend index (%llu bytes) does not fit in device memory",
-                  (unsigned long long)table_bytes(ctx));
-    return EBIC_OK;
-  }
-  EBIC_TRY(st);
-  *yes = true;
+  if (ctx->path == EBIC_PATH_LAZY)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "lazy pair-trend index unavailable for this matrix (%llu x %llu)",
+                (unsigned long long)ctx->n_rows, (unsigned long long)ctx->n_cols);
+  ctx->index_mode = kIndexNone;
   return EBIC_OK;
 }
 
@@ -507,14 +668,28 @@ bool tma_table_kernel(const ebic_ctx* ctx) {
   return table_wp(ctx) / 4 <= 256 && (ctx->table_kernel == 0 || ctx->table_kernel == 3);
 }
 
+// The index one counting launch uses (use_index), decided once per launch.
+struct IndexPlan {
+  int mode = kIndexNone;
+  ebic::LazyArgs la{};
+};
+
+// Worst-case new pair vectors of a batch (n_idx unknown on the device API:
+// an estimate; an underestimate only costs private builds, never exactness).
+uint64_t worst_pairs(uint64_t n_cand, uint64_t n_idx, int neg) {
+  const uint64_t pairs = n_idx != 0xffffffffull && n_idx >= n_cand ? n_idx - n_cand : 4 * n_cand;
+  return pairs * (neg ? 2 : 1);
+}
+
 // Counts WRITTEN to out (any device-accessible pointer), optional row masks.
 // n_idx bounds the offsets (checked on device).
 template <bool MASK>
 int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand, uint64_t n_idx,
-                 int neg, uint32_t* out, int* err_out, uint32_t* d_mask, cudaStream_t s) {
+                 int neg, uint32_t* out, int* err_out, uint32_t* d_mask, cudaStream_t s, const IndexPlan& plan) {
   const uint32_t nv = (uint32_t)(table_wp(ctx) / 4);
+  const bool lazy = plan.mode == kIndexLazy;
   const bool many = n_cand >= (uint64_t)ctx->n_sms * 32;  // enough warps to fill every SM
-  if (nv > 256 && (ctx->table_kernel == 1 || (ctx->table_kernel == 0 && many))) {
+  if (!lazy && nv > 256 && (ctx->table_kernel == 1 || (ctx->table_kernel == 0 && many))) {
     // long vectors, many candidates: a warp per candidate sweeping its vectors
     // in passes of 256 slices (no block barriers; measured 0.44 vs 0.67 ms for
     // the CTA kernel at 200k x 2000, P = 32768).  Few candidates (C5: 1024)
@@ -531,12 +706,13 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     EBIC_CUDA(cudaGetLastError());
     return EBIC_OK;
   }
-  if (tma_table_kernel(ctx)) {
+  if (lazy || tma_table_kernel(ctx)) {
     // short vectors (the default): through the TMA engine -- bulk copies of
     // whole pair vectors into per-warp shared-memory slots, mbarrier
-    // completion (27.5 vs 31 us for the register-load warp kernel at C3, ncu)
+    // completion (27.5 vs 31 us for the register-load warp kernel at C3, ncu).
+    // The lazy index always runs here (S = 2).
     const uint32_t J = (nv + 31) / 32;
-    const int S = ctx->tma_slots;
+    const int S = lazy ? 2 : ctx->tma_slots;
     const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
     auto go = [&](auto kern) -> int {
       EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(kern), ctx));
@@ -550,7 +726,7 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
       EBIC_CUDA(launch_pdl(kern, dim3(grid), dim3(ebic::kTmaWarps * 32), smem, s, ctx->pdl,
                            (const uint32_t*)ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
                            (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out,
-                           err_out ? err_out : ctx->d_err, d_mask, (uint64_t)(ctx->ld / 32)));
+                           err_out ? err_out : ctx->d_err, d_mask, (uint64_t)(ctx->ld / 32), plan.la));
       return EBIC_OK;
     };
     auto pickj = [&](auto negc, auto sc) -> int {
@@ -567,8 +743,22 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
         default: return go(ebic::table_count_tma_kernel<8, SS, N, MASK>);
       }
     };
+    auto pickj_lazy = [&](auto negc) -> int {
+      constexpr bool N = decltype(negc)::value;
+      switch (J) {
+        case 1: return go(ebic::table_count_tma_kernel<1, 2, N, MASK, true>);
+        case 2: return go(ebic::table_count_tma_kernel<2, 2, N, MASK, true>);
+        case 3: return go(ebic::table_count_tma_kernel<3, 2, N, MASK, true>);
+        case 4: return go(ebic::table_count_tma_kernel<4, 2, N, MASK, true>);
+        case 5: return go(ebic::table_count_tma_kernel<5, 2, N, MASK, true>);
+        case 6: return go(ebic::table_count_tma_kernel<6, 2, N, MASK, true>);
+        case 7: return go(ebic::table_count_tma_kernel<7, 2, N, MASK, true>);
+        default: return go(ebic::table_count_tma_kernel<8, 2, N, MASK, true>);
+      }
+    };
     int st;
-    if (S >= 4) st = neg ? pickj(std::true_type{}, std::integral_constant<int, 4>{})
+    if (lazy) st = neg ? pickj_lazy(std::true_type{}) : pickj_lazy(std::false_type{});
+    else if (S >= 4) st = neg ? pickj(std::true_type{}, std::integral_constant<int, 4>{})
                          : pickj(std::false_type{}, std::integral_constant<int, 4>{});
     else if (S == 3) st = neg ? pickj(std::true_type{}, std::integral_constant<int, 3>{})
                               : pickj(std::false_type{}, std::integral_constant<int, 3>{});
@@ -833,17 +1023,20 @@ int launch_slab(ebic_ctx* ctx, const SlabCfg& cfg, const uint32_t* d_cols, const
 
 // Counting launch.  d_counts must be zero: the kernels ADD into it -- except
 // slab_pair_kernel, which writes final counts to po->out (see count_into).
+// `plan_in`: the index decision already taken for this launch (nullptr:
+// decide here).
 template <bool MASK>
 int launch_count(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand,
                  double approx, int neg, uint32_t* d_counts, uint32_t* d_mask, cudaStream_t s,
-                 const PairOut* po = nullptr, uint64_t n_idx = 0xffffffffull) {
+                 const PairOut* po = nullptr, uint64_t n_idx = 0xffffffffull, const IndexPlan* plan_in = nullptr) {
   if (n_cand == 0) return EBIC_OK;
   if (n_cand > 0xffffffffull / 2) return fail(EBIC_ERR_INVALID_ARGUMENT, "too many candidates");
-  bool table = false;
-  EBIC_TRY(use_table(ctx, approx, s, &table));
-  if (table)
+  IndexPlan local;
+  if (!plan_in) EBIC_TRY(use_index(ctx, approx, worst_pairs(n_cand, n_idx, neg), s, &local.mode, &local.la));
+  const IndexPlan& plan = plan_in ? *plan_in : local;
+  if (plan.mode != kIndexNone)
     return launch_table<MASK>(ctx, d_cols, d_offs, n_cand, n_idx, neg, po ? po->out : d_counts,
-                              po ? po->err_out : nullptr, d_mask, s);
+                              po ? po->err_out : nullptr, d_mask, s, plan);
   if (ctx->path != EBIC_PATH_VALUE && ctx->path != EBIC_PATH_TABLE && plane_fits(ctx)) {
     const SlabCfg cfg = choose_slab(ctx, n_cand, MASK);
     if (cfg.ok) {
@@ -890,29 +1083,38 @@ bool pair_path(const ebic_ctx* ctx, uint64_t n_cand) {
   return cfg.ok && cfg.simd && cfg.v2;
 }
 
-// Will the counting launch write its results directly (pair-trend index or
-// slab_pair_kernel)?  Builds the index on first use.
-int direct_path(ebic_ctx* ctx, uint64_t n_cand, double approx, cudaStream_t s, bool* yes) {
-  EBIC_TRY(use_table(ctx, approx, s, yes));
-  if (!*yes) *yes = pair_path(ctx, n_cand);
+// The decisions of one counting launch: which index (built or reserved now),
+// and whether the kernel writes its results directly (an index kernel or
+// slab_pair_kernel) -- then `out` may be the device alias of host memory.
+struct LaunchPlan {
+  IndexPlan index;
+  bool direct = false;
+};
+
+int plan_launch(ebic_ctx* ctx, uint64_t n_cand, uint64_t n_idx, double approx, int neg, cudaStream_t s,
+                LaunchPlan* lp) {
+  EBIC_TRY(use_index(ctx, approx, worst_pairs(n_cand, n_idx, neg), s, &lp->index.mode, &lp->index.la));
+  lp->direct = lp->index.mode != kIndexNone || pair_path(ctx, n_cand);
   return EBIC_OK;
 }
 
 // Evaluate and leave the FINAL counts in `out` and the device error flag in
 // `err_out` (nullptr: ctx->d_err, read by ebic_ctx_sync).  `out` may be host
-// memory (device alias) only when pair_path(ctx, n_cand); `err_out` may be
-// host memory (device alias) always.
+// memory (device alias) only when the plan is direct; `err_out` may be host
+// memory (device alias) always.  `lp_in`: a plan already made for this launch.
 int count_into(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, uint64_t n_cand, double approx,
-               int neg, uint32_t* out, int* err_out, cudaStream_t s, uint64_t n_idx = 0xffffffffull) {
+               int neg, uint32_t* out, int* err_out, cudaStream_t s, uint64_t n_idx = 0xffffffffull,
+               const LaunchPlan* lp_in = nullptr) {
   if (n_cand == 0) return EBIC_OK;
-  bool direct = false;
-  EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
-  if (direct) {
+  LaunchPlan local;
+  if (!lp_in) EBIC_TRY(plan_launch(ctx, n_cand, n_idx, approx, neg, s, &local));
+  const LaunchPlan& lp = lp_in ? *lp_in : local;
+  if (lp.direct) {
     const PairOut po{out, err_out};
-    return launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, nullptr, nullptr, s, &po, n_idx);
+    return launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, nullptr, nullptr, s, &po, n_idx, &lp.index);
   }
   EBIC_CUDA(cudaMemsetAsync(out, 0, n_cand * sizeof(uint32_t), s));
-  EBIC_TRY(launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, out, nullptr, s));
+  EBIC_TRY(launch_count<false>(ctx, d_cols, d_offs, n_cand, approx, neg, out, nullptr, s, nullptr, n_idx, &lp.index));
   if (err_out && err_out != ctx->d_err) {
     EBIC_CUDA(cudaMemcpyAsync(err_out, ctx->d_err, sizeof(int), cudaMemcpyDefault, s));
     EBIC_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(int), s));
@@ -972,6 +1174,13 @@ void drop_matrix(ebic_ctx* ctx, bool keep_index_alloc) {
   }
   ctx->table_valid = ctx->table_failed = false;
   ctx->plane_timed = ctx->index_timed = false;
+  ctx->full_requested = false;
+  if (ctx->d_lpool) lazy_release(ctx, ctx->stream);
+  if (ctx->d_lmap) cudaFree(ctx->d_lmap);
+  ctx->d_lmap = nullptr;
+  ctx->lazy_valid = false;
+  ctx->lazy_built = ctx->lazy_epoch_seen = ctx->lazy_resets = 0;
+  ctx->index_mode = kIndexNone;
   ctx->d_mat = nullptr;
   ctx->store = 0;
   ctx->n_rows = ctx->n_cols = ctx->ld = ctx->row_base = 0;
@@ -1086,6 +1295,13 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
       ctx->table_cap = 0;
     }
   }
+  if (lazy_allowed(ctx)) {  // the lazy index's pair map now, not on the first batch
+    const cudaError_t me = cudaMalloc(&ctx->d_lmap, lazy_map_bytes(ctx));
+    if (me != cudaSuccess) {
+      cudaGetLastError();
+      ctx->d_lmap = nullptr;  // retried (and reported) on first use
+    }
+  }
   if (store_out) *store_out = chosen;
   return EBIC_OK;
 }
@@ -1156,6 +1372,15 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
   }
   for (int i = 0; i < EBIC_MARSHAL_SLOTS && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(&ctx->slots[i].done, cudaEventDisableTiming);
+  // the lazy index's bookkeeping (counter, host-mapped mirror) up front: a
+  // page-locked allocation costs milliseconds, not a cost for the first batch
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_lcount, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_lmirror.p, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) {
+    ctx->h_lmirror.n = 2;
+    ctx->h_lmirror.p[0] = ctx->h_lmirror.p[1] = 0;
+    ctx->h_lmirror_dev = static_cast<uint32_t*>(dev_alias(ctx->h_lmirror.p));
+  }
   if (e != cudaSuccess) {
     ebic_ctx_destroy(ctx);
     return fail(EBIC_ERR_CUDA, "context creation on device %d: %s", device, cudaGetErrorString(e));
@@ -1232,6 +1457,8 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   if (ctx->xchg_stream) cudaStreamDestroy(ctx->xchg_stream);
   for (cudaEvent_t& e : ctx->ev_build)
     if (e) cudaEventDestroy(e);
+  if (ctx->d_lcount) cudaFree(ctx->d_lcount);
+  ctx->h_lmirror.release();
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -1361,15 +1588,15 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
     // the index / pair kernels write the counts and the error flag straight
     // into the slot's page-locked buffers; otherwise device counts + a D2H copy
     const bool mapped = h_counts_dev && h_err_dev;
-    bool direct = false;
-    EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
-    if (mapped && direct) {
+    LaunchPlan lp;
+    EBIC_TRY(plan_launch(ctx, n_cand, n_idx, approx, negative_trends, s, &lp));
+    if (mapped && lp.direct) {
       sl.h_err.p[0] = 0;  // the index kernel only writes on error (the slot is not in flight)
       EBIC_TRY(count_into(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends, h_counts_dev,
-                          h_err_dev, s));
+                          h_err_dev, s, n_idx, &lp));
     } else {
       EBIC_TRY(count_into(ctx, sl.d_cols.p, sl.d_offs.p, n_cand, approx, negative_trends, sl.d_counts.p,
-                          nullptr, s));
+                          nullptr, s, n_idx, &lp));
       EBIC_CUDA(cudaMemcpyAsync(sl.h_counts.p, sl.d_counts.p, n_cand * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, s));
       EBIC_CUDA(cudaMemcpyAsync(sl.h_err.p, ctx->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1430,9 +1657,11 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
     if (!err_dev) return fail(EBIC_ERR_CUDA, "page-locked error flag is not device-mapped");
     ctx->h_err1.p[0] = 0;
     const bool one_copy = offsets + (n_cand + 1) == cols;
-    bool table = false;
-    EBIC_TRY(use_table(ctx, approx, s, &table));
-    const int pieces = (table && n_cand >= 2048) ? ctx->pipeline_pieces : 1;
+    const uint64_t n_idx_h = offsets[n_cand];
+    LaunchPlan lp;
+    EBIC_TRY(plan_launch(ctx, n_cand, n_idx_h, approx, negative_trends, s, &lp));
+    const bool table = lp.index.mode != kIndexNone;  // an index kernel: offsets checked on device
+    const int pieces = (lp.index.mode == kIndexFull && n_cand >= 2048) ? ctx->pipeline_pieces : 1;
     if (pieces > 1) {
       // pair-trend index, pipelined: the population goes over in `pieces`
       // DMAs on the copy stream (offsets + the first columns first) and the
@@ -1477,7 +1706,7 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
       for (int k = 0; k < pieces; ++k) {
         EBIC_CUDA(cudaStreamWaitEvent(s, ctx->piece_ev[k], 0));
         EBIC_TRY(launch_table<false>(ctx, d_cols, d_offs + cb[k], cb[k + 1] - cb[k], n_idx, negative_trends,
-                                     out_dev + cb[k], err_dev, nullptr, s));
+                                     out_dev + cb[k], err_dev, nullptr, s, lp.index));
       }
       EBIC_CUDA(cudaStreamSynchronize(s));
       const int e = *(volatile int*)ctx->h_err1.p;
@@ -1504,8 +1733,6 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
       d_offs = ctx->d_tmp_offs.p;
       d_cols = ctx->d_tmp_cols.p;
     }
-    bool direct = false;
-    EBIC_TRY(direct_path(ctx, n_cand, approx, s, &direct));
     // the index kernel checks every candidate's offsets on device (increasing,
     // within offsets[n_cand]); the other kernels need them checked here
     if (!table && validate_population(ctx, cols, offsets, n_cand, /*check_cols=*/false) != EBIC_OK) {
@@ -1513,11 +1740,12 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
       cudaStreamSynchronize(s);  // the scratch buffers may be reused by the next call
       return fail(EBIC_ERR_INVALID_ARGUMENT, "%s", msg.c_str());
     }
-    if (direct) {
-      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, out_dev, err_dev, s, n_idx));
+    if (lp.direct) {
+      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, out_dev, err_dev, s, n_idx, &lp));
     } else {
       EBIC_TRY(ensure(ctx->d_tmp_counts, n_cand));
-      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, ctx->d_tmp_counts.p, err_dev, s));
+      EBIC_TRY(count_into(ctx, d_cols, d_offs, n_cand, approx, negative_trends, ctx->d_tmp_counts.p, err_dev, s,
+                          n_idx, &lp));
       EBIC_CUDA(cudaMemcpyAsync(counts_out, ctx->d_tmp_counts.p, n_cand * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     }
     EBIC_CUDA(cudaStreamSynchronize(s));
@@ -1736,9 +1964,25 @@ int ebic_matrix_build_info(ebic_ctx* ctx, double* alloc_ms, double* plane_ms, do
   return EBIC_OK;
 }
 
+int ebic_matrix_index_stats(ebic_ctx* ctx, int* mode, uint64_t* full_bytes, uint64_t* lazy_slots_used,
+                            uint64_t* lazy_slots_cap, uint64_t* lazy_bytes, uint64_t* lazy_built,
+                            uint64_t* lazy_resets) {
+  EBIC_TRY(need_matrix(ctx));
+  const uint64_t vec = table_wp(ctx) * sizeof(uint32_t);
+  const uint32_t m_count = ctx->h_lmirror.p ? *(volatile uint32_t*)&ctx->h_lmirror.p[0] : 0;
+  if (mode) *mode = ctx->index_mode;
+  if (full_bytes) *full_bytes = ctx->table_valid ? table_bytes(ctx) : 0;
+  if (lazy_slots_used) *lazy_slots_used = ctx->lazy_valid ? std::min<uint64_t>(m_count, ctx->lcap) : 0;
+  if (lazy_slots_cap) *lazy_slots_cap = ctx->lcap;
+  if (lazy_bytes) *lazy_bytes = ctx->lcap * vec + (ctx->d_lmap ? lazy_map_bytes(ctx) : 0);
+  if (lazy_built) *lazy_built = ctx->lazy_built;
+  if (lazy_resets) *lazy_resets = ctx->lazy_resets;
+  return EBIC_OK;
+}
+
 int ebic_ctx_set_path(ebic_ctx* ctx, int path) {
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
-  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_TABLE) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
+  if (path < EBIC_PATH_AUTO || path > EBIC_PATH_LAZY) return fail(EBIC_ERR_INVALID_ARGUMENT, "bad path %d", path);
   ctx->path = path;
   return EBIC_OK;
 }
@@ -1747,10 +1991,13 @@ int ebic_matrix_prepare(ebic_ctx* ctx, double approx) {
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   EBIC_TRY(set_device(ctx));
-  if (ctx->path == EBIC_PATH_VALUE || !plane_fits(ctx)) return EBIC_OK;
-  EBIC_TRY(ensure_plane(ctx, approx, ctx->stream));
-  bool table = false;
-  EBIC_TRY(use_table(ctx, approx, ctx->stream, &table));
+  if (ctx->path == EBIC_PATH_VALUE) return EBIC_OK;
+  // an explicit request: the full index now if it fits the budget (else the
+  // lazy index, or the rank plane of the slab kernels)
+  ctx->full_requested = true;
+  IndexPlan plan;
+  EBIC_TRY(use_index(ctx, approx, 0, ctx->stream, &plan.mode, &plan.la));
+  if (plan.mode == kIndexNone && plane_fits(ctx)) EBIC_TRY(ensure_plane(ctx, approx, ctx->stream));
   EBIC_CUDA(cudaStreamSynchronize(ctx->stream));
   return EBIC_OK;
 }

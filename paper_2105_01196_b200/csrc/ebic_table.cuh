@@ -23,6 +23,7 @@
 #include <cstdint>
 
 #include "ebic_plane.cuh"
+#include "ebic_lazy.cuh"
 
 namespace ebic {
 
@@ -534,12 +535,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <int J, int S, bool NEG, bool MASK>
+// LAZY: the vectors come from the lazy index (ebic_lazy.cuh) -- the pair's
+// slot is looked up in la.map (for a candidate's first 31 pairs, one lookup
+// per lane, prefetched with the candidate's columns); a ready slot is copied
+// from la.pool by TMA like a full-index vector; a missing one is built by the
+// warp straight into its shared-memory slot (and, if the warp wins the pool
+// slot, written to the pool and published for every later candidate).
+template <int J, int S, bool NEG, bool MASK, bool LAZY = false>
 __global__ void __launch_bounds__(kTmaWarps * 32)
 table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
                        const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
                        uint32_t n_idx, uint32_t* __restrict__ out, int* err_out, uint32_t* __restrict__ mask,
-                       uint64_t mask_wpc) {
+                       uint64_t mask_wpc, LazyArgs la) {
   extern __shared__ __align__(128) unsigned char smem[];  // [warp][S (x2 with NEG)][pair vector]
   __shared__ __align__(8) uint64_t s_bar[kTmaWarps];    // "full": the slots' bulk copies have landed
   __shared__ __align__(8) uint64_t s_empty[kTmaWarps];  // "empty": all 32 lanes are done reading the slots
@@ -548,9 +555,15 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
   const uint32_t nv = wp / 4, slot = wp * 4;  // uint4 / bytes per pair vector
   const uint32_t my = smem_u32(smem) + (uint32_t)warp * NS * slot;
   const uint32_t bar = smem_u32(&s_bar[warp]), empty = smem_u32(&s_empty[warp]);
+  const uint32_t* vec_base = LAZY ? la.pool : table;
   if (lane == 0) {
     mbar_init(bar, 1);
     mbar_init(empty, 32);
+  }
+  if (LAZY && la.count_out && blockIdx.x == 0 && threadIdx.x == 0) {  // the host's lagged view of the pool's fill
+    la.count_out[0] = *(volatile uint32_t*)la.count;
+    __threadfence_system();
+    la.count_out[1] = la.seq;
   }
   __syncwarp();
   pdl_trigger();
@@ -561,6 +574,18 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
       dep_done = true;
     }
   };
+  // LAZY: slots of pair (position lane -> lane + 1) of a candidate, looked up
+  // as soon as its columns are known (clamped: columns are validated later)
+  auto lookup = [&](uint32_t c_l, uint32_t L, uint32_t& sf, uint32_t& sr) {
+    sf = sr = kSlotEmpty;
+    if (!LAZY) return;
+    const uint32_t c_n = __shfl_down_sync(kFull, c_l, 1);
+    if (lane < 31 && lane + 1 < L) {
+      const uint32_t x = min(c_l, n_cols - 1), y = min(c_n, n_cols - 1);
+      sf = lazy_lookup(la, (uint64_t)x * n_cols + y);
+      if (NEG) sr = lazy_lookup(la, (uint64_t)y * n_cols + x);
+    }
+  };
   uint32_t phase = 0, ephase = 0;
   // Persistent warps, software-pipelined over candidates: the next candidate's
   // offsets are loaded at the top of an iteration and its columns once the
@@ -568,16 +593,17 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
   // chain of one candidate overlaps the previous candidate's copies.
   const uint32_t warps = gridDim.x * kTmaWarps;
   uint32_t i = blockIdx.x * kTmaWarps + warp;
-  uint32_t b = 0, e = 0, c_lane = 0;
+  uint32_t b = 0, e = 0, c_lane = 0, sf_lane = kSlotEmpty, sr_lane = kSlotEmpty;
   if (i < n_cand) {
     b = __ldg(offs + i);
     e = __ldg(offs + i + 1);
     const uint32_t L0 = (e > b && e <= n_idx) ? e - b : 0u;
     c_lane = lane < L0 ? __ldg(cols + b + lane) : 0u;
+    lookup(c_lane, L0, sf_lane, sr_lane);
   }
   for (; i < n_cand; i += warps) {
     const uint32_t inext = i + warps;
-    uint32_t bn = 0, en = 0, cn = 0;
+    uint32_t bn = 0, en = 0, cn = 0, sfn = kSlotEmpty, srn = kSlotEmpty;
     bool next_cols = false;
     if (inext < n_cand) {  // in flight while this candidate is processed
       bn = __ldg(offs + inext);
@@ -588,6 +614,7 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
       next_cols = true;
       const uint32_t Ln = (inext < n_cand && en > bn && en <= n_idx) ? en - bn : 0u;
       cn = lane < Ln ? __ldg(cols + bn + lane) : 0u;
+      lookup(cn, Ln, sfn, srn);
     };
     do {  // one candidate; `break` = done with it
     const bool bad_offs = e <= b || e > n_idx;
@@ -626,15 +653,68 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
         const uint32_t k = k0 + q;
         pc[q + 1] = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : (k < L ? __ldg(cols + b + k) : 0u);
       }
+      // vector index of each pair of the group: a*C + b (full index) or the
+      // pool slot (LAZY; kSlotEmpty / busy = build it here)
+      uint32_t vf[S], vr[S];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint32_t k = k0 + q;
+        if (LAZY) {
+          const bool in_lane = k - 1 < 31;
+          const uint32_t x = __shfl_sync(kFull, sf_lane, (k - 1) & 31);
+          const uint32_t y = __shfl_sync(kFull, sr_lane, (k - 1) & 31);
+          vf[q] = in_lane ? x : (k < L ? lazy_lookup(la, (uint64_t)pc[q] * n_cols + pc[q + 1]) : 0u);
+          vr[q] = !NEG ? 0u : in_lane ? y : (k < L ? lazy_lookup(la, (uint64_t)pc[q + 1] * n_cols + pc[q]) : 0u);
+          // one view per warp: lanes loading the same entry while another warp
+          // publishes it could disagree, and the code below is warp-collective
+          vf[q] = __shfl_sync(kFull, vf[q], 0);
+          vr[q] = __shfl_sync(kFull, vr[q], 0);
+        } else {
+          vf[q] = pc[q] * n_cols + pc[q + 1];
+          vr[q] = pc[q + 1] * n_cols + pc[q];
+        }
+      }
       if (lane == 0) {
-        mbar_expect_tx(bar, g * slot * (NEG ? 2u : 1u));
+        uint32_t bytes = 0;
+#pragma unroll
+        for (int q = 0; q < S; ++q)
+          if ((uint32_t)q < g) bytes += (slot_ready(vf[q]) || !LAZY ? slot : 0u) + (NEG && (slot_ready(vr[q]) || !LAZY) ? slot : 0u);
+        if (LAZY) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic writes to the slots
+        mbar_expect_tx(bar, bytes);
 #pragma unroll
         for (int q = 0; q < S; ++q) {
           if ((uint32_t)q < g) {
-            bulk_g2s(my + q * slot, table + ((uint64_t)pc[q] * n_cols + pc[q + 1]) * wp, slot, bar);
-            if (NEG) bulk_g2s(my + (S + q) * slot, table + ((uint64_t)pc[q + 1] * n_cols + pc[q]) * wp, slot, bar);
+            if (!LAZY || slot_ready(vf[q])) bulk_g2s(my + q * slot, vec_base + (uint64_t)vf[q] * wp, slot, bar);
+            if (NEG && (!LAZY || slot_ready(vr[q])))
+              bulk_g2s(my + (S + q) * slot, vec_base + (uint64_t)vr[q] * wp, slot, bar);
           }
         }
+      }
+      if (LAZY) {
+        // vectors not in the pool yet: built by the warp into their slots
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          const bool rev = q >= S;
+          const int qq = rev ? q - S : q;
+          if ((uint32_t)qq >= g) continue;
+          const uint32_t v = rev ? vr[qq] : vf[qq];
+          if (slot_ready(v)) continue;
+          const uint32_t pa = rev ? pc[qq + 1] : pc[qq], pb = rev ? pc[qq] : pc[qq + 1];
+          const uint64_t key = (uint64_t)pa * n_cols + pb;
+          uint32_t cl = kSlotEmpty;
+          if (v == kSlotEmpty && lane == 0) cl = lazy_claim(la, key);
+          cl = __shfl_sync(kFull, cl, 0);
+          const uint32_t dst = my + q * slot;
+          build_pair_vector_warp(la, n_rows, pa, pb, wp, lane, [&](uint32_t w, uint32_t word) { sts_u32(dst + 4 * w, word); });
+          if (cl != kSlotEmpty) {  // this warp owns the pool slot: copy the vector there and publish it
+            const uint32_t sl = cl & ~kSlotBusy;
+            __syncwarp();
+            uint4* dst_g = reinterpret_cast<uint4*>(la.pool + (uint64_t)sl * wp);
+            for (uint32_t t = lane; t < nv; t += 32) dst_g[t] = lds<uint4>(dst + 16 * t);
+            lazy_publish(la, key, sl, lane);
+          }
+        }
+        __syncwarp();
       }
       mbar_wait(bar, phase);
       phase ^= 1u;
@@ -691,6 +771,8 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
     b = bn;
     e = en;
     c_lane = cn;
+    sf_lane = sfn;
+    sr_lane = srn;
   }
 }
 

@@ -231,6 +231,16 @@ class Evaluator:
         """Build the rank plane for `approx` now (otherwise built on first use)."""
         check(self._L.ebic_matrix_prepare(self._h, float(approx)))
 
+    def index_stats(self) -> dict:
+        """The index behind the last evaluation: mode ('none' | 'full' | 'lazy'), full-index
+        bytes, lazy pool fill / capacity / bytes, vectors built lazily, pool resets."""
+        mode = C.c_int(0)
+        v = [C.c_uint64(0) for _ in range(6)]
+        check(self._L.ebic_matrix_index_stats(self._h, C.byref(mode), *[C.byref(x) for x in v]))
+        return {"mode": ("none", "full", "lazy")[mode.value], "full_bytes": v[0].value,
+                "lazy_slots_used": v[1].value, "lazy_slots_cap": v[2].value, "lazy_bytes": v[3].value,
+                "lazy_built": v[4].value, "lazy_resets": v[5].value}
+
     def build_info(self) -> dict:
         """One-time costs (ms) of the last preparation: index allocation, rank plane, pair-trend index."""
         a, pl, ix = C.c_double(0), C.c_double(0), C.c_double(0)

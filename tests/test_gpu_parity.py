@@ -197,6 +197,48 @@ def test_config3_full_size_bit_exact(evaluator):
     np.testing.assert_array_equal(evaluator.evaluate_population(pop, tp), want)
 
 
+@pytest.mark.skipif(not oracle.reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("policy", ["auto", "full", "lazy"])
+def test_config3_full_size_vs_reference_library(evaluator, policy):
+    """BASELINE config 3 at full size against the LIVE reference: the
+    unmodified evaluate_population (oracle/_ref, trend.cpp:56-72) on a
+    WorkerPool of all host cores, the whole 16384-candidate population, with
+    the default policy (lazy index on a fresh matrix), the full index, and the
+    lazy index; approx 0.03 and, with negatives, approx 0."""
+    from paper_2105_01196_b200._lib import EBIC_PATH_LAZY, EBIC_PATH_TABLE
+
+    m, _ = synth.planted_trend_matrix(20_000, 1000, 3, 500, 20, seed=3)
+    pop = synth.random_population(16384, 1000, seed=42)
+    evaluator.upload(m)
+    evaluator.set_path({"auto": EBIC_PATH_AUTO, "full": EBIC_PATH_TABLE, "lazy": EBIC_PATH_LAZY}[policy])
+    try:
+        mat, rp, pool = oracle.RefMatrix(m.astype(np.float64)), oracle.RefPopulation(pop.cols, pop.offsets), oracle.RefPool(0)
+        for approx, neg in ((0.03, False), (0.0, True)):
+            want = oracle.ref_evaluate(mat, rp, approx, neg, pool)
+            np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
+    finally:
+        evaluator.set_path(EBIC_PATH_AUTO)
+
+
+@pytest.mark.skipif(not oracle.reference_available(), reason="oracle/_ref not built")
+def test_config4_sample_vs_reference_library(evaluator):
+    """BASELINE config 4 (200k x 2000, 1.6 GB f32): a 2048-candidate sample of
+    the P=32768 population against the live reference library on all host
+    cores (the whole population would take minutes of CPU)."""
+    rng = np.random.default_rng(44)
+    m = rng.standard_normal((200_000, 2000), dtype=np.float32)
+    m[:4000] = np.sort(m[:4000], axis=1)  # rows that support long sorted candidates
+    evaluator.upload(m)
+    pop = synth.random_population(32768, 2000, seed=42)
+    got = evaluator.evaluate_population(pop, TrendParams(approx=0.03))
+    sample = np.sort(rng.choice(32768, size=2048, replace=False))
+    sub = Population.from_sequences([pop.sequence(i) for i in sample])
+    mat = oracle.RefMatrix(m.astype(np.float64))
+    want = oracle.ref_evaluate(mat, oracle.RefPopulation(sub.cols, sub.offsets), 0.03, False, oracle.RefPool(0))
+    np.testing.assert_array_equal(got[sample], want)
+    del mat
+
+
 def test_config4_full_size_properties(evaluator):
     """BASELINE config 4 (200k x 2000, 1.6 GB f32, P=32768): bit-exact on a candidate
     sample, plus size-independent properties over the whole population."""
@@ -538,8 +580,8 @@ def test_pair_trend_index_vs_oracle(evaluator, R, n_cols):
 
 
 def test_pair_trend_index_budget_and_fallback(evaluator):
-    """AUTO builds the index only within the budget; below it the slab kernels
-    run (same counts); the index is rebuilt per approx and per matrix."""
+    """AUTO builds the full index only within the budget; below it the lazy
+    index serves (same counts); the index is rebuilt per approx and per matrix."""
     rng = np.random.default_rng(5)
     m = rng.standard_normal((2000, 120)).astype(np.float32)
     pop = synth.random_population(800, 120, seed=9)
@@ -550,7 +592,7 @@ def test_pair_trend_index_budget_and_fallback(evaluator):
         evaluator.set_table_budget(need - 1)
         want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
         np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams()), want)
-        assert not evaluator.index_info()[1]
+        assert not evaluator.index_info()[1] and evaluator.index_stats()["mode"] == "lazy"
         evaluator.set_table_budget(1 << 40)
         for approx in (0.03, 0.2, 0.0, 0.03):
             want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, True)
@@ -562,7 +604,7 @@ def test_pair_trend_index_budget_and_fallback(evaluator):
         want = oracle.evaluate_population(m2, pop.cols, pop.offsets, 0.03, False)
         np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams()), want)
     finally:
-        evaluator.set_table_budget(128 << 30)
+        evaluator.set_table_budget(0)  # the library default
 
 
 @pytest.mark.parametrize("layout", ["separate", "one_block"])

@@ -99,3 +99,34 @@ def test_concurrent_runs_one_context_per_thread():
     assert len(got_l) == len(want_l) == 4
     for a, b in zip(want_l, got_l):
         assert json.loads(a) == json.loads(b)
+
+
+NONDEFAULT = {
+    "overlap_0.3": ["--overlap", "0.3"],
+    "tournament9_crossover_heavy": ["--tournament", "9", "--weights", "0.05,0.05,0.1,0.1,0.7"],
+    "six_biclusters_two_elites": ["--biclusters", "6", "--elite", "2"],
+    "penalty2_approx0.1_neg": ["--penalty", "2.0", "--approx", "0.1", "--negative", "1"],
+}
+
+
+@pytest.mark.parametrize("label", sorted(NONDEFAULT))
+def test_run_nondefault_params_byte_identical(label):
+    """run() with non-default GA parameters (evolution.hpp:20-39: overlap
+    threshold, tournament size, crossover-heavy operator weights, bicluster
+    count, elites, crowding penalty, approx/negatives): the unchanged reference
+    GA on the drop-in TU (default environment: the cached matrix verified on
+    every call) and the device-aware driver (bicseek_run_device.cpp, its own
+    restatement of the archive and breeding loop) both equal the reference CPU
+    build, result, generations and termination."""
+    exe_ref, exe_dev, exe_drv = _need("run_ref"), _need("run_device"), _need("run_device_overlap")
+    args = ["--rows", "2000", "--cols", "150", "--bic-rows", "120", "--bic-cols", "10", "--num-bics", "3",
+            "--pop", "600", "--iters", "40", "--tabu", "1000000000000", *NONDEFAULT[label]]
+    env = dict(os.environ)
+    env.pop("EBIC_SHIM_TRUST_POINTER", None)
+    want = json.loads(subprocess.run([str(exe_ref), *args], check=True, capture_output=True, text=True,
+                                     timeout=600).stdout)
+    for exe, extra in ((exe_dev, []), (exe_drv, ["--engine", "device"])):
+        got = json.loads(subprocess.run([str(exe), *extra, *args], check=True, capture_output=True, text=True,
+                                        timeout=600, env=env).stdout)
+        assert got["result"] == want["result"], (exe.name, label)
+        assert got["generations"] == want["generations"] and got["termination"] == want["termination"]
