@@ -202,13 +202,16 @@ struct ebic_ctx {
   uint32_t* d_lmap = nullptr;       // C x C slot per ordered pair
   uint32_t* d_lpool = nullptr;      // lcap x wp words
   uint32_t* d_lcount = nullptr;     // slots handed out (device)
+  uint32_t* d_lkeys = nullptr;      // long vectors: per slot, the pair it was claimed for (lkcap slots)
+  uint32_t* d_lleft = nullptr;      // long vectors: per slot, 32-word chunks still to build
+  uint32_t* d_lstart = nullptr;     // long vectors: the count at the batch's start
+  uint64_t lkcap = 0;
   uint64_t lcap = 0;                // pool capacity (slots)
   HostBuf<uint32_t> h_lmirror;      // page-locked, mapped: {count at a lazy kernel's start, its batch sequence}
   uint32_t* h_lmirror_dev = nullptr;
   bool lazy_valid = false;
   double lazy_approx = 0.0;
   uint32_t lazy_seq = 0, lazy_epoch_seq = 1;  // batch sequence; first batch of the current map epoch
-  std::vector<std::pair<uint32_t, uint64_t>> lazy_inflight;  // (seq, worst-case new pairs) not yet seen by the mirror
   uint64_t lazy_built = 0;          // slots filled over all epochs of this (matrix, approx) (ski-rental rent)
   uint64_t lazy_epoch_seen = 0;     // slots of the current epoch already added to lazy_built
   uint64_t lazy_resets = 0;
@@ -510,17 +513,19 @@ constexpr double kLazyRentFrac = 0.5;                // ski rental: buy the full
 bool lazy_allowed(const ebic_ctx* ctx) {
   if (!(ctx->path == EBIC_PATH_AUTO || ctx->path == EBIC_PATH_LAZY)) return false;
   const uint64_t C = ctx->n_cols;
-  return C >= 1 && C <= kLazyMaxCols && table_wp(ctx) / 4 <= 256 && ctx->table_kernel != 1 && ctx->table_kernel != 2;
+  return C >= 1 && C <= kLazyMaxCols && ctx->table_kernel != 1 && ctx->table_kernel != 2;
 }
 
 uint64_t lazy_map_bytes(const ebic_ctx* ctx) { return ctx->n_cols * ctx->n_cols * sizeof(uint32_t); }
 
 void lazy_release(ebic_ctx* ctx, cudaStream_t s) {
-  if (ctx->d_lpool) cudaFreeAsync(ctx->d_lpool, s);
-  ctx->d_lpool = nullptr;
-  ctx->lcap = 0;
+  (void)s;  // (cudaFree waits for the device's work in flight)
+  if (ctx->d_lpool) cudaFree(ctx->d_lpool);
+  if (ctx->d_lkeys) cudaFree(ctx->d_lkeys);
+  if (ctx->d_lleft) cudaFree(ctx->d_lleft);
+  ctx->d_lpool = ctx->d_lkeys = ctx->d_lleft = nullptr;
+  ctx->lcap = ctx->lkcap = 0;
   ctx->lazy_valid = false;
-  ctx->lazy_inflight.clear();
 }
 
 // Start a new map epoch (first use, new approx, or a full pool): every pair
@@ -530,16 +535,15 @@ int lazy_new_epoch(ebic_ctx* ctx, cudaStream_t s) {
   EBIC_CUDA(cudaMemsetAsync(ctx->d_lcount, 0, sizeof(uint32_t), s));
   ctx->lazy_epoch_seq = ctx->lazy_seq + 1;
   ctx->lazy_epoch_seen = 0;
-  ctx->lazy_inflight.clear();
   return EBIC_OK;
 }
 
 // Make room for a batch that may need `worst` new vectors, without a host
 // sync: the mirror tells how full the pool was when some earlier batch
-// started; every batch issued since may have added its worst case.  Grows the
-// pool (cudaMallocAsync + copy + cudaFreeAsync on the stream) up to the
-// budget, or starts a new epoch when it cannot grow.  An underestimate is
-// still exact: a warp that finds no free slot builds a private copy.
+// started.  Grows the pool (cudaMalloc + copy on the stream + cudaFree of the
+// old one) up to the budget, or starts a new epoch when it cannot grow.  An
+// underestimate is still exact: a pair that finds no free slot is built
+// privately (short vectors) or computed by the count kernel (long ones).
 int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, ebic::LazyArgs* la) {
   const uint64_t vec_bytes = table_wp(ctx) * sizeof(uint32_t);
   if (!ctx->d_lmap) {
@@ -568,41 +572,64 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
       ctx->lazy_built += used - ctx->lazy_epoch_seen;
       ctx->lazy_epoch_seen = used;
     }
-    auto& f = ctx->lazy_inflight;
-    f.erase(std::remove_if(f.begin(), f.end(), [&](const std::pair<uint32_t, uint64_t>& x) { return x.first < m_seq; }),
-            f.end());
   }
-  uint64_t pending = 0;
-  for (const auto& x : ctx->lazy_inflight) pending += x.second;
+  // Room for this batch at its worst case.  Batches issued since the
+  // mirror's sample are not counted at theirs: a GA's populations (and a
+  // cycled benchmark pool) reuse most pairs, so a sum of worst cases grows
+  // the pool -- or restarts it -- for pairs that never come.  An
+  // underestimate stays exact: a claim past the capacity is computed by the
+  // count kernel itself.  A new pool holds three worst-case batches.
   const uint64_t c2 = ctx->n_cols * ctx->n_cols;
   const uint64_t budget = ctx->table_budget > lazy_map_bytes(ctx) ? ctx->table_budget - lazy_map_bytes(ctx) : 0;
   const uint64_t max_slots = std::max<uint64_t>(1, std::min<uint64_t>({c2, budget / vec_bytes, 0x7fffffffull}));
-  const uint64_t need_raw = used + pending + worst;
+  const uint64_t need_raw = used + worst;
   const uint64_t need = std::min<uint64_t>(need_raw, max_slots);
   if (need_raw > ctx->lcap) {
     if (ctx->lcap < max_slots) {
       // room for ~3 batches of this size: the mirror lags by a batch or two,
       // so a pool sized for one batch would grow again on the next call
       const uint64_t cap = std::min<uint64_t>(max_slots, std::max<uint64_t>({need + 2 * worst, 2 * ctx->lcap, 4096}));
+      // cudaMalloc, not the stream-ordered allocator: measured on B200, making
+      // 4 GB usable takes 4 ms with cudaMalloc and 120 ms with cudaMallocAsync
+      // from the default pool (profiles/r2_alloc_cost.txt).  Freeing the old
+      // pool waits for the copy (cudaFree synchronises): growth is rare.
       uint32_t* np = nullptr;
-      if (cudaMallocAsync(reinterpret_cast<void**>(&np), cap * vec_bytes, s) != cudaSuccess) {
+      if (cudaMalloc(reinterpret_cast<void**>(&np), cap * vec_bytes) != cudaSuccess) {
         cudaGetLastError();  // cannot grow: stay at this capacity (warps build private copies)
       } else {
         if (ctx->d_lpool) {
           EBIC_CUDA(cudaMemcpyAsync(np, ctx->d_lpool, ctx->lcap * vec_bytes, cudaMemcpyDeviceToDevice, s));
-          EBIC_CUDA(cudaFreeAsync(ctx->d_lpool, s));
+          EBIC_CUDA(cudaFree(ctx->d_lpool));
         }
         ctx->d_lpool = np;
         ctx->lcap = cap;
       }
-    } else if (ctx->lcap < c2 && used + pending >= ctx->lcap / 2) {
-      ++ctx->lazy_resets;  // the pool cannot grow and is filling up: start over (a pool of all C^2 never is)
+    } else if (ctx->lcap < c2) {
+      // the pool cannot grow and this batch may not fit: start over (a pool
+      // of all C^2 pairs never fills)
+      ++ctx->lazy_resets;
       EBIC_TRY(lazy_new_epoch(ctx, s));
     }
   }
+  if (table_wp(ctx) / 4 > 256 && ctx->lkcap < ctx->lcap) {
+    // long vectors: per-slot claim bookkeeping (only read within one batch: no copy)
+    uint32_t *nk = nullptr, *nl = nullptr;
+    if (cudaMalloc(reinterpret_cast<void**>(&nk), ctx->lcap * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&nl), ctx->lcap * sizeof(uint32_t)) != cudaSuccess) {
+      cudaGetLastError();
+      if (nk) cudaFree(nk);
+      return fail(EBIC_ERR_CUDA, "lazy index: cannot allocate %llu slots of bookkeeping",
+                  (unsigned long long)ctx->lcap);
+    }
+    EBIC_CUDA(cudaMemsetAsync(nk, 0xFF, ctx->lcap * sizeof(uint32_t), s));  // kSlotEmpty: nothing claimed
+    if (ctx->d_lkeys) cudaFree(ctx->d_lkeys);
+    if (ctx->d_lleft) cudaFree(ctx->d_lleft);
+    ctx->d_lkeys = nk;
+    ctx->d_lleft = nl;
+    ctx->lkcap = ctx->lcap;
+  }
+  if (!ctx->d_lstart) EBIC_CUDA(cudaMalloc(&ctx->d_lstart, ebic::kLazyStartRing * sizeof(uint32_t)));
   const uint32_t seq = ++ctx->lazy_seq;
-  ctx->lazy_inflight.emplace_back(seq, worst);
-  if (ctx->lazy_inflight.size() > 256) ctx->lazy_inflight.erase(ctx->lazy_inflight.begin());
   la->map = ctx->d_lmap;
   la->pool = ctx->d_lpool;
   la->count = ctx->d_lcount;
@@ -613,6 +640,14 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
   la->ld = ctx->ld;
   la->f64 = ctx->store == EBIC_STORE_F64 ? 1 : 0;
   la->approx = approx;
+  {
+    const ebic::TrendArgs ta = make_args(approx, 0);
+    la->a_f = ta.a_f;
+    la->kscale = ta.kscale;
+  }
+  la->keys = ctx->d_lkeys;
+  la->left = ctx->d_lleft;
+  la->start = ctx->d_lstart;
   return EBIC_OK;
 }
 
@@ -689,6 +724,32 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
   const uint32_t nv = (uint32_t)(table_wp(ctx) / 4);
   const bool lazy = plan.mode == kIndexLazy;
   const bool many = n_cand >= (uint64_t)ctx->n_sms * 32;  // enough warps to fill every SM
+  if (lazy && nv > 256) {
+    // long vectors from the lazy index: claim the batch's missing pairs, build
+    // them (ebic_lazy.cuh), then count through the pool
+    const uint32_t wp = (uint32_t)table_wp(ctx);
+    EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + plan.la.seq % ebic::kLazyStartRing, ctx->d_lcount, sizeof(uint32_t),
+                              cudaMemcpyDeviceToDevice, s));
+    const unsigned cgrid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, (uint64_t)ctx->n_sms * 16);
+    ebic::lazy_claim_kernel<<<cgrid, 256, 0, s>>>(plan.la, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx,
+                                                  (uint32_t)ctx->n_cols, (wp + 31) / 32, neg);
+    const unsigned bgrid = (unsigned)ctx->n_sms * 8;
+    if (ctx->store == EBIC_STORE_F64)
+      ebic::lazy_build_kernel<double><<<bgrid, 256, 0, s>>>(plan.la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+    else
+      ebic::lazy_build_kernel<float><<<bgrid, 256, 0, s>>>(plan.la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
+    auto go = [&](auto kern) {
+      kern<<<grid, 256, 0, s>>>(nullptr, (uint32_t)ctx->n_cols, wp, (uint32_t)ctx->n_rows, d_cols, d_offs,
+                                (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,
+                                ctx->ld / 32, plan.la);
+    };
+    if (neg) go(ebic::table_count_warp_multi_kernel<8, true, MASK, true, true>);
+    else go(ebic::table_count_warp_multi_kernel<8, false, MASK, true, true>);
+    ctx->launches += 3;
+    EBIC_CUDA(cudaGetLastError());
+    return EBIC_OK;
+  }
   if (!lazy && nv > 256 && (ctx->table_kernel == 1 || (ctx->table_kernel == 0 && many))) {
     // long vectors, many candidates: a warp per candidate sweeping its vectors
     // in passes of 256 slices (no block barriers; measured 0.44 vs 0.67 ms for
@@ -698,7 +759,7 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     auto go = [&](auto kern) {
       kern<<<grid, 256, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
                                 d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err,
-                                d_mask, ctx->ld / 32);
+                                d_mask, ctx->ld / 32, ebic::LazyArgs{});
     };
     if (neg) go(ebic::table_count_warp_multi_kernel<8, true, MASK>);
     else go(ebic::table_count_warp_multi_kernel<8, false, MASK>);
@@ -1458,6 +1519,7 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   for (cudaEvent_t& e : ctx->ev_build)
     if (e) cudaEventDestroy(e);
   if (ctx->d_lcount) cudaFree(ctx->d_lcount);
+  if (ctx->d_lstart) cudaFree(ctx->d_lstart);
   ctx->h_lmirror.release();
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

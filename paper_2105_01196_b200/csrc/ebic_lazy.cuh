@@ -39,6 +39,13 @@ constexpr uint32_t kSlotBusy = 0x80000000u;  // high bit: claimed, vector not ye
 
 struct LazyArgs {
   uint32_t* map;        // C x C slots
+  // long vectors only (lazy_claim_kernel / lazy_build_kernel): per pool slot,
+  // the pair it was claimed for and the claiming batch's tag (kSlotEmpty:
+  // not waiting to be built), the 32-word chunks still to build, and a ring
+  // of batch start counts (entry seq % kLazyStartRing)
+  uint32_t* keys;
+  uint32_t* left;
+  const uint32_t* start;
   uint32_t* pool;       // cap x wp words
   uint32_t* count;      // slots handed out
   uint32_t* count_out;  // (optional, host-mapped) {count at kernel start, seq}: the host's lagged view of the fill
@@ -48,7 +55,17 @@ struct LazyArgs {
   uint64_t ld;
   int f64;              // store is double
   double approx;
+  float a_f, kscale;    // float32 bracket of the threshold (ebic_kernels.cuh bracket / make_args)
 };
+
+// The per-row test's parameters: the reference threshold in double, and a
+// float32 bracket of it that decides all but the near-threshold rows of a
+// float32 store without float64 arithmetic.
+struct PairThr {
+  double approx;
+  float a_f, kscale;
+};
+__device__ __forceinline__ PairThr pair_thr(const LazyArgs& la) { return PairThr{la.approx, la.a_f, la.kscale}; }
 
 __device__ __forceinline__ bool slot_ready(uint32_t s) { return s < kSlotBusy; }
 
@@ -64,33 +81,64 @@ __device__ __forceinline__ uint32_t index_row_of_lane(int lane) {
 }
 
 // One row's bit of B(a, b): trend.cpp:22 in double, two rounded ops (thr64).
+__device__ __forceinline__ bool pair_bit(double x, double y, const PairThr& th) { return y > thr64(x, th.approx); }
+// float32 store: y > thr64(x) decided by the float32 bracket [t - d, t + d]
+// of the threshold (the value kernels' filter mode); the double test runs
+// only for y inside it
+__device__ __forceinline__ bool pair_bit(float x, float y, const PairThr& th) {
+  const float ax = fabsf(x);
+  const float t = __fmaf_rn(-th.a_f, ax, x);
+  const float d = __fmaf_rn(th.kscale, ax, 0x1p-146f);
+  if (y > __fadd_rn(t, d)) return true;
+  if (y <= __fsub_rn(t, d)) return false;
+  return (double)y > thr64((double)x, th.approx);
+}
 template <typename T>
 __device__ __forceinline__ bool pair_row_bit(const T* __restrict__ ca, const T* __restrict__ cb, uint32_t r,
-                                             double approx) {
-  return (double)__ldg(cb + r) > thr64((double)__ldg(ca + r), approx);
+                                             const PairThr& th) {
+  return pair_bit(__ldg(ca + r), __ldg(cb + r), th);
+}
+
+// Words w0 .. w0 + 31 of B(a, b), computed by the warp: lane l returns word
+// w0 + l.  Each ballot is one word (lane l tests row index_row_of_lane(l) of
+// it).  The loads of 8 words are issued (clamped to valid rows) before any
+// test, so the occasional exact double test never serialises them.
+template <typename T>
+__device__ __forceinline__ uint32_t pair_chunk_warp(const T* __restrict__ ca, const T* __restrict__ cb,
+                                                    uint32_t n_rows, uint32_t w0, const PairThr& th, int lane) {
+  constexpr int B = 8;
+  const uint32_t rl = index_row_of_lane(lane);
+  const uint32_t last = n_rows - 1;
+  uint32_t mine = 0;
+#pragma unroll 1
+  for (int j0 = 0; j0 < 32; j0 += B) {
+    T x[B], y[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const uint32_t r = min(32u * (w0 + j0 + i) + rl, last);
+      x[i] = __ldg(ca + r);
+      y[i] = __ldg(cb + r);
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const bool bit = pair_bit(x[i], y[i], th) && 32u * (w0 + j0 + i) + rl < n_rows;
+      const uint32_t word = __ballot_sync(kFull, bit);
+      mine = lane == j0 + i ? word : mine;
+    }
+  }
+  return mine;
 }
 
 // The warp builds the wp-word vector B(a, b) and hands word w to `emit(w, word)`
-// on lane w % 32 (one call per 32-word chunk per lane).  Loads are clamped to
-// valid rows and issued unconditionally (8 words in flight per lane).
+// on lane w % 32 (one call per 32-word chunk per lane).
 template <typename T, typename Emit>
 __device__ __forceinline__ void build_pair_vector_warp_t(const T* __restrict__ mat, uint64_t ld, uint32_t n_rows,
-                                                         uint32_t a, uint32_t b, double approx, uint32_t wp, int lane,
+                                                         uint32_t a, uint32_t b, const PairThr& th, uint32_t wp, int lane,
                                                          Emit emit) {
   const T* ca = mat + (uint64_t)a * ld;
   const T* cb = mat + (uint64_t)b * ld;
-  const uint32_t rl = index_row_of_lane(lane);
-  const uint32_t last = n_rows - 1;
   for (uint32_t w0 = 0; w0 < wp; w0 += 32) {
-    uint32_t mine = 0;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t r = 32u * (w0 + j) + rl;
-      const bool ok = r < n_rows;
-      const bool bit = pair_row_bit(ca, cb, ok ? r : last, approx) && ok;
-      const uint32_t word = __ballot_sync(kFull, bit);
-      mine = lane == j ? word : mine;
-    }
+    const uint32_t mine = pair_chunk_warp(ca, cb, n_rows, w0, th, lane);
     if (w0 + lane < wp) emit(w0 + lane, mine);
   }
 }
@@ -99,17 +147,17 @@ template <typename Emit>
 __device__ __forceinline__ void build_pair_vector_warp(const LazyArgs& la, uint32_t n_rows, uint32_t a, uint32_t b,
                                                        uint32_t wp, int lane, Emit emit) {
   if (la.f64)
-    build_pair_vector_warp_t(static_cast<const double*>(la.mat), la.ld, n_rows, a, b, la.approx, wp, lane, emit);
+    build_pair_vector_warp_t(static_cast<const double*>(la.mat), la.ld, n_rows, a, b, pair_thr(la), wp, lane, emit);
   else
-    build_pair_vector_warp_t(static_cast<const float*>(la.mat), la.ld, n_rows, a, b, la.approx, wp, lane, emit);
+    build_pair_vector_warp_t(static_cast<const float*>(la.mat), la.ld, n_rows, a, b, pair_thr(la), wp, lane, emit);
 }
 
 // uint4 slice v (words 4v .. 4v + 3, rows 128 v .. 128 v + 127) of B(a, b),
 // by one thread -- the slow path of the long-vector kernels for a vector that
 // another warp is still building (or that found the pool full).
 template <typename T>
-__device__ uint4 pair_slice_thread_t(const T* __restrict__ mat, uint64_t ld, uint32_t n_rows, uint32_t a, uint32_t b,
-                                     uint32_t v, double approx) {
+__device__ __noinline__ uint4 pair_slice_thread_t(const T* __restrict__ mat, uint64_t ld, uint32_t n_rows, uint32_t a, uint32_t b,
+                                     uint32_t v, const PairThr& th) {
   const T* ca = mat + (uint64_t)a * ld;
   const T* cb = mat + (uint64_t)b * ld;
   uint32_t w[4];
@@ -119,7 +167,7 @@ __device__ uint4 pair_slice_thread_t(const T* __restrict__ mat, uint64_t ld, uin
     const uint32_t r0 = 128u * v + 32u * q;
     for (int j = 0; j < 32; ++j) {
       const uint32_t r = r0 + index_row_of_lane(j);
-      if (r < n_rows && pair_row_bit(ca, cb, r, approx)) word |= 1u << j;
+      if (r < n_rows && pair_row_bit(ca, cb, r, th)) word |= 1u << j;
     }
     w[q] = word;
   }
@@ -128,8 +176,8 @@ __device__ uint4 pair_slice_thread_t(const T* __restrict__ mat, uint64_t ld, uin
 
 __device__ __forceinline__ uint4 pair_slice_thread(const LazyArgs& la, uint32_t n_rows, uint32_t a, uint32_t b,
                                                    uint32_t v) {
-  return la.f64 ? pair_slice_thread_t(static_cast<const double*>(la.mat), la.ld, n_rows, a, b, v, la.approx)
-                : pair_slice_thread_t(static_cast<const float*>(la.mat), la.ld, n_rows, a, b, v, la.approx);
+  return la.f64 ? pair_slice_thread_t(static_cast<const double*>(la.mat), la.ld, n_rows, a, b, v, pair_thr(la))
+                : pair_slice_thread_t(static_cast<const float*>(la.mat), la.ld, n_rows, a, b, v, pair_thr(la));
 }
 
 // Claim the slot of pair p for this warp (lane 0 calls; result broadcast by
@@ -159,6 +207,98 @@ __device__ __forceinline__ uint32_t lazy_lookup(const LazyArgs& la, uint64_t p) 
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(la.map + p) : "memory");
   return v;
+}
+
+// ---------------------------------------------------------------------------
+// Long pair vectors (more than 256 uint4 slices: rows > 32768, e.g. 200k x
+// 2000).  A 25-KB vector is too big for a warp to build inside the count
+// kernel, so a batch runs three kernels:
+//   lazy_claim_kernel  every pair of the batch not in the map is claimed: a
+//                      pool slot t (count), map[p] = t | kSlotBusy (CAS),
+//                      keys[t] = p, left[t] = the vector's 32-word chunks;
+//   lazy_build_kernel  the slots claimed since the batch started ([*start,
+//                      count)) are built, one warp per (chunk, slot) unit,
+//                      chunk-major: the units in flight at once all read the
+//                      same 1024-row slice of the matrix (8 MB at 2000
+//                      columns), which stays in L2; the warp that finishes a
+//                      slot's last chunk publishes it (map[p] = t);
+//   table_count_warp_multi_kernel<..., LAZY>  reads ready vectors from the
+//                      pool and computes any other pair's slices itself
+//                      (pool full, or busy in another stream's batch).
+// ---------------------------------------------------------------------------
+// Batches may run on several streams at once (the device API takes the
+// caller's stream), so a build kernel's slot window [start, count) can hold
+// slots another batch claimed: a slot's key carries the claiming batch's tag
+// (seq mod 63, bits 26..31; pair keys are < 2^26 since C <= 8192) and a build
+// kernel builds only its own; the last chunk's warp clears the key again, so
+// a key is set only between its batch's claim and build.
+constexpr uint32_t kLazyKeyBits = 26;
+constexpr uint32_t kLazyStartRing = 64;
+__host__ __device__ __forceinline__ uint32_t lazy_tag(uint32_t seq) { return seq % 63u; }
+
+__device__ __forceinline__ void lazy_claim_pair(const LazyArgs& la, uint64_t p, uint32_t n_chunks) {
+  if (lazy_lookup(la, p) != kSlotEmpty) return;  // ready, or claimed already
+  const uint32_t t = atomicAdd(la.count, 1u);
+  if (t >= la.cap) return;  // pool full: the count kernel computes this pair itself
+  const uint32_t old = atomicCAS(la.map + p, kSlotEmpty, t | kSlotBusy);
+  if (old == kSlotEmpty) {  // (otherwise another thread claimed p first: slot t stays unused)
+    la.left[t] = n_chunks;
+    la.keys[t] = (uint32_t)p | (lazy_tag(la.seq) << kLazyKeyBits);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+lazy_claim_kernel(const LazyArgs la, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs,
+                  uint32_t n_cand, uint32_t n_idx, uint32_t n_cols, uint32_t n_chunks, int neg) {
+  if (la.count_out && blockIdx.x == 0 && threadIdx.x == 0) {  // the host's lagged view of the pool's fill
+    la.count_out[0] = *(volatile uint32_t*)la.count;
+    __threadfence_system();
+    la.count_out[1] = la.seq;
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_cand; i += warps) {
+    const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
+    if (e <= b || e > n_idx) continue;  // (reported by the count kernel)
+    for (uint32_t k = b + 1 + lane; k < e; k += 32) {
+      const uint32_t x = __ldg(cols + k - 1), y = __ldg(cols + k);
+      if (x >= n_cols || y >= n_cols) continue;
+      lazy_claim_pair(la, (uint64_t)x * n_cols + y, n_chunks);
+      if (neg) lazy_claim_pair(la, (uint64_t)y * n_cols + x, n_chunks);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+lazy_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t wp) {
+  const uint32_t start = la.start[la.seq % kLazyStartRing];
+  const uint32_t end = min(*(volatile uint32_t*)la.count, la.cap);
+  const uint32_t tag = lazy_tag(la.seq);
+  if (end <= start) return;
+  const uint32_t n_jobs = end - start, n_chunks = (wp + 31) / 32;
+  const uint64_t total = (uint64_t)n_jobs * n_chunks;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const T* mat = static_cast<const T*>(la.mat);
+  for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < total; u += warps) {
+    const uint32_t chunk = (uint32_t)(u / n_jobs), t = start + (uint32_t)(u % n_jobs);
+    const uint32_t tk = __ldcg(la.keys + t);
+    if (tk == kSlotEmpty || (tk >> kLazyKeyBits) != tag) continue;  // not claimed by this batch
+    const uint32_t key = tk & ((1u << kLazyKeyBits) - 1u);
+    const uint32_t a = key / n_cols, b = key % n_cols;
+    const uint32_t w0 = chunk * 32;
+    const uint32_t word = pair_chunk_warp(mat + (uint64_t)a * la.ld, mat + (uint64_t)b * la.ld, n_rows, w0,
+                                          pair_thr(la), lane);
+    if (w0 + lane < wp) la.pool[(uint64_t)t * wp + w0 + lane] = word;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0 && atomicSub(la.left + t, 1u) == 1u) {  // the slot's last chunk: publish it
+      __threadfence();
+      la.keys[t] = kSlotEmpty;
+      atomicExch(la.map + key, t);
+    }
+  }
 }
 
 }  // namespace ebic

@@ -392,16 +392,23 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
 // candidate scheme sweeping the vectors in passes of 32 J slices (every slice
 // index clamped, loads still unconditional).  A separate kernel so that the
 // single-pass kernel above keeps its register allocation and load schedule.
-template <int J, bool NEG, bool MASK, bool MULTI = true>
+//
+// LAZY (long vectors only, MULTI): the vectors come from the lazy index's
+// pool, built ahead of this kernel by lazy_claim_kernel / lazy_build_kernel
+// (ebic_lazy.cuh); a pair whose slot is not ready (the pool was full, or
+// another stream's batch is still building it) is computed here, slice by
+// slice, from the value store -- the same bits either way.
+template <int J, bool NEG, bool MASK, bool MULTI = true, bool LAZY = false>
 __global__ void __launch_bounds__(256)
 table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
                         const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
                         uint32_t n_idx, uint32_t* __restrict__ out, int* err_out, uint32_t* __restrict__ mask,
-                        uint64_t mask_wpc) {
+                        uint64_t mask_wpc, const LazyArgs la) {
+  static_assert(!LAZY || MULTI, "the lazy index runs the multi-pass kernel");
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const uint32_t nv = wp / 4;  // uint4 per pair vector (== 32 J unless MULTI or J == 1)
-  const uint4* t4 = reinterpret_cast<const uint4*>(table);
+  const uint4* t4 = reinterpret_cast<const uint4*>(LAZY ? la.pool : table);
   for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_cand; i += warps) {
     const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
     const bool bad_offs = e <= b || e > n_idx;
@@ -424,6 +431,16 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
     }
     // the candidate's columns, 32 at a time in lane registers (shuffled out per pair)
     const uint32_t c_lane = lane < L ? __ldg(cols + b + lane) : 0u;
+    // LAZY: pool slots of the candidate's first 31 forward / reversed pairs
+    // (pair lane -> lane + 1), looked up once for all passes
+    uint32_t sf_lane = kSlotEmpty, sr_lane = kSlotEmpty;
+    if (LAZY) {
+      const uint32_t c_n = __shfl_down_sync(kFull, c_lane, 1);
+      if (lane < 31 && (uint32_t)lane + 1 < L) {
+        sf_lane = lazy_lookup(la, (uint64_t)c_lane * n_cols + c_n);
+        if (NEG) sr_lane = lazy_lookup(la, (uint64_t)c_n * n_cols + c_lane);
+      }
+    }
     uint32_t n = 0;
     // MULTI: vectors longer than 32 J slices are swept in passes of 32 J
     for (uint32_t v0 = 0; v0 < (MULTI ? nv : 1u); v0 += 32 * J) {
@@ -445,7 +462,31 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
         const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv;
         const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv;
         uint4 x[J], y[J];
-        if constexpr (MULTI) {
+        if constexpr (LAZY) {
+          uint32_t sf = k - 1 < 31 ? __shfl_sync(kFull, sf_lane, (k - 1) & 31)
+                                   : lazy_lookup(la, (uint64_t)cp * n_cols + cc);
+          uint32_t sr = !NEG ? 0u : k - 1 < 31 ? __shfl_sync(kFull, sr_lane, (k - 1) & 31)
+                                              : lazy_lookup(la, (uint64_t)cc * n_cols + cp);
+          sf = __shfl_sync(kFull, sf, 0);  // one view per warp
+          sr = __shfl_sync(kFull, sr, 0);
+          if (slot_ready(sf)) {
+#pragma unroll
+            for (int u = 0; u < J; ++u) x[u] = __ldcg(t4 + (uint64_t)sf * nv + min(v0 + u * 32 + lane, nv - 1));
+          } else {
+#pragma unroll
+            for (int u = 0; u < J; ++u) x[u] = pair_slice_thread(la, n_rows, cp, cc, min(v0 + u * 32 + lane, nv - 1));
+          }
+          if (NEG) {
+            if (slot_ready(sr)) {
+#pragma unroll
+              for (int u = 0; u < J; ++u) y[u] = __ldcg(t4 + (uint64_t)sr * nv + min(v0 + u * 32 + lane, nv - 1));
+            } else {
+#pragma unroll
+              for (int u = 0; u < J; ++u)
+                y[u] = pair_slice_thread(la, n_rows, cc, cp, min(v0 + u * 32 + lane, nv - 1));
+            }
+          }
+        } else if constexpr (MULTI) {
 #pragma unroll
           for (int u = 0; u < J; ++u) {
             const uint32_t v = min(v0 + u * 32 + lane, nv - 1);

@@ -38,7 +38,9 @@ def _pop(C, n, seed, dup_pairs=False):
     return Population.from_sequences(seqs)
 
 
-@pytest.mark.parametrize("R", [1, 33, 1000, 4099, 20000, 32768])
+# R > 32768: long vectors (> 256 slices) -- claim / build kernels ahead of the
+# multi-pass count kernel instead of builds inside the TMA kernel
+@pytest.mark.parametrize("R", [1, 33, 1000, 4099, 20000, 32768, 32769, 70001])
 @pytest.mark.parametrize("f64", [False, True])
 def test_lazy_index_vs_oracle(evaluator, R, f64):
     C = 150
@@ -64,10 +66,12 @@ def test_lazy_index_vs_oracle(evaluator, R, f64):
         evaluator.set_path(EBIC_PATH_AUTO)
 
 
-def test_lazy_pool_too_small_resets_and_private_builds(evaluator):
+@pytest.mark.parametrize("R", [9000, 40000])
+def test_lazy_pool_too_small_resets_and_private_builds(evaluator, R):
     """A budget that holds only a few dozen pair vectors: most new pairs find
-    no slot (private builds), the pool starts over; counts stay exact."""
-    R, C = 9000, 200
+    no slot (private builds; for long vectors, slices computed by the count
+    kernel), the pool starts over; counts stay exact."""
+    C = 200
     m = _matrix(R, C, 3)
     evaluator.upload(m)
     wp = ((R + 31) // 32 + 127) // 128 * 128 if (R + 31) // 32 > 128 else ((R + 31) // 32 + 3) // 4 * 4
@@ -87,11 +91,14 @@ def test_lazy_pool_too_small_resets_and_private_builds(evaluator):
         evaluator.set_table_budget(0)
 
 
-def test_lazy_device_api_back_to_back(evaluator):
+@pytest.mark.parametrize("R,n_streams", [(12000, 1), (40000, 1), (40000, 2)])
+def test_lazy_device_api_back_to_back(evaluator, R, n_streams):
     """Device-pointer batches issued back to back (no host sync, programmatic
-    dependent launch, the host's view of the pool lagging): exact."""
+    dependent launch, the host's view of the pool lagging): exact.  With two
+    streams, long-vector batches claim and build concurrently (the batch tags
+    keep each build kernel to its own slots)."""
     torch = pytest.importorskip("torch")
-    R, C = 12000, 400
+    C = 400
     m = _matrix(R, C, 11)
     evaluator.upload(m)
     evaluator.set_path(EBIC_PATH_LAZY)
@@ -101,13 +108,14 @@ def test_lazy_device_api_back_to_back(evaluator):
         dev = [(torch.from_numpy(p.cols.view(np.int32)).cuda(), torch.from_numpy(p.offsets.view(np.int32)).cuda())
                for p in pops]
         outs = [torch.full((5000,), -1, dtype=torch.int32, device="cuda") for _ in range(18)]
-        s = torch.cuda.Stream()
+        streams = [torch.cuda.Stream() for _ in range(n_streams)]
         torch.cuda.synchronize()
         for i in range(18):
             dc, do = dev[i % 6]
             evaluator.evaluate_population_device(dc.data_ptr(), do.data_ptr(), 5000, outs[i].data_ptr(),
-                                                 TrendParams(0.03, True), stream=s.cuda_stream)
-        s.synchronize()
+                                                 TrendParams(0.03, True), stream=streams[i % n_streams].cuda_stream)
+        for s in streams:
+            s.synchronize()
         evaluator.sync()
         for i in range(18):
             np.testing.assert_array_equal(outs[i].cpu().numpy().view(np.uint32), want[i % 6], err_msg=f"launch {i}")
@@ -142,3 +150,26 @@ def test_auto_policy_lazy_then_full(evaluator):
     evaluator.prepare(0.03)
     np.testing.assert_array_equal(evaluator.evaluate_population(pop0, TrendParams()), want0)
     assert evaluator.index_stats()["mode"] == "full"
+
+
+def test_auto_long_vectors_over_budget_use_lazy(evaluator):
+    """Long pair vectors whose full index exceeds the budget (BASELINE config
+    4's situation, scaled down): AUTO serves them from the lazy index, not the
+    slab kernels, and keeps only the population's pairs."""
+    R, C = 50000, 300  # full index 300^2 x 1664 words = 599 MB
+    m = _matrix(R, C, 23)
+    evaluator.upload(m)
+    evaluator.set_table_budget(256 << 20)
+    try:
+        for k in range(3):
+            pop = synth.random_population(3000, C, 3, 5, seed=50 + k % 2)
+            for approx, neg in ((0.03, False), (0.03, True)):
+                want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+                np.testing.assert_array_equal(evaluator.evaluate_population(pop, TrendParams(approx, neg)), want)
+            st = evaluator.index_stats()
+            assert st["mode"] == "lazy" and st["full_bytes"] == 0, st
+        rows = evaluator.supporting_rows(pop.sequence(0), TrendParams(0.03, True))
+        np.testing.assert_array_equal(rows, oracle.supporting_rows(m, pop.sequence(0), 0.03, True))
+        assert evaluator.index_stats()["lazy_bytes"] <= 256 << 20
+    finally:
+        evaluator.set_table_budget(0)
