@@ -10,8 +10,7 @@
 //   map[a * C + b]   uint32 per ordered pair: kSlotEmpty, the pool slot s of
 //                    a ready vector, or s | kSlotBusy while its builder runs
 //   pool[s * wp ...] the vector of slot s, same word layout as the full index
-//                    (even rows in the low half of a word, odd rows in the high
-//                    half: index_valid_bits / index_to_natural)
+//                    (index_bit_row / index_valid_bits / index_to_natural)
 //   count            slots handed out so far (may exceed the capacity: a
 //                    failed allocation still counts, so the host sees a full
 //                    pool and grows or resets it before the next batch)
@@ -73,11 +72,11 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-// Row of a 32-row word evaluated by `lane`: with lane l on row perm(l), a
-// ballot over the warp is the index word itself (bit j < 16: row 2j, bit
-// 16 + j: row 2j + 1).
+// Row of a 32-row word evaluated by `lane`: with lane l on the row of word
+// bit l (index_bit_row, ebic_table.cuh), a ballot over the warp is the index
+// word itself.
 __device__ __forceinline__ uint32_t index_row_of_lane(int lane) {
-  return lane < 16 ? 2u * lane : 2u * (lane - 16) + 1u;
+  return 16u * ((uint32_t)lane >> 4) + (((uint32_t)lane >> 3) & 1u) + 2u * ((uint32_t)lane & 7u);
 }
 
 // One row's bit of B(a, b): trend.cpp:22 in double, two rounded ops (thr64).

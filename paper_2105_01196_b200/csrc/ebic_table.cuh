@@ -14,7 +14,7 @@
 // AND, written out as the row mask (bit r = row r, natural order).
 //
 // Layout: table[(a * C + b) * wp + w]; word w covers rows 32 w .. 32 w + 31
-// (even rows in the low half, odd rows in the high half: index_valid_bits);
+// (byte-interleaved even / odd rows: index_bit_row, index_valid_bits);
 // wp = ceil(R / 32) rounded up to 4 words, or to 128 above 128 words; bits of
 // rows >= R are zero.  Size
 // C^2 * wp * 4 bytes: 2.5 GB at 20k x 1000 -- it is used when it fits the
@@ -30,19 +30,28 @@ namespace ebic {
 constexpr int kTableBuildWarps = 32;   // a-columns per builder CTA
 constexpr int kTableRowsPerCta = 1024;  // rows per builder CTA (32 words)
 
-// Bit order inside an index word.  Word w covers rows 32 w .. 32 w + 31 with
-// the EVEN rows in the low half and the ODD rows in the high half: bit j (j <
-// 16) is row 32 w + 2 j, bit 16 + j is row 32 w + 2 j + 1 -- the order in
-// which the builder's packed two-row compare produces them.  Counting does not
-// care; the valid-row masks and the row-mask output (supporting_rows) use
-// these helpers.
+// Bit order inside an index word.  Word w covers rows 32 w .. 32 w + 31 in
+// four bytes: byte 0 holds the even rows of the first 16 (bit j: row 2 j),
+// byte 1 their odd rows (bit j: row 2 j + 1), bytes 2 and 3 the same for rows
+// 16 .. 31 -- the order in which the builder's packed two-row compares come
+// out of one PRMT (build_pair_table_kernel).  Counting does not care; the
+// valid-row masks, the lazy builders' lane -> row map and the row-mask output
+// (supporting_rows) use these helpers.
+__host__ __device__ __forceinline__ uint32_t index_bit_row(uint32_t bit) {  // row offset (0..31) of a word bit
+  return 16u * (bit >> 4) + ((bit >> 3) & 1u) + 2u * (bit & 7u);
+}
+__host__ __device__ __forceinline__ uint32_t swap_bytes12(uint32_t x) {  // bytes 1 and 2 exchanged
+  return (x & 0xFF0000FFu) | ((x & 0x0000FF00u) << 8) | ((x & 0x00FF0000u) >> 8);
+}
 __host__ __device__ __forceinline__ uint32_t index_valid_bits(uint32_t n_rows, uint32_t word) {
-  // branch-free: rem = valid rows of the word (0..32); rows 2j < rem fill the
-  // low half, rows 2j + 1 < rem the high half (shifts stay <= 16)
+  // branch-free: rem = valid rows of the word (0..32); rows 2j < rem (bits j
+  // of bytes 0 / 2) and 2j + 1 < rem (bytes 1 / 3): built as "even rows in
+  // the low half, odd rows in the high half" (shifts stay <= 16), then bytes
+  // 1 and 2 exchanged
   const uint32_t r0 = 32 * word;
   const uint32_t rem = n_rows > r0 ? min(n_rows - r0, 32u) : 0u;
   const uint32_t even = (rem + 1) >> 1, odd = rem >> 1;
-  return ((1u << even) - 1u) | (((1u << odd) - 1u) << 16);
+  return swap_bytes12(((1u << even) - 1u) | (((1u << odd) - 1u) << 16));
 }
 __device__ __forceinline__ uint32_t spread_even(uint32_t x) {  // bit i of a 16-bit value -> bit 2 i
   x &= 0xFFFFu;
@@ -54,7 +63,19 @@ __device__ __forceinline__ uint32_t spread_even(uint32_t x) {  // bit i of a 16-
 }
 // index word -> natural order (bit k = row 32 w + k)
 __device__ __forceinline__ uint32_t index_to_natural(uint32_t w) {
-  return spread_even(w) | (spread_even(w >> 16) << 1);
+  const uint32_t h = __byte_perm(w, 0u, 0x3120);  // even rows in the low half, odd rows in the high half
+  return spread_even(h) | (spread_even(h >> 16) << 1);
+}
+
+// Sign-replicating byte permute: byte k of the result is 0xFF or 0x00 by
+// bit 15 (k = 0) / 31 (k = 1) of lo and bit 15 (k = 2) / 31 (k = 3) of hi.
+__device__ __forceinline__ uint32_t prmt_sign15_31(uint32_t lo, uint32_t hi) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_u2(const uint32_t* p) {
+  return __ldg(reinterpret_cast<const uint2*>(p));
 }
 
 // Builder: CTA = (row block of 1024 rows, tile of 32 columns a).  Warp w owns
@@ -62,14 +83,15 @@ __device__ __forceinline__ uint32_t index_to_natural(uint32_t w) {
 // their negated thresholds as 16 packed row pairs (NT, as in the slab kernel:
 // 0 - (T_even | T_odd << 16) - 0x00010001).  The CTA streams every column b's
 // guarded ranks (Rg = R | 0x8000 per row, two rows per word) through shared
-// memory, two columns per barrier, the next two already loading.  For a pair
-// word, D = Rg(b) + NT(a) has bit 15 set iff R_b > T_a for the even row and
-// bit 31 for the odd row (ebic_simd.cuh), so one IADD tests two rows and one
-// shift + OR files both bits: 16 such steps make the lane's index word, and
-// the warp's 32 words leave as one coalesced 128-byte store.  About 2
-// instructions per output word (a ballot-based builder needs 5).  Shared
-// layout: pair j of word l at 16 l + (j ^ ((l >> 1) & 15)) -- conflict-free
-// for the 32 lanes reading pair j of their words at once.
+// memory, two columns per barrier, the next two already loading (one 8-byte
+// load per row pair).  For a pair word, D = Rg(b) + NT(a) has bit 15 set iff
+// R_b > T_a for the even row and bit 31 for the odd row (ebic_simd.cuh), so
+// one IADD tests two rows; pairs j and j + 8 are filed together by one
+// sign-replicating PRMT (four bytes of 0x00 / 0xFF) and one LOP3 (bit j of
+// each byte): 16 IADD + 8 PRMT + 8 LOP3 per index word, and the warp's 32
+// words leave as one coalesced 128-byte store.  Shared layout: pair j of word
+// l at j * 33 + l -- conflict-free reads at immediate offsets (lane l reads
+// word l of row j), at most 2-way conflicts for the staging stores.
 //
 // A = a-columns per warp: with A = 2 a warp keeps the thresholds of columns
 // a and a + 16 (32 packed registers) and every shared-memory read of a column
@@ -83,7 +105,9 @@ build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_
   const uint32_t b_begin = blockIdx.z * b_per_z, b_end = min(n_cols, b_begin + b_per_z);
   constexpr int T = kTableBuildWarps / A * 32;                 // threads
   constexpr int PAIRS = kTableRowsPerCta / 2;                  // row pairs of the block
-  __shared__ uint32_t s_rg[2][2][PAIRS];  // [iteration parity][column of the pair][swizzled pair]
+  constexpr int SW = 33;                                       // words per staged pair row j (32 + 1 pad)
+  constexpr uint32_t COLB = 16 * SW * 4;                       // bytes per staged column
+  __shared__ uint32_t s_rg[2][2][16 * SW];  // [iteration parity][column of the pair][pair j * SW + word]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r0 = blockIdx.x * kTableRowsPerCta;
   const uint32_t w0 = r0 / 32;  // first word of this row block
@@ -98,15 +122,14 @@ build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_
     const uint32_t rl = r0 + 32 * lane;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const uint32_t re = rl + 2 * j;
-      const uint32_t te = (a_ok[q] && re < n_rows) ? (__ldg(plane + (uint64_t)ac[q] * ld + re) & 0xFFFFu) : 0u;
-      const uint32_t to = (a_ok[q] && re + 1 < n_rows) ? (__ldg(plane + (uint64_t)ac[q] * ld + re + 1) & 0xFFFFu) : 0u;
-      nt[q][j] = 0u - (te | (to << 16)) - 0x00010001u;
+      const uint32_t re = rl + 2 * j;  // (re < n_rows keeps re + 1 inside the column's ld rows)
+      const uint2 v = (a_ok[q] && re < n_rows) ? ldg_u2(plane + (uint64_t)ac[q] * ld + re) : make_uint2(0u, 0u);
+      nt[q][j] = 0u - __byte_perm(v.x, v.y, 0x5410) - 0x00010001u;  // T_even | T_odd << 16, negated
     }
   }
   const uint32_t valid = index_valid_bits(n_rows, w0 + lane);
-  // staging: each thread packs PAIRS / T row pairs of columns b and b + 1
-  constexpr int PER = 2 * PAIRS / T;  // values staged per thread per iteration (2 with A = 1, 4 with A = 2)
+  // staging: each thread packs PER row pairs of columns b and b + 1
+  constexpr int PER = 2 * PAIRS / T;  // pairs staged per thread per iteration (2 with A = 1, 4 with A = 2)
   uint32_t nxt[PER];
   auto fetch = [&](uint32_t b) {
 #pragma unroll
@@ -114,13 +137,8 @@ build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_
       const uint32_t idx = threadIdx.x + k * T;  // 0 .. 2 PAIRS - 1
       const uint32_t col = b + idx / PAIRS, tp = idx % PAIRS;
       const uint32_t re = r0 + 2 * tp;
-      uint32_t v = 0u;
-      if (col < n_cols) {
-        const uint32_t we = re < n_rows ? __ldg(plane + (uint64_t)col * ld + re) : 0u;
-        const uint32_t wo = re + 1 < n_rows ? __ldg(plane + (uint64_t)col * ld + re + 1) : 0u;
-        v = ((we >> 16) | 0x8000u) | (((wo >> 16) | 0x8000u) << 16);  // guarded ranks Rg of the pair
-      }
-      nxt[k] = v;
+      const uint2 v = (col < n_cols && re < n_rows) ? ldg_u2(plane + (uint64_t)col * ld + re) : make_uint2(0u, 0u);
+      nxt[k] = __byte_perm(v.x, v.y, 0x7632) | 0x80008000u;  // guarded ranks Rg of the pair
     }
   };
   auto stage = [&](int par) {
@@ -128,14 +146,18 @@ build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_
     for (int k = 0; k < PER; ++k) {
       const uint32_t idx = threadIdx.x + k * T;
       const uint32_t tp = idx % PAIRS;
-      const uint32_t sidx = 16 * (tp >> 4) + ((tp & 15) ^ ((tp >> 5) & 15));  // pair j = tp & 15 of word tp >> 4
-      s_rg[par][idx / PAIRS][sidx] = nxt[k];
+      s_rg[par][idx / PAIRS][(tp & 15) * SW + (tp >> 4)] = nxt[k];  // pair j = tp & 15 of word tp >> 4
     }
   };
   fetch(b_begin);
-  const uint32_t sw = (uint32_t)(lane >> 1) & 15u;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(&s_rg[0][0][0]) + 4 * lane;
+  // this lane's output word of pair (a_0, b): advanced by wp per column b; the
+  // other a-columns of the warp are kTableBuildWarps / A columns further on
+  const bool st_ok = w0 + lane < wp;
+  uint32_t* trow = table + ((uint64_t)ac[0] * n_cols + b_begin) * wp + w0 + lane;
+  const uint64_t qstride = (uint64_t)(kTableBuildWarps / A) * n_cols * wp;
   int par = 0;
-  for (uint32_t b = b_begin; b < b_end; b += 2, par ^= 1) {
+  for (uint32_t b = b_begin; b < b_end; b += 2, par ^= 1, trow += 2 * wp) {
     // one barrier per two columns: the buffers alternate between iterations,
     // so writing this pair never races the previous pair's readers
     stage(par);
@@ -144,21 +166,22 @@ build_pair_table_kernel(const uint32_t* __restrict__ plane, uint64_t ld, uint32_
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (b + h < b_end) {
-        const uint32_t* rg = s_rg[par][h] + 16 * lane;
+        const uint32_t base = sbase + (uint32_t)(2 * par + h) * COLB;
+        uint32_t x[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x[j]) : "r"(base + j * SW * 4));
         uint32_t word[A];
 #pragma unroll
         for (int q = 0; q < A; ++q) word[q] = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t x = rg[j ^ sw];
-#pragma unroll
-          for (int q = 0; q < A; ++q) word[q] |= ((x + nt[q][j]) & 0x80008000u) >> (15 - j);
-        }
-        if (w0 + lane < wp) {
+        for (int j = 0; j < 8; ++j) {
 #pragma unroll
           for (int q = 0; q < A; ++q)
-            if (a_ok[q]) table[((uint64_t)ac[q] * n_cols + b + h) * wp + w0 + lane] = word[q] & valid;
+            word[q] |= prmt_sign15_31(x[j] + nt[q][j], x[j + 8] + nt[q][j + 8]) & (0x01010101u << j);
         }
+#pragma unroll
+        for (int q = 0; q < A; ++q)
+          if (st_ok && a_ok[q]) trow[h * wp + q * qstride] = word[q] & valid;
       }
     }
   }
