@@ -175,6 +175,10 @@ struct ebic_ctx {
   bool xchg_xdone_armed[kXchgDepth] = {};
   DevBuf<uint32_t> d_xchg_local[kXchgDepth];       // this rank's partial counts, per ring slot
   int pipeline_pieces = 1;       // EBIC_HOST_PIECES (1 = no pipelining; measured faster on B200 at 16K candidates)
+  // EBIC_ZC_READ_MAX: page-locked inputs up to this many bytes are read in place
+  // by the index kernel (measured: 29.1 -> 24.4 us at P = 392, 30.3 -> 28.4 us
+  // at C2 (82 KB), 52.7 -> 58.7 us at C3 (327 KB): profiles/r2_e2e_small.txt)
+  uint64_t zc_read_max = 128 * 1024;
   Slot slots[EBIC_MARSHAL_SLOTS];
   uint64_t next_ticket = 1;
   // tickets retired early (ring reuse / slot growth) whose device-side check failed
@@ -1460,6 +1464,8 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (pf) ctx->prefetch = std::atoi(pf) ? 1 : 0;
     const char* tb = std::getenv("EBIC_TABLE_BUDGET_MB");
     if (tb) ctx->table_budget_user = (uint64_t)std::strtoull(tb, nullptr, 10) << 20;
+    const char* zr = std::getenv("EBIC_ZC_READ_MAX");
+    if (zr) ctx->zc_read_max = std::strtoull(zr, nullptr, 10);
     const char* hp = std::getenv("EBIC_HOST_PIECES");
     if (hp) ctx->pipeline_pieces = std::max(1, std::min(4, std::atoi(hp)));
     const char* tba = std::getenv("EBIC_TABLE_BUILD_A");
@@ -1780,7 +1786,14 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
     // it is in flight (the copy reads exactly [0, offsets[n_cand]) of cols, the
     // size the caller declares), and the kernel is launched only if they pass
     const uint32_t *d_cols, *d_offs;
-    if (one_copy) {
+    const uint64_t in_bytes = (n_cand + 1 + n_idx) * sizeof(uint32_t);
+    if (table && lp.direct && in_bytes <= ctx->zc_read_max) {
+      // a small batch: the index kernel reads the page-locked arrays over the
+      // bus itself (two dependent round trips per warp) instead of waiting for
+      // a DMA -- no copy at all (EBIC_ZC_READ_MAX bytes; see DESIGN 4.2)
+      d_offs = static_cast<const uint32_t*>(dev_alias(offsets));
+      d_cols = static_cast<const uint32_t*>(dev_alias(cols));
+    } else if (one_copy) {
       EBIC_TRY(ensure(ctx->d_tmp_cols, n_cand + 1 + n_idx));
       EBIC_CUDA(cudaMemcpyAsync(ctx->d_tmp_cols.p, offsets, (n_cand + 1 + n_idx) * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice, s));
