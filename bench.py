@@ -458,6 +458,11 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     n_warm = max(args.warmup, 3, 2 * n_pops)
     w_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_warm)]
     for i in range(n_warm):
+        if i == n_pops:
+            # the host runs ahead of the device: sync once so that the pool's
+            # size is settled (grown if a worst-case batch may not fit) here,
+            # not on the first timed step
+            torch.cuda.synchronize()
         w_ev[i][0].record(stream)
         step(i)
         w_ev[i][1].record(stream)
