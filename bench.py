@@ -315,6 +315,8 @@ def bench_reference(args, cfg, rank):
 def index_kernel_name(wp, n_cand, n_sms=148, lazy=False):
     """The index kernel launch_table picks (ebic_capi.cu) for this vector length
     and candidate count, with the default EBIC_TABLE_KERNEL."""
+    if wp // 4 <= 32 and not lazy:
+        return "table_count_group_kernel"
     if wp // 4 <= 256:
         return "table_count_tma_kernel"
     if lazy:

@@ -239,7 +239,7 @@ struct ebic_ctx {
   uint64_t table_cap = 0;   // bytes allocated at d_table (kept across uploads for reuse)
   int table_build_a = 2;    // EBIC_TABLE_BUILD_A: a-columns per builder warp (1 or 2)
   int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
-  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (TMA warps up to 256 slices; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA (A/B)
+  int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (lane groups up to 32 slices, TMA warps up to 256; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA, 4 lane groups (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
   bool pdl = true;         // programmatic dependent launch of the count kernels (EBIC_PDL=0 disables)
   // one-time build costs of the last (matrix, approx) preparation
@@ -738,6 +738,34 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
   const uint32_t nv = (uint32_t)(table_wp(ctx) / 4);
   const bool lazy = plan.mode == kIndexLazy;
   const bool many = n_cand >= (uint64_t)ctx->n_sms * 32;  // enough warps to fill every SM
+  if (!lazy && nv <= 32 && (ctx->table_kernel == 0 || ctx->table_kernel == 4) && !MASK) {
+    // tiny vectors (R <= 4096 rows): a group of next_pow2(nv) lanes per
+    // candidate, register loads (table_count_group_kernel)
+    // lanes per candidate GL <= 8 (at least 4 candidates per warp), J = nv / GL
+    // slices per lane: nv 1, 2, 4 -> GL = nv; 8 -> 8 x 1; 16 -> 8 x 2; 32 -> 8 x 4
+    const int GL = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : 8;
+    const int J = nv <= 8 ? 1 : nv <= 16 ? 2 : 4;
+    const uint64_t per_cta = 8ull * (32 / GL);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + per_cta - 1) / per_cta, (uint64_t)ctx->n_sms * 8);
+    auto go = [&](auto kern) {
+      kern<<<grid, 256, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
+                                d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err);
+    };
+    auto pick = [&](auto negc) {
+      constexpr bool N = decltype(negc)::value;
+      if (GL == 1) go(ebic::table_count_group_kernel<1, 1, 4, N>);
+      else if (GL == 2) go(ebic::table_count_group_kernel<2, 1, 4, N>);
+      else if (GL == 4) go(ebic::table_count_group_kernel<4, 1, 4, N>);
+      else if (J == 1) go(ebic::table_count_group_kernel<8, 1, 4, N>);
+      else if (J == 2) go(ebic::table_count_group_kernel<8, 2, 4, N>);
+      else go(ebic::table_count_group_kernel<8, 4, 2, N>);
+    };
+    if (neg) pick(std::true_type{});
+    else pick(std::false_type{});
+    ctx->launches++;
+    EBIC_CUDA(cudaGetLastError());
+    return EBIC_OK;
+  }
   if (lazy && nv > 256) {
     // long vectors from the lazy index: claim the batch's missing pairs, build
     // them (ebic_lazy.cuh), then count through the pool

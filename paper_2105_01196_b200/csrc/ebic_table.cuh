@@ -554,6 +554,110 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
   }
 }
 
+// Tiny vectors (nv <= 32 uint4 slices: R <= 4096 rows): a GROUP of GL lanes
+// per candidate (32 / GL candidates per warp), lane s of the group owning
+// slices s, s + GL, ... (J of them) of every pair vector.  A 128-B vector
+// (R = 1000) is then one 16-B load per lane instead of a whole warp's bulk
+// copy and mbarrier round trip; U pairs' loads are issued before they are
+// combined, and the next candidate's offsets load while this one runs.  The
+// index is small enough to sit in L2 (64^2 x 128 B = 512 KB at 1000 rows), so
+// the kernel is bound by L2 latency and issue, not HBM.  Counts and error
+// codes as table_count_kernel; no masks, no lazy index.
+template <int GL, int J, int U, bool NEG>
+__global__ void __launch_bounds__(256)
+table_count_group_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
+                         const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs, uint32_t n_cand,
+                         uint32_t n_idx, uint32_t* __restrict__ out, int* err_out) {
+  static_assert(GL >= 1 && GL <= 32 && (GL & (GL - 1)) == 0, "group size is a power of two");
+  constexpr int CPW = 32 / GL;  // candidates per warp
+  const int lane = threadIdx.x & 31, s = lane % GL;
+  const uint32_t nv = wp / 4;
+  uint32_t sl[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) sl[j] = min((uint32_t)(s + j * GL), nv - 1);  // past the vector: re-read (dropped)
+  const uint4* t4 = reinterpret_cast<const uint4*>(table);
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x / 32) * CPW;
+  uint64_t i0 = ((uint64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) * CPW;
+  auto load_offs = [&](uint64_t i, uint32_t& b, uint32_t& e) {
+    b = i < n_cand ? __ldg(offs + i) : 0u;
+    e = i < n_cand ? __ldg(offs + i + 1) : 0u;
+  };
+  uint32_t b, e;
+  load_offs(i0 + lane / GL, b, e);
+  for (; i0 < n_cand; i0 += stride) {
+    const uint64_t i = i0 + lane / GL;
+    const bool live = i < n_cand;
+    uint32_t bn, en;  // the next candidate's offsets, in flight during this one
+    load_offs(i + stride, bn, en);
+    const bool bad_offs = live && (e <= b || e > n_idx);
+    const uint32_t L = (live && !bad_offs) ? e - b : 0u;
+    uint4 f[J], r[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      f[j] = make_uint4(~0u, ~0u, ~0u, ~0u);
+      r[j] = NEG ? f[j] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    bool badc = false;
+    uint32_t cp = L ? __ldg(cols + b) : 0u;
+    badc |= L && cp >= n_cols;
+    // the warp runs to its longest candidate; shorter groups are predicated off
+    uint32_t Lmax = L;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) Lmax = max(Lmax, __shfl_xor_sync(kFull, Lmax, o));
+    for (uint32_t k0 = 1; k0 < Lmax; k0 += U) {
+      uint32_t cc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cc[u] = k0 + u < L ? __ldg(cols + b + k0 + u) : 0u;
+      uint4 x[U][J], y[U][J];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t a = u == 0 ? cp : cc[u - 1];
+        const bool ok = k0 + u < L && a < n_cols && cc[u] < n_cols;
+        badc |= k0 + u < L && cc[u] >= n_cols;
+        const uint64_t pf = ok ? (uint64_t)a * n_cols + cc[u] : 0u, pr = ok ? (uint64_t)cc[u] * n_cols + a : 0u;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          x[u][j] = __ldg(t4 + pf * nv + sl[j]);
+          if (NEG) y[u][j] = __ldg(t4 + pr * nv + sl[j]);
+          if (!ok) {
+            x[u][j] = make_uint4(~0u, ~0u, ~0u, ~0u);
+            y[u][j] = x[u][j];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          f[j].x &= x[u][j].x; f[j].y &= x[u][j].y; f[j].z &= x[u][j].z; f[j].w &= x[u][j].w;
+          if (NEG) {
+            r[j].x &= y[u][j].x; r[j].y &= y[u][j].y; r[j].z &= y[u][j].z; r[j].w &= y[u][j].w;
+          }
+        }
+      }
+      cp = cc[U - 1];  // (past the candidate's end the pairs are predicated off)
+    }
+    uint32_t n = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const uint4 o = NEG ? make_uint4(f[j].x | r[j].x, f[j].y | r[j].y, f[j].z | r[j].z, f[j].w | r[j].w) : f[j];
+      if ((uint32_t)(s + j * GL) < nv) n += __popc(o.x) + __popc(o.y) + __popc(o.z) + __popc(o.w);
+    }
+#pragma unroll
+    for (int w = GL / 2; w >= 1; w >>= 1) n += __shfl_xor_sync(kFull, n, w);
+    if (live && s == 0) {
+      if (bad_offs || badc) {  // (every lane of a group loads the same columns: same flags)
+        out[i] = 0;
+        *err_out = bad_offs ? 2 : 1;
+      } else {
+        out[i] = L == 1 ? n_rows : n;
+      }
+    }
+    b = bn;
+    e = en;
+  }
+}
+
 // TMA variant of the warp-per-candidate kernel (short vectors, nv <= 256
 // slices).  One elected lane issues a bulk copy (cp.async.bulk, the TMA
 // engine) per pair vector -- S pairs at a time, into the warp's shared-memory
