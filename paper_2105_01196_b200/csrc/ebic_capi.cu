@@ -19,6 +19,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ebic.h"
 #include "ebic_kernels.cuh"
 #include "ebic_plane.cuh"
@@ -26,6 +28,16 @@
 #include "ebic_pair.cuh"
 #include "ebic_table.cuh"
 #include "ebic_xchg.cuh"
+
+// NVTX ranges (header-only NVTX v3; no-ops unless a profiler is attached):
+// every public entry point and every one-time build shows up by name on an
+// nsys / ncu timeline ("ebic:<call>").
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 
@@ -310,6 +322,7 @@ double host_ms() {
 bool plane_fits(const ebic_ctx* ctx) { return ctx->n_cols >= 1 && ctx->n_cols <= ebic::kPlaneMaxCols; }
 
 int ensure_plane(ebic_ctx* ctx, double approx, cudaStream_t s) {
+  NvtxRange nvtx_("ebic:build_rank_plane");
   // bitwise comparison: -0.0 and 0.0 give identical thresholds, but keep it simple and exact
   if (ctx->plane_valid && std::memcmp(&ctx->plane_approx, &approx, sizeof(double)) == 0) return EBIC_OK;
   ctx->plane_valid = false;
@@ -459,6 +472,7 @@ bool table_allowed(const ebic_ctx* ctx) {
 // allocated (the caller falls back to the slab kernels; not retried for this
 // matrix).
 int ensure_table(ebic_ctx* ctx, double approx, cudaStream_t s) {
+  NvtxRange nvtx_("ebic:build_pair_trend_index");
   if (ctx->table_valid && std::memcmp(&ctx->table_approx, &approx, sizeof(double)) == 0) return EBIC_OK;
   EBIC_TRY(ensure_plane(ctx, approx, s));
   ctx->table_valid = false;
@@ -559,6 +573,7 @@ int lazy_new_epoch(ebic_ctx* ctx, cudaStream_t s) {
 // underestimate is still exact: a pair that finds no free slot is built
 // privately (short vectors) or computed by the count kernel (long ones).
 int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, ebic::LazyArgs* la) {
+  NvtxRange nvtx_("ebic:lazy_reserve");
   const uint64_t vec_bytes = table_wp(ctx) * sizeof(uint32_t);
   if (!ctx->d_lmap) {
     EBIC_CUDA(cudaMalloc(&ctx->d_lmap, lazy_map_bytes(ctx)));
@@ -1671,21 +1686,25 @@ int ebic_ctx_sync(ebic_ctx* ctx) {
 
 int ebic_matrix_upload_f64(ebic_ctx* ctx, const double* row_major, uint64_t n_rows, uint64_t n_cols,
                            uint64_t row_base, int store, int* store_out) {
+  NvtxRange nvtx_("ebic:matrix_upload");
   return upload_impl<double>(ctx, row_major, n_rows, n_cols, row_base, store, store_out);
 }
 
 int ebic_matrix_upload_f32(ebic_ctx* ctx, const float* row_major, uint64_t n_rows, uint64_t n_cols,
                            uint64_t row_base) {
+  NvtxRange nvtx_("ebic:matrix_upload");
   return upload_impl<float>(ctx, row_major, n_rows, n_cols, row_base, EBIC_STORE_F32, nullptr);
 }
 
 int ebic_matrix_upload_device_f64(ebic_ctx* ctx, const double* d_row_major, uint64_t n_rows, uint64_t n_cols,
                                   uint64_t row_base, int store, int* store_out) {
+  NvtxRange nvtx_("ebic:matrix_upload_device");
   return upload_impl<double>(ctx, d_row_major, n_rows, n_cols, row_base, store, store_out, true);
 }
 
 int ebic_matrix_upload_device_f32(ebic_ctx* ctx, const float* d_row_major, uint64_t n_rows, uint64_t n_cols,
                                   uint64_t row_base) {
+  NvtxRange nvtx_("ebic:matrix_upload_device");
   return upload_impl<float>(ctx, d_row_major, n_rows, n_cols, row_base, EBIC_STORE_F32, nullptr, true);
 }
 
@@ -1709,6 +1728,7 @@ int ebic_matrix_free(ebic_ctx* ctx) {
 int ebic_eval_counts_device(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
                             uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
                             void* stream) {
+  NvtxRange nvtx_("ebic:eval_counts_device");
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   if (n_cand && (!d_cols || !d_offsets || !d_counts))
@@ -1721,6 +1741,7 @@ int ebic_eval_counts_device(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_
 
 int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
                      double approx, int negative_trends, uint32_t* counts_out, uint64_t* ticket_out) {
+  NvtxRange nvtx_("ebic:eval_submit");
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   if (n_cand && !counts_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null counts_out");
@@ -1793,6 +1814,7 @@ int ebic_eval_submit(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
 }
 
 int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket) {
+  NvtxRange nvtx_("ebic:eval_wait");
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
   Slot& sl = ctx->slots[ticket % EBIC_MARSHAL_SLOTS];
   if (sl.ticket != ticket) {
@@ -1813,6 +1835,7 @@ int ebic_eval_wait(ebic_ctx* ctx, uint64_t ticket) {
 
 int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
                      double approx, int negative_trends, uint32_t* counts_out) {
+  NvtxRange nvtx_("ebic:eval_counts");
   // Zero-copy when the caller's arrays are already page-locked (cudaHostAlloc /
   // cudaHostRegister / torch pin_memory): the inputs are DMA'd straight from
   // them (ONE copy when the offsets are immediately followed by the columns in
@@ -1948,6 +1971,7 @@ int ebic_eval_counts(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offset
 int ebic_support_rows_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets,
                             uint64_t n_cand, double approx, int negative_trends, uint32_t* rows_out,
                             uint64_t cap, uint64_t* row_offsets) {
+  NvtxRange nvtx_("ebic:support_rows_batch");
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   if (!row_offsets) return fail(EBIC_ERR_INVALID_ARGUMENT, "null row_offsets");
@@ -1995,6 +2019,7 @@ int ebic_support_rows_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t*
 
 int ebic_support_overlap_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32_t* offsets, uint64_t n_cand,
                                double approx, int negative_trends, uint64_t* sizes_out, uint64_t* inter_out) {
+  NvtxRange nvtx_("ebic:support_overlap_batch");
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   if (n_cand > EBIC_OVERLAP_MAX)
@@ -2038,6 +2063,7 @@ int ebic_support_overlap_batch(ebic_ctx* ctx, const uint32_t* cols, const uint32
 
 int ebic_support_rows(ebic_ctx* ctx, const uint32_t* cols, uint32_t len, double approx,
                       int negative_trends, uint32_t* rows_out, uint64_t cap, uint64_t* n_out) {
+  NvtxRange nvtx_("ebic:support_rows");
   const uint32_t offs[2] = {0, len};
   uint64_t ro[2] = {0, 0};
   int st = ebic_support_rows_batch(ctx, cols, offs, 1, approx, negative_trends, rows_out, cap, ro);
@@ -2047,6 +2073,7 @@ int ebic_support_rows(ebic_ctx* ctx, const uint32_t* cols, uint32_t len, double 
 
 int ebic_row_supports(ebic_ctx* ctx, uint64_t row, const uint32_t* cols, uint32_t len, double approx,
                       int negative_trends, int* supports_out) {
+  NvtxRange nvtx_("ebic:row_supports");
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   if (!supports_out) return fail(EBIC_ERR_INVALID_ARGUMENT, "null supports_out");
@@ -2174,6 +2201,7 @@ int ebic_ctx_set_path(ebic_ctx* ctx, int path) {
 }
 
 int ebic_matrix_prepare(ebic_ctx* ctx, double approx) {
+  NvtxRange nvtx_("ebic:matrix_prepare");
   EBIC_TRY(need_matrix(ctx));
   EBIC_TRY(check_approx(approx));
   EBIC_TRY(set_device(ctx));
@@ -2196,6 +2224,7 @@ __attribute__((visibility("hidden"))) int ebic_internal_fail(int code, const cha
 
 int ebic_matrix_load_tsv(ebic_ctx* ctx, const char* path, int n_threads, int store, int* store_out,
                          uint64_t* rows_out, uint64_t* cols_out) {
+  NvtxRange nvtx_("ebic:matrix_load_tsv");
   if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
   uint64_t rows = 0, cols = 0;
   const int st = ebic_tsv_read(path, n_threads, nullptr, 0, &rows, &cols);
@@ -2397,6 +2426,7 @@ int ebic_xchg_destroy(ebic_ctx* ctx) {
 int ebic_eval_counts_rows_sum_async(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets,
                                     uint64_t n_cand, double approx, int negative_trends, uint32_t* d_counts,
                                     void* stream) {
+  NvtxRange nvtx_("ebic:eval_counts_rows_sum_async");
   EBIC_TRY(xchg_ready(ctx, n_cand, d_cols, d_offsets, d_counts));
   EBIC_TRY(set_device(ctx));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
@@ -2411,6 +2441,7 @@ int ebic_xchg_fence(ebic_ctx* ctx, void* stream) {
 
 int ebic_eval_counts_rows_sum(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offsets, uint64_t n_cand,
                               double approx, int negative_trends, uint32_t* d_counts, void* stream) {
+  NvtxRange nvtx_("ebic:eval_counts_rows_sum");
   EBIC_TRY(xchg_ready(ctx, n_cand, d_cols, d_offsets, d_counts));
   EBIC_TRY(set_device(ctx));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;

@@ -120,3 +120,15 @@ def test_header_is_plain_c(tmp_path):
                          capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
     assert subprocess.run([str(tmp_path / "use")]).returncode == 0
+
+
+def test_entry_points_carry_nvtx_ranges(L):
+    """every evaluating entry point and one-time build is an
+    NVTX range ("ebic:<call>") for nsys / ncu --nvtx timelines."""
+    from paper_2105_01196_b200 import build
+
+    blob = build.LIB_PATH.read_bytes()
+    for name in ("eval_counts", "eval_counts_device", "eval_submit", "support_rows_batch", "matrix_upload",
+                 "matrix_prepare", "build_pair_trend_index", "build_rank_plane", "lazy_reserve",
+                 "eval_counts_rows_sum"):
+        assert f"ebic:{name}".encode() in blob, name
