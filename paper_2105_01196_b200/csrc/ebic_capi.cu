@@ -232,6 +232,17 @@ struct ebic_ctx {
   uint32_t* d_lleft = nullptr;      // long vectors: per slot, 32-word chunks still to build
   uint32_t* d_lstart = nullptr;     // long vectors: the count at the batch's start
   uint64_t lkcap = 0;
+  // long vectors: per-batch scratch -- candidates the count kernel deferred
+  // (lazy_deferred_kernel) and each candidate's first 31 pair slots
+  // (lazy_claim_kernel) -- in a ring, so batches on different streams never
+  // share one (a batch reusing a ring entry waits for its previous user)
+  struct LazyScratch {
+    DevBuf<uint32_t> defer, pslot;
+    cudaEvent_t done = nullptr;
+    bool armed = false;
+  };
+  static constexpr int kLazyScratch = 4;
+  LazyScratch lscratch[kLazyScratch];
   uint64_t lcap = 0;                // pool capacity (slots)
   HostBuf<uint32_t> h_lmirror;      // page-locked, mapped: {count at a lazy kernel's start, its batch sequence}
   uint32_t* h_lmirror_dev = nullptr;
@@ -785,25 +796,45 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     // long vectors from the lazy index: claim the batch's missing pairs, build
     // them (ebic_lazy.cuh), then count through the pool
     const uint32_t wp = (uint32_t)table_wp(ctx);
-    EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + plan.la.seq % ebic::kLazyStartRing, ctx->d_lcount, sizeof(uint32_t),
+    auto& sc = ctx->lscratch[plan.la.seq % ebic_ctx::kLazyScratch];
+    if (!sc.done) EBIC_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
+    if (sc.armed) EBIC_CUDA(cudaStreamWaitEvent(s, sc.done, 0));
+    EBIC_TRY(ensure(sc.defer, n_cand + 1));  // (a reallocation's cudaFree waits for the device)
+    EBIC_TRY(ensure(sc.pslot, n_cand * 64));
+    ebic::LazyArgs la = plan.la;
+    la.defer = sc.defer.p;
+    la.pslot = sc.pslot.p;
+    EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + la.seq % ebic::kLazyStartRing, ctx->d_lcount, sizeof(uint32_t),
                               cudaMemcpyDeviceToDevice, s));
     const unsigned cgrid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, (uint64_t)ctx->n_sms * 16);
-    ebic::lazy_claim_kernel<<<cgrid, 256, 0, s>>>(plan.la, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx,
+    ebic::lazy_claim_kernel<<<cgrid, 256, 0, s>>>(la, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx,
                                                   (uint32_t)ctx->n_cols, (wp + 31) / 32, neg);
     const unsigned bgrid = (unsigned)ctx->n_sms * 8;
     if (ctx->store == EBIC_STORE_F64)
-      ebic::lazy_build_kernel<double><<<bgrid, 256, 0, s>>>(plan.la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+      ebic::lazy_build_kernel<double><<<bgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
     else
-      ebic::lazy_build_kernel<float><<<bgrid, 256, 0, s>>>(plan.la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
-    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
+      ebic::lazy_build_kernel<float><<<bgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
     auto go = [&](auto kern) {
+      // a warp per candidate for the whole population (the block scheduler
+      // balances the tail better than a grid-stride loop over fewer warps)
+      const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
       kern<<<grid, 256, 0, s>>>(nullptr, (uint32_t)ctx->n_cols, wp, (uint32_t)ctx->n_rows, d_cols, d_offs,
                                 (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,
-                                ctx->ld / 32, plan.la);
+                                ctx->ld / 32, la);
     };
     if (neg) go(ebic::table_count_warp_multi_kernel<8, true, MASK, true, true>);
     else go(ebic::table_count_warp_multi_kernel<8, false, MASK, true, true>);
-    ctx->launches += 3;
+    // candidates with a pair not in the pool (rare): computed from the store
+    const unsigned dgrid = (unsigned)ctx->n_sms * 2;
+    auto god = [&](auto kern) {
+      kern<<<dgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_cols, wp, (uint32_t)ctx->n_rows, d_cols, d_offs, out, d_mask,
+                                 ctx->ld / 32);
+    };
+    if (neg) god(ebic::lazy_deferred_kernel<true, MASK>);
+    else god(ebic::lazy_deferred_kernel<false, MASK>);
+    EBIC_CUDA(cudaEventRecord(sc.done, s));
+    sc.armed = true;
+    ctx->launches += 4;
     EBIC_CUDA(cudaGetLastError());
     return EBIC_OK;
   }
@@ -812,8 +843,10 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     // in passes of 256 slices (no block barriers; measured 0.44 vs 0.67 ms for
     // the CTA kernel at 200k x 2000, P = 32768).  Few candidates (C5: 1024)
     // keep the CTA kernel, which puts a whole CTA on each.
-    const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
     auto go = [&](auto kern) {
+      // a warp per candidate for the whole population (the block scheduler
+      // balances the tail better than a grid-stride loop over fewer warps)
+      const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
       kern<<<grid, 256, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
                                 d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err,
                                 d_mask, ctx->ld / 32, ebic::LazyArgs{});
@@ -1633,6 +1666,12 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   ebic_xchg_destroy(ctx);
   ctx->d_acc.release();
   ctx->d_done.release();
+  for (auto& sc : ctx->lscratch) {
+    sc.defer.release();
+    sc.pslot.release();
+    if (sc.done) cudaEventDestroy(sc.done);
+    sc.done = nullptr;
+  }
   ctx->h_err1.release();
   for (cudaEvent_t& e : ctx->piece_ev)
     if (e) cudaEventDestroy(e);

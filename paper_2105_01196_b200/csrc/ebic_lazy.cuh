@@ -45,6 +45,8 @@ struct LazyArgs {
   uint32_t* keys;
   uint32_t* left;
   const uint32_t* start;
+  uint32_t* defer;      // [0]: candidates deferred by the count kernel, [1..]: their indices
+  uint32_t* pslot;      // [i * 64 + k (+ 32)]: slot of candidate i's k-th forward (reversed) pair, k < 31
   uint32_t* pool;       // cap x wp words
   uint32_t* count;      // slots handed out
   uint32_t* count_out;  // (optional, host-mapped) {count at kernel start, seq}: the host's lagged view of the fill
@@ -215,15 +217,19 @@ __device__ __forceinline__ uint32_t lazy_lookup(const LazyArgs& la, uint64_t p) 
 //   lazy_claim_kernel  every pair of the batch not in the map is claimed: a
 //                      pool slot t (count), map[p] = t | kSlotBusy (CAS),
 //                      keys[t] = p, left[t] = the vector's 32-word chunks;
+//                      each candidate's first 31 pair slots go to pslot;
 //   lazy_build_kernel  the slots claimed since the batch started ([*start,
 //                      count)) are built, one warp per (chunk, slot) unit,
 //                      chunk-major: the units in flight at once all read the
 //                      same 1024-row slice of the matrix (8 MB at 2000
 //                      columns), which stays in L2; the warp that finishes a
 //                      slot's last chunk publishes it (map[p] = t);
-//   table_count_warp_multi_kernel<..., LAZY>  reads ready vectors from the
-//                      pool and computes any other pair's slices itself
-//                      (pool full, or busy in another stream's batch).
+//   table_count_warp_multi_kernel<..., LAZY>  reads the vectors from the
+//                      pool (slots from pslot, loaded with the columns) and
+//                      defers a candidate with any pair not available (pool
+//                      full, or busy in another stream's batch) to
+//                      lazy_deferred_kernel, which computes such pairs from
+//                      the value store.
 // ---------------------------------------------------------------------------
 // Batches may run on several streams at once (the device API takes the
 // caller's stream), so a build kernel's slot window [start, count) can hold
@@ -235,24 +241,51 @@ constexpr uint32_t kLazyKeyBits = 26;
 constexpr uint32_t kLazyStartRing = 64;
 __host__ __device__ __forceinline__ uint32_t lazy_tag(uint32_t seq) { return seq % 63u; }
 
-__device__ __forceinline__ void lazy_claim_pair(const LazyArgs& la, uint64_t p, uint32_t n_chunks) {
-  if (lazy_lookup(la, p) != kSlotEmpty) return;  // ready, or claimed already
-  const uint32_t t = atomicAdd(la.count, 1u);
-  if (t >= la.cap) return;  // pool full: the count kernel computes this pair itself
-  const uint32_t old = atomicCAS(la.map + p, kSlotEmpty, t | kSlotBusy);
-  if (old == kSlotEmpty) {  // (otherwise another thread claimed p first: slot t stays unused)
-    la.left[t] = n_chunks;
-    la.keys[t] = (uint32_t)p | (lazy_tag(la.seq) << kLazyKeyBits);
-  }
+// Did this batch claim slot s for pair p?  (A claim's key is written right
+// after its CAS: a reader that comes too early answers "no", which only
+// defers the candidate to lazy_deferred_kernel.)
+__device__ __forceinline__ bool lazy_own_claim(const LazyArgs& la, uint32_t s, uint64_t p) {
+  uint32_t k;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(k) : "l"(la.keys + s) : "memory");
+  return k == ((uint32_t)p | (lazy_tag(la.seq) << kLazyKeyBits));
 }
 
+// The slot this batch will find pair p in once its build kernel has run:
+// a ready slot, a slot this batch claims now (or claimed already, in another
+// warp), or kSlotEmpty -- the pool is full, or another stream's batch is
+// building p -- which defers the candidate.
+__device__ __forceinline__ uint32_t lazy_claim_pair(const LazyArgs& la, uint64_t p, uint32_t n_chunks) {
+  uint32_t v = lazy_lookup(la, p);
+  if (v == kSlotEmpty) {
+    const uint32_t t = atomicAdd(la.count, 1u);
+    if (t >= la.cap) return kSlotEmpty;  // pool full
+    v = atomicCAS(la.map + p, kSlotEmpty, t | kSlotBusy);
+    if (v == kSlotEmpty) {  // ours (otherwise another thread claimed p first: slot t stays unused)
+      la.left[t] = n_chunks;
+      __threadfence();  // left before the key: the build kernel reads the key first
+      la.keys[t] = (uint32_t)p | (lazy_tag(la.seq) << kLazyKeyBits);
+      return t;
+    }
+  }
+  if (slot_ready(v)) return v;
+  const uint32_t s = v & ~kSlotBusy;
+  return lazy_own_claim(la, s, p) ? s : kSlotEmpty;
+}
+
+// Claims the batch's missing pairs and records, per candidate, the slots of
+// its first 31 forward (and reversed) pairs: pslot[i * 64 + k] (+ 32), so the
+// count kernel loads them next to the columns instead of looking them up
+// after the columns arrive (one dependent round trip less per candidate).
 __global__ void __launch_bounds__(256)
 lazy_claim_kernel(const LazyArgs la, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs,
                   uint32_t n_cand, uint32_t n_idx, uint32_t n_cols, uint32_t n_chunks, int neg) {
-  if (la.count_out && blockIdx.x == 0 && threadIdx.x == 0) {  // the host's lagged view of the pool's fill
-    la.count_out[0] = *(volatile uint32_t*)la.count;
-    __threadfence_system();
-    la.count_out[1] = la.seq;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    la.defer[0] = 0;  // (read by this batch's count kernel, which runs after this one)
+    if (la.count_out) {  // the host's lagged view of the pool's fill
+      la.count_out[0] = *(volatile uint32_t*)la.count;
+      __threadfence_system();
+      la.count_out[1] = la.seq;
+    }
   }
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -261,9 +294,14 @@ lazy_claim_kernel(const LazyArgs la, const uint32_t* __restrict__ cols, const ui
     if (e <= b || e > n_idx) continue;  // (reported by the count kernel)
     for (uint32_t k = b + 1 + lane; k < e; k += 32) {
       const uint32_t x = __ldg(cols + k - 1), y = __ldg(cols + k);
-      if (x >= n_cols || y >= n_cols) continue;
-      lazy_claim_pair(la, (uint64_t)x * n_cols + y, n_chunks);
-      if (neg) lazy_claim_pair(la, (uint64_t)y * n_cols + x, n_chunks);
+      if (x >= n_cols || y >= n_cols) continue;  // (reported by the count kernel)
+      const uint32_t sf = lazy_claim_pair(la, (uint64_t)x * n_cols + y, n_chunks);
+      const uint32_t sr = neg ? lazy_claim_pair(la, (uint64_t)y * n_cols + x, n_chunks) : kSlotEmpty;
+      const uint32_t q = k - b - 1;  // pair index
+      if (q < 31) {
+        la.pslot[(uint64_t)i * 64 + q] = sf;
+        if (neg) la.pslot[(uint64_t)i * 64 + 32 + q] = sr;
+      }
     }
   }
 }

@@ -418,9 +418,13 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
 //
 // LAZY (long vectors only, MULTI): the vectors come from the lazy index's
 // pool, built ahead of this kernel by lazy_claim_kernel / lazy_build_kernel
-// (ebic_lazy.cuh); a pair whose slot is not ready (the pool was full, or
-// another stream's batch is still building it) is computed here, slice by
-// slice, from the value store -- the same bits either way.
+// (ebic_lazy.cuh).  A candidate with a pair whose slot is not ready (the pool
+// was full, or another stream's batch is still building it) is deferred to
+// lazy_deferred_kernel, which computes such pairs from the value store -- the
+// same bits either way -- so this kernel keeps the register budget of the
+// plain index kernel.  (A persistent, software-pipelined variant of this
+// kernel -- the next candidate's offsets, columns and slots fetched during the
+// current one's passes -- measured 0.70 vs 0.44 ms at C4 and was dropped.)
 template <int J, bool NEG, bool MASK, bool MULTI = true, bool LAZY = false>
 __global__ void __launch_bounds__(256)
 table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
@@ -458,10 +462,22 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
     // (pair lane -> lane + 1), looked up once for all passes
     uint32_t sf_lane = kSlotEmpty, sr_lane = kSlotEmpty;
     if (LAZY) {
-      const uint32_t c_n = __shfl_down_sync(kFull, c_lane, 1);
+      // the slots lazy_claim_kernel recorded for the first 31 pairs (claimed
+      // ones are built by now); the later pairs are looked up in the map
+      bool ready = true;
       if (lane < 31 && (uint32_t)lane + 1 < L) {
-        sf_lane = lazy_lookup(la, (uint64_t)c_lane * n_cols + c_n);
-        if (NEG) sr_lane = lazy_lookup(la, (uint64_t)c_n * n_cols + c_lane);
+        sf_lane = __ldg(la.pslot + (uint64_t)i * 64 + lane);
+        if (NEG) sr_lane = __ldg(la.pslot + (uint64_t)i * 64 + 32 + lane);
+        ready = slot_ready(sf_lane) && (!NEG || slot_ready(sr_lane));
+      }
+      for (uint32_t k = 32 + lane; k < L; k += 32) {  // pairs past the lanes
+        const uint32_t x = __ldg(cols + b + k - 1), y = __ldg(cols + b + k);
+        ready = ready && slot_ready(lazy_lookup(la, (uint64_t)x * n_cols + y)) &&
+                (!NEG || slot_ready(lazy_lookup(la, (uint64_t)y * n_cols + x)));
+      }
+      if (!__all_sync(kFull, ready)) {
+        if (lane == 0) la.defer[1 + atomicAdd(la.defer, 1u)] = i;
+        continue;
       }
     }
     uint32_t n = 0;
@@ -492,22 +508,13 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
                                               : lazy_lookup(la, (uint64_t)cc * n_cols + cp);
           sf = __shfl_sync(kFull, sf, 0);  // one view per warp
           sr = __shfl_sync(kFull, sr, 0);
-          if (slot_ready(sf)) {
 #pragma unroll
-            for (int u = 0; u < J; ++u) x[u] = __ldcg(t4 + (uint64_t)sf * nv + min(v0 + u * 32 + lane, nv - 1));
-          } else {
-#pragma unroll
-            for (int u = 0; u < J; ++u) x[u] = pair_slice_thread(la, n_rows, cp, cc, min(v0 + u * 32 + lane, nv - 1));
-          }
-          if (NEG) {
-            if (slot_ready(sr)) {
-#pragma unroll
-              for (int u = 0; u < J; ++u) y[u] = __ldcg(t4 + (uint64_t)sr * nv + min(v0 + u * 32 + lane, nv - 1));
-            } else {
-#pragma unroll
-              for (int u = 0; u < J; ++u)
-                y[u] = pair_slice_thread(la, n_rows, cc, cp, min(v0 + u * 32 + lane, nv - 1));
-            }
+          for (int u = 0; u < J; ++u) {
+            const uint32_t v = min(v0 + u * 32 + lane, nv - 1);
+            // (every pair is ready: checked above.  A slot's bits never change
+            // while it is ready, so the read-only path is safe for them.)
+            x[u] = __ldg(t4 + (uint64_t)sf * nv + v);
+            if (NEG) y[u] = __ldg(t4 + (uint64_t)sr * nv + v);
           }
         } else if constexpr (MULTI) {
 #pragma unroll
@@ -941,6 +948,58 @@ table_count_tma_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uint
     c_lane = cn;
     sf_lane = sfn;
     sr_lane = srn;
+  }
+}
+
+// The candidates the count kernel deferred (a pair not ready in the pool):
+// a warp per candidate, one uint4 slice per lane at a time, ready pairs from
+// the pool and the others computed from the value store (pair_slice_thread).
+// Rare (a full pool, or batches on several streams sharing pairs), so simple.
+template <bool NEG, bool MASK>
+__global__ void __launch_bounds__(256)
+lazy_deferred_kernel(const LazyArgs la, uint32_t n_cols, uint32_t wp, uint32_t n_rows,
+                     const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs,
+                     uint32_t* __restrict__ out, uint32_t* __restrict__ mask, uint64_t mask_wpc) {
+  const uint32_t n_def = *(volatile uint32_t*)la.defer;
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  const uint32_t nv = wp / 4;
+  const uint4* p4 = reinterpret_cast<const uint4*>(la.pool);
+  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n_def; d += warps) {
+    const uint32_t i = la.defer[1 + d];
+    const uint32_t b = __ldg(offs + i), L = __ldg(offs + i + 1) - b;  // (validated by the count kernel)
+    uint32_t n = 0;
+    for (uint32_t v0 = 0; v0 < nv; v0 += 32) {
+      const uint32_t v = min(v0 + lane, nv - 1);
+      uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u), r = NEG ? f : make_uint4(0u, 0u, 0u, 0u);
+      uint32_t cp = __ldg(cols + b);
+      for (uint32_t k = 1; k < L; ++k) {
+        const uint32_t cc = __ldg(cols + b + k);
+        const uint32_t sf = lazy_lookup(la, (uint64_t)cp * n_cols + cc);
+        const uint4 x = slot_ready(sf) ? __ldcg(p4 + (uint64_t)sf * nv + v) : pair_slice_thread(la, n_rows, cp, cc, v);
+        f.x &= x.x; f.y &= x.y; f.z &= x.z; f.w &= x.w;
+        if (NEG) {
+          const uint32_t sr = lazy_lookup(la, (uint64_t)cc * n_cols + cp);
+          const uint4 y = slot_ready(sr) ? __ldcg(p4 + (uint64_t)sr * nv + v) : pair_slice_thread(la, n_rows, cc, cp, v);
+          r.x &= y.x; r.y &= y.y; r.z &= y.z; r.w &= y.w;
+        }
+        cp = cc;
+      }
+      const uint4 o = NEG ? make_uint4(f.x | r.x, f.y | r.y, f.z | r.z, f.w | r.w) : f;
+      if (v0 + lane < nv) {
+        n += __popc(o.x) + __popc(o.y) + __popc(o.z) + __popc(o.w);
+        if (MASK) {
+          uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
+          const uint32_t words[4] = {index_to_natural(o.x), index_to_natural(o.y), index_to_natural(o.z),
+                                     index_to_natural(o.w)};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (4 * v + q < mask_wpc) mw[q] = words[q];
+        }
+      }
+    }
+    n = __reduce_add_sync(kFull, n);
+    if (lane == 0) out[i] = n;
   }
 }
 
