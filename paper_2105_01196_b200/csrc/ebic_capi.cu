@@ -812,8 +812,13 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     const unsigned bgrid = (unsigned)ctx->n_sms * 8;
     if (ctx->store == EBIC_STORE_F64)
       ebic::lazy_build_kernel<double><<<bgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
-    else
-      ebic::lazy_build_kernel<float><<<bgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+    else {
+      const size_t smem = 8 * ebic::kStageFloats * sizeof(float);
+      EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(ebic::lazy_build_kernel<float>), ctx));
+      const unsigned fgrid = (unsigned)ctx->n_sms *
+          (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(ebic::lazy_build_kernel<float>), 256, smem));
+      ebic::lazy_build_kernel<float><<<fgrid, 256, smem, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+    }
     auto go = [&](auto kern) {
       // a warp per candidate for the whole population (the block scheduler
       // balances the tail better than a grid-stride loop over fewer warps)

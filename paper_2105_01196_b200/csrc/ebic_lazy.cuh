@@ -28,8 +28,10 @@
 // built vector is the same bits the full-index builder produces.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "ebic_kernels.cuh"
+#include "ebic_index.cuh"
 
 namespace ebic {
 
@@ -74,13 +76,6 @@ __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-// Row of a 32-row word evaluated by `lane`: with lane l on the row of word
-// bit l (index_bit_row, ebic_table.cuh), a ballot over the warp is the index
-// word itself.
-__device__ __forceinline__ uint32_t index_row_of_lane(int lane) {
-  return 16u * ((uint32_t)lane >> 4) + (((uint32_t)lane >> 3) & 1u) + 2u * ((uint32_t)lane & 7u);
-}
-
 // One row's bit of B(a, b): trend.cpp:22 in double, two rounded ops (thr64).
 __device__ __forceinline__ bool pair_bit(double x, double y, const PairThr& th) { return y > thr64(x, th.approx); }
 // float32 store: y > thr64(x) decided by the float32 bracket [t - d, t + d]
@@ -100,34 +95,104 @@ __device__ __forceinline__ bool pair_row_bit(const T* __restrict__ ca, const T* 
   return pair_bit(__ldg(ca + r), __ldg(cb + r), th);
 }
 
-// Words w0 .. w0 + 31 of B(a, b), computed by the warp: lane l returns word
-// w0 + l.  Each ballot is one word (lane l tests row index_row_of_lane(l) of
-// it).  The loads of 8 words are issued (clamped to valid rows) before any
-// test, so the occasional exact double test never serialises them.
+// Word w of B(a, b) (rows 32 w .. 32 w + 31) by one thread: its 32 rows of
+// both columns are read as 16-byte vectors (8 rows of each column in flight
+// at a time) and tested with no cross-lane traffic, so a warp fills 32 words
+// at once (round 2 used a ballot per word: ~41 warp-instructions per word,
+// 31 ms for C4's 98K first-visit vectors).
+// Rows past the column's allocation (ld) are not read; rows >= n_rows are
+// masked out.
 template <typename T>
-__device__ __forceinline__ uint32_t pair_chunk_warp(const T* __restrict__ ca, const T* __restrict__ cb,
-                                                    uint32_t n_rows, uint32_t w0, const PairThr& th, int lane) {
-  constexpr int B = 8;
-  const uint32_t rl = index_row_of_lane(lane);
-  const uint32_t last = n_rows - 1;
-  uint32_t mine = 0;
-#pragma unroll 1
-  for (int j0 = 0; j0 < 32; j0 += B) {
-    T x[B], y[B];
+__device__ __forceinline__ uint32_t pair_word_lane(const T* __restrict__ ca, const T* __restrict__ cb, uint32_t n_rows,
+                                                   uint64_t ld, uint32_t w, const PairThr& th) {
+  constexpr int VW = 16 / sizeof(T);  // rows per 16-byte vector
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  const uint32_t r0 = 32u * w;
+  const bool whole = (uint64_t)r0 + 32 <= ld;
+  uint32_t word = 0;
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-      const uint32_t r = min(32u * (w0 + j0 + i) + rl, last);
-      x[i] = __ldg(ca + r);
-      y[i] = __ldg(cb + r);
+  for (int g = 0; g < 32; g += 8) {
+    T x[8], y[8];
+    if (whole) {
+#pragma unroll
+      for (int q = 0; q < 8; q += VW) {
+        const V va = __ldg(reinterpret_cast<const V*>(ca + r0 + g + q));
+        const V vb = __ldg(reinterpret_cast<const V*>(cb + r0 + g + q));
+        const T* pa = reinterpret_cast<const T*>(&va);
+        const T* pb = reinterpret_cast<const T*>(&vb);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          x[q + e] = pa[e];
+          y[q + e] = pb[e];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t r = r0 + g + j;
+        x[j] = r < n_rows ? __ldg(ca + r) : (T)0;
+        y[j] = r < n_rows ? __ldg(cb + r) : (T)0;
+      }
     }
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-      const bool bit = pair_bit(x[i], y[i], th) && 32u * (w0 + j0 + i) + rl < n_rows;
-      const uint32_t word = __ballot_sync(kFull, bit);
-      mine = lane == j0 + i ? word : mine;
+    for (int j = 0; j < 8; ++j)
+      if (pair_bit(x[j], y[j], th)) word |= 1u << index_row_bit((uint32_t)(g + j));
+  }
+  return word & index_valid_bits(n_rows, w);
+}
+
+// Words w0 .. w0 + 31 of B(a, b) for a float32 store, lane l returning word
+// w0 + l, through shared memory: the warp reads the chunk's 1024 rows of both
+// columns with coalesced 16-byte loads into `st` (2 x 32 x 33 floats, row r
+// at (r / 32) * 33 + r % 32: conflict-free both ways), then each lane tests
+// its own 32 rows.  (pair_word_lane reads a lane's 128-B row runs directly;
+// with 64 warps per SM those lines leave L1 before their 8 loads are done.)
+constexpr uint32_t kStageFloats = 2 * 32 * 33;
+__device__ __forceinline__ uint32_t pair_word_staged(const float* __restrict__ ca, const float* __restrict__ cb,
+                                                     uint32_t n_rows, uint64_t ld, uint32_t w0, const PairThr& th,
+                                                     int lane, float* st) {
+  float* sx = st;
+  float* sy = st + 32 * 33;
+  const uint32_t r0 = 32u * w0;
+  if ((uint64_t)r0 + 1024 <= ld) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t r = 128u * k + 4u * lane;  // 4 rows per lane per k
+      const float4 va = __ldg(reinterpret_cast<const float4*>(ca + r0 + r));
+      const float4 vb = __ldg(reinterpret_cast<const float4*>(cb + r0 + r));
+      const uint32_t o = (r >> 5) * 33u + (r & 31u);
+      sx[o] = va.x; sx[o + 1] = va.y; sx[o + 2] = va.z; sx[o + 3] = va.w;
+      sy[o] = vb.x; sy[o + 1] = vb.y; sy[o + 2] = vb.z; sy[o + 3] = vb.w;
+    }
+  } else {  // the column's last chunk: rows past ld are not read
+    for (uint32_t r = lane; r < 1024; r += 32) {
+      const uint32_t o = (r >> 5) * 33u + (r & 31u);
+      sx[o] = r0 + r < n_rows ? __ldg(ca + r0 + r) : 0.f;
+      sy[o] = r0 + r < n_rows ? __ldg(cb + r0 + r) : 0.f;
     }
   }
-  return mine;
+  __syncwarp();
+  // branch-free float32 bracket per row (bit set above it, `unc` inside it);
+  // the rare rows inside the bracket get the exact double test afterwards
+  uint32_t word = 0, unc = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float x = sx[lane * 33 + j], y = sy[lane * 33 + j];
+    const float ax = fabsf(x);
+    const float t = __fmaf_rn(-th.a_f, ax, x);
+    const float d = __fmaf_rn(th.kscale, ax, 0x1p-146f);
+    const uint32_t bit = 1u << index_row_bit((uint32_t)j);
+    word |= y > __fadd_rn(t, d) ? bit : 0u;
+    unc |= (y > __fsub_rn(t, d) && !(y > __fadd_rn(t, d))) ? (1u << j) : 0u;
+  }
+  while (unc) {
+    const int j = __ffs(unc) - 1;
+    unc &= unc - 1;
+    const float x = sx[lane * 33 + j], y = sy[lane * 33 + j];
+    if ((double)y > thr64((double)x, th.approx)) word |= 1u << index_row_bit((uint32_t)j);
+  }
+  __syncwarp();  // (the stage is refilled by the warp's next unit)
+  return word & index_valid_bits(n_rows, w0 + lane);
 }
 
 // The warp builds the wp-word vector B(a, b) and hands word w to `emit(w, word)`
@@ -139,7 +204,7 @@ __device__ __forceinline__ void build_pair_vector_warp_t(const T* __restrict__ m
   const T* ca = mat + (uint64_t)a * ld;
   const T* cb = mat + (uint64_t)b * ld;
   for (uint32_t w0 = 0; w0 < wp; w0 += 32) {
-    const uint32_t mine = pair_chunk_warp(ca, cb, n_rows, w0, th, lane);
+    const uint32_t mine = pair_word_lane(ca, cb, n_rows, ld, w0 + lane, th);
     if (w0 + lane < wp) emit(w0 + lane, mine);
   }
 }
@@ -162,16 +227,8 @@ __device__ __noinline__ uint4 pair_slice_thread_t(const T* __restrict__ mat, uin
   const T* ca = mat + (uint64_t)a * ld;
   const T* cb = mat + (uint64_t)b * ld;
   uint32_t w[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t word = 0;
-    const uint32_t r0 = 128u * v + 32u * q;
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t r = r0 + index_row_of_lane(j);
-      if (r < n_rows && pair_row_bit(ca, cb, r, th)) word |= 1u << j;
-    }
-    w[q] = word;
-  }
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) w[q] = pair_word_lane(ca, cb, n_rows, ld, 4u * v + q, th);
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -318,6 +375,7 @@ lazy_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t 
   const int lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const T* mat = static_cast<const T*>(la.mat);
+  extern __shared__ float stage[];  // float stores: kStageFloats per warp (pair_word_staged)
   for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < total; u += warps) {
     const uint32_t chunk = (uint32_t)(u / n_jobs), t = start + (uint32_t)(u % n_jobs);
     const uint32_t tk = __ldcg(la.keys + t);
@@ -325,8 +383,14 @@ lazy_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t 
     const uint32_t key = tk & ((1u << kLazyKeyBits) - 1u);
     const uint32_t a = key / n_cols, b = key % n_cols;
     const uint32_t w0 = chunk * 32;
-    const uint32_t word = pair_chunk_warp(mat + (uint64_t)a * la.ld, mat + (uint64_t)b * la.ld, n_rows, w0,
-                                          pair_thr(la), lane);
+    uint32_t word;
+    if constexpr (sizeof(T) == 4) {
+      word = pair_word_staged(mat + (uint64_t)a * la.ld, mat + (uint64_t)b * la.ld, n_rows, la.ld, w0,
+                              pair_thr(la), lane, stage + (threadIdx.x >> 5) * kStageFloats);
+    } else {
+      word = pair_word_lane(mat + (uint64_t)a * la.ld, mat + (uint64_t)b * la.ld, n_rows, la.ld, w0 + lane,
+                            pair_thr(la));
+    }
     if (w0 + lane < wp) la.pool[(uint64_t)t * wp + w0 + lane] = word;
     __threadfence();
     __syncwarp();
