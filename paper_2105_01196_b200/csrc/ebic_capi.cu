@@ -187,10 +187,9 @@ struct ebic_ctx {
   cudaEvent_t xchg_cdone[kXchgDepth] = {}, xchg_xdone[kXchgDepth] = {};
   bool xchg_xdone_armed[kXchgDepth] = {};
   DevBuf<uint32_t> d_xchg_local[kXchgDepth];       // this rank's partial counts, per ring slot
-  // staged upload of pageable host matrices (staged_h2d): per worker thread
-  // one page-locked staging buffer, a stream and an event, kept across uploads
+  // staged upload of pageable host matrices (staged_h2d): per worker thread a
+  // stream and an event (the page-locked buffers are process-wide)
   struct Stager {
-    HostBuf<unsigned char> buf;
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
     bool armed = false;
@@ -1351,13 +1350,34 @@ void drop_matrix(ebic_ctx* ctx, bool keep_index_alloc) {
 // 16-thread copy into page-locked memory, 29 ms for a page-locked DMA
 // (profiles/r2_host_copy.txt).  `s` waits for every chunk's DMA.
 constexpr size_t kStageChunk = 8u << 20;
+constexpr int kStageThreads = 8;
+// The page-locked staging buffers are shared by every context of the process
+// (cudaHostAllocPortable): a page-locked allocation costs ~0.45 ms per MB on
+// the B200 host, so each context paying for its own made a context's first
+// upload 56 ms slower.  Uploads through them are serialised by `mu`.
+struct StagePool {
+  std::mutex mu;
+  std::vector<unsigned char*> bufs;
+};
+StagePool& stage_pool() {
+  static StagePool* p = new StagePool;  // (never freed: lives as long as the process)
+  return *p;
+}
+
 int staged_h2d(ebic_ctx* ctx, void* d_dst, const void* h_src, size_t bytes, cudaStream_t s) {
   const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  const int T = (int)std::max<size_t>(1, std::min<size_t>({(size_t)std::min(hw, 16), bytes / (4 * kStageChunk)}));
+  const int T = (int)std::max<size_t>(1, std::min<size_t>({(size_t)std::min(hw, kStageThreads), bytes / (4 * kStageChunk)}));
+  StagePool& sp = stage_pool();
+  std::lock_guard<std::mutex> lock(sp.mu);
+  const double ta = host_ms();
+  while ((int)sp.bufs.size() < T) {
+    unsigned char* b = nullptr;
+    EBIC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b), kStageChunk, cudaHostAllocPortable));
+    sp.bufs.push_back(b);
+  }
   if ((int)ctx->stagers.size() < T) ctx->stagers.resize(T);
   for (int t = 0; t < T; ++t) {
     auto& st = ctx->stagers[t];
-    EBIC_TRY(ensure(st.buf, kStageChunk));
     if (!st.stream) EBIC_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
     if (!st.done) EBIC_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
     // (the destination may still be in use by work queued on s)
@@ -1365,17 +1385,18 @@ int staged_h2d(ebic_ctx* ctx, void* d_dst, const void* h_src, size_t bytes, cuda
     EBIC_CUDA(cudaStreamWaitEvent(st.stream, st.done, 0));
     st.armed = false;
   }
+  if (std::getenv("EBIC_UPLOAD_TRACE")) std::fprintf(stderr, "upload: staging setup %.1f ms (%d threads)\n", host_ms() - ta, T);
   const size_t n_chunks = (bytes + kStageChunk - 1) / kStageChunk;
   std::vector<cudaError_t> errs(T, cudaSuccess);
   auto work = [&](int t) {
     auto& st = ctx->stagers[t];
+    unsigned char* buf = sp.bufs[t];
     cudaSetDevice(ctx->device);
     for (size_t k = t; k < n_chunks && errs[t] == cudaSuccess; k += T) {
       const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
       if (st.armed && (errs[t] = cudaEventSynchronize(st.done)) != cudaSuccess) break;
-      std::memcpy(st.buf.p, static_cast<const unsigned char*>(h_src) + off, len);
-      errs[t] = cudaMemcpyAsync(static_cast<unsigned char*>(d_dst) + off, st.buf.p, len, cudaMemcpyHostToDevice,
-                                st.stream);
+      std::memcpy(buf, static_cast<const unsigned char*>(h_src) + off, len);
+      errs[t] = cudaMemcpyAsync(static_cast<unsigned char*>(d_dst) + off, buf, len, cudaMemcpyHostToDevice, st.stream);
       if (errs[t] == cudaSuccess) errs[t] = cudaEventRecord(st.done, st.stream);
       st.armed = true;
     }
@@ -1389,6 +1410,8 @@ int staged_h2d(ebic_ctx* ctx, void* d_dst, const void* h_src, size_t bytes, cuda
     EBIC_CUDA(cudaEventRecord(ctx->stagers[t].done, ctx->stagers[t].stream));
     EBIC_CUDA(cudaStreamWaitEvent(s, ctx->stagers[t].done, 0));
   }
+  // the shared buffers may be refilled by the next upload: wait for the DMAs
+  for (int t = 0; t < T; ++t) EBIC_CUDA(cudaEventSynchronize(ctx->stagers[t].done));
   return EBIC_OK;
 }
 
@@ -1432,7 +1455,9 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   if (src_on_device) {
     d_in = const_cast<TI*>(host);
   } else {
+    const double t0 = host_ms();
     EBIC_CUDA(cudaMalloc(&d_in, n * sizeof(TI)));
+    const double t1 = host_ms();
     if (n * sizeof(TI) >= 4 * kStageChunk && pageable(host)) {
       if (staged_h2d(ctx, d_in, host, n * sizeof(TI), s) != EBIC_OK) {
         cudaFree(d_in);
@@ -1440,6 +1465,10 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
       }
     } else {
       ce = cudaMemcpyAsync(d_in, host, n * sizeof(TI), cudaMemcpyHostToDevice, s);
+    }
+    if (std::getenv("EBIC_UPLOAD_TRACE")) {
+      cudaStreamSynchronize(s);
+      std::fprintf(stderr, "upload: malloc %.1f ms, h2d %.1f ms\n", t1 - t0, host_ms() - t1);
     }
   }
   auto release_in = [&]() {
@@ -1689,7 +1718,6 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
   for (cudaEvent_t& e : ctx->ev_build)
     if (e) cudaEventDestroy(e);
   for (auto& st : ctx->stagers) {
-    st.buf.release();
     if (st.stream) cudaStreamDestroy(st.stream);
     if (st.done) cudaEventDestroy(st.done);
   }
