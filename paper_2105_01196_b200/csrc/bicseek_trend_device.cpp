@@ -274,7 +274,7 @@ struct Deps {
 // EBIC_SHIM_STATS=1: per-kind call counts and time spent verifying the
 // cached matrix, printed to stderr at exit (diagnostics).
 struct ShimStats {
-  std::atomic<uint64_t> calls[3] = {}, ns[3] = {};
+  std::atomic<uint64_t> calls[3] = {}, ns[3] = {}, bind_ns{0}, binds{0};
   bool on = [] {
     const char* e = std::getenv("EBIC_SHIM_STATS");
     return e && e[0] == '1';
@@ -285,6 +285,8 @@ struct ShimStats {
     for (int k = 0; k < 3; ++k)
       std::fprintf(stderr, "shim %s: %llu calls, %.3f ms verifying the cached matrix\n", names[k],
                    (unsigned long long)calls[k].load(), ns[k].load() / 1e6);
+    std::fprintf(stderr, "shim: %llu uploads (+ shadow copies), %.3f ms\n", (unsigned long long)binds.load(),
+                 bind_ns.load() / 1e6);
   }
 };
 ShimStats g_stats;
@@ -322,6 +324,7 @@ ebic_ctx* bind(const ExpressionMatrix& m, const Deps& deps = Deps{}) {
   const bool same = s.key == v.data() && s.rows == m.rows() && s.cols == m.cols() &&
                     (trust_pointer() || unchanged(s, v, m.cols(), deps));
   if (!same) {
+    const auto t0 = std::chrono::steady_clock::now();
     s.key = nullptr;
     check(ebic_matrix_upload_f64(s.ctx, v.data(), m.rows(), m.cols(), 0, EBIC_STORE_AUTO, nullptr),
           "matrix upload");
@@ -329,6 +332,11 @@ ebic_ctx* bind(const ExpressionMatrix& m, const Deps& deps = Deps{}) {
     s.rows = m.rows();
     s.cols = m.cols();
     if (!trust_pointer()) s.shadow.assign(v.data(), v.size());
+    if (g_stats.on) {
+      g_stats.binds++;
+      g_stats.bind_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                             std::chrono::steady_clock::now() - t0).count();
+    }
   }
   return s.ctx;
 }
