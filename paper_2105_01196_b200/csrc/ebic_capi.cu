@@ -551,7 +551,7 @@ constexpr double kLazyRentFrac = 0.5;                // ski rental: buy the full
 bool lazy_allowed(const ebic_ctx* ctx) {
   if (!(ctx->path == EBIC_PATH_AUTO || ctx->path == EBIC_PATH_LAZY)) return false;
   const uint64_t C = ctx->n_cols;
-  return C >= 1 && C <= kLazyMaxCols && ctx->table_kernel != 1 && ctx->table_kernel != 2;
+  return C >= 1 && C <= kLazyMaxCols;  // (the lazy index runs its own kernels whatever EBIC_TABLE_KERNEL says)
 }
 
 uint64_t lazy_map_bytes(const ebic_ctx* ctx) { return ctx->n_cols * ctx->n_cols * sizeof(uint32_t); }

@@ -326,6 +326,36 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
       f[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
       r[u] = NEG ? f[u] : make_uint4(0u, 0u, 0u, 0u);
     }
+    const uint32_t lv = J == 1 ? min((uint32_t)lane, nv - 1) : (uint32_t)lane;
+    if constexpr (!NEG) {
+      // software-pipelined: pair k + 1's J loads are in flight while pair k is
+      // combined (as in the multi-pass kernel)
+      auto col = [&](uint32_t j) -> uint32_t { return j < 32 ? __shfl_sync(kFull, c_lane, j & 31) : __ldg(cols + b + j); };
+      auto vec = [&](uint32_t k) -> const uint4* {
+        return t4 + ((uint64_t)col(k - 1) * n_cols + col(k)) * nv + lv;
+      };
+      uint4 xa[J];
+      {
+        const uint4* p0 = vec(1);
+#pragma unroll
+        for (int u = 0; u < J; ++u) xa[u] = __ldg(p0 + u * 32);
+      }
+      for (uint32_t k = 1; k + 1 < L; ++k) {
+        const uint4* pn = vec(k + 1);
+        uint4 xb[J];
+#pragma unroll
+        for (int u = 0; u < J; ++u) xb[u] = __ldg(pn + u * 32);
+#pragma unroll
+        for (int u = 0; u < J; ++u) {
+          f[u].x &= xa[u].x; f[u].y &= xa[u].y; f[u].z &= xa[u].z; f[u].w &= xa[u].w;
+          xa[u] = xb[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < J; ++u) {
+        f[u].x &= xa[u].x; f[u].y &= xa[u].y; f[u].z &= xa[u].z; f[u].w &= xa[u].w;
+      }
+    } else {
     uint32_t cp = __shfl_sync(kFull, c_lane, 0);
     for (uint32_t k = 1; k < L; ++k) {
       const uint32_t cc = k < 32 ? __shfl_sync(kFull, c_lane, k & 31) : __ldg(cols + b + k);
@@ -335,7 +365,6 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
       // more than 32 slices to a multiple of 32 (nv == 32 J); below that the
       // lanes past the vector re-read its last slice (same line; their
       // accumulators start at 0)
-      const uint32_t lv = J == 1 ? min((uint32_t)lane, nv - 1) : (uint32_t)lane;
       const uint4* fwd = t4 + ((uint64_t)cp * n_cols + cc) * nv + lv;
       const uint4* rev = t4 + ((uint64_t)cc * n_cols + cp) * nv + lv;
       uint4 x[J], y[J];
@@ -352,6 +381,7 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
         }
       }
       cp = cc;
+    }
     }
     uint32_t n = 0;
 #pragma unroll
@@ -439,10 +469,67 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
         ready = ready && slot_ready(lazy_lookup(la, (uint64_t)x * n_cols + y)) &&
                 (!NEG || slot_ready(lazy_lookup(la, (uint64_t)y * n_cols + x)));
       }
+      if (!NEG) ready = ready && L <= 32;  // (the pipelined loop takes every slot from a lane register)
       if (!__all_sync(kFull, ready)) {
         if (lane == 0) la.defer[1 + atomicAdd(la.defer, 1u)] = i;
         continue;
       }
+    }
+    if constexpr (MULTI && !NEG) {
+      // Software-pipelined over the candidate's pairs: pair k + 1's J loads are
+      // in flight while pair k is combined.  (The plain loop below kept only
+      // ~3 of its 8 loads in flight when fed from lazy pool slots -- ptxas
+      // reused their registers -- and ran C4 at 0.58 ms; pipelined, the lazy
+      // pool runs at 0.41 ms.)
+      // base of pair k's vector (pair k joins columns k - 1 and k)
+      auto col = [&](uint32_t j) -> uint32_t { return j < 32 ? __shfl_sync(kFull, c_lane, j & 31) : __ldg(cols + b + j); };
+      auto vec = [&](uint32_t k) -> const uint4* {
+        if constexpr (LAZY) return t4 + (uint64_t)__shfl_sync(kFull, sf_lane, (k - 1) & 31) * nv;
+        else return t4 + ((uint64_t)col(k - 1) * n_cols + col(k)) * nv;
+      };
+      uint32_t n = 0;
+      for (uint32_t v0 = 0; v0 < nv; v0 += 32 * J) {
+        uint32_t vv[J];
+#pragma unroll
+        for (int u = 0; u < J; ++u) vv[u] = min(v0 + u * 32 + lane, nv - 1);
+        uint4 f[J], xa[J];
+#pragma unroll
+        for (int u = 0; u < J; ++u) f[u] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        {
+          const uint4* p0 = vec(1);
+#pragma unroll
+          for (int u = 0; u < J; ++u) xa[u] = __ldg(p0 + vv[u]);
+        }
+        for (uint32_t k = 1; k + 1 < L; ++k) {
+          const uint4* pn = vec(k + 1);
+          uint4 xb[J];
+#pragma unroll
+          for (int u = 0; u < J; ++u) xb[u] = __ldg(pn + vv[u]);
+#pragma unroll
+          for (int u = 0; u < J; ++u) {
+            f[u].x &= xa[u].x; f[u].y &= xa[u].y; f[u].z &= xa[u].z; f[u].w &= xa[u].w;
+            xa[u] = xb[u];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < J; ++u) {
+          f[u].x &= xa[u].x; f[u].y &= xa[u].y; f[u].z &= xa[u].z; f[u].w &= xa[u].w;
+          const uint32_t v = v0 + u * 32 + lane;
+          const uint4 s = v < nv ? f[u] : make_uint4(0u, 0u, 0u, 0u);
+          n += __popc(s.x) + __popc(s.y) + __popc(s.z) + __popc(s.w);
+          if (MASK && v < nv) {
+            uint32_t* mw = mask + (uint64_t)i * mask_wpc + 4 * v;
+            const uint32_t words[4] = {index_to_natural(s.x), index_to_natural(s.y), index_to_natural(s.z),
+                                       index_to_natural(s.w)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (4 * v + q < mask_wpc) mw[q] = words[q];
+          }
+        }
+      }
+      n = __reduce_add_sync(kFull, n);
+      if (lane == 0) out[i] = n;
+      continue;
     }
     uint32_t n = 0;
     // MULTI: vectors longer than 32 J slices are swept in passes of 32 J
