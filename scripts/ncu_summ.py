@@ -6,7 +6,7 @@ else:
     out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
 h = r[0]; u = r[1]
-want = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'lts__t_bytes.sum',
+want = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'lts__t_bytes.sum', 'lts__t_sectors.sum',
         'sm__throughput.avg.pct_of_peak_sustained_elapsed', 'lts__throughput.avg.pct_of_peak_sustained_elapsed',
         'dram__throughput.avg.pct_of_peak_sustained_elapsed',
         'l1tex__throughput.avg.pct_of_peak_sustained_elapsed', 'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum',
@@ -19,6 +19,11 @@ for v in r[2:]:
     for w in want:
         if w in h:
             i = h.index(w); print('   %-60s %s %s' % (w, v[i], u[i]))
+    if 'lts__t_sectors.sum' in h and 'gpu__time_duration.sum' in h:  # L2 traffic (32-B sectors) per second
+        i, j = h.index('lts__t_sectors.sum'), h.index('gpu__time_duration.sum')
+        t = float(v[j].replace(',', '')) * {'ns': 1e-9, 'nsecond': 1e-9, 'us': 1e-6, 'usecond': 1e-6,
+                                            'ms': 1e-3, 'msecond': 1e-3}.get(u[j], 1e-9)
+        print('   %-60s %.1f GB/s' % ('L2 sector bytes / duration', float(v[i].replace(',', '')) * 32 / t / 1e9))
     st = []
     for i, name in enumerate(h):
         if 'pcsamp_warps_issue_stalled' in name and not name.endswith('not_issued'):

@@ -548,6 +548,43 @@ def test_zero_copy_host_path(evaluator, layout, path):
 
 
 
+@pytest.mark.parametrize("zc_read_max", ["0", "1000000000"])
+@pytest.mark.parametrize("R", [500, 20000, 40000])
+def test_small_batches_read_in_place(monkeypatch, zc_read_max, R):
+    """Page-locked populations small enough (EBIC_ZC_READ_MAX) are read in
+    place by the index kernel over the bus instead of being DMA'd: the same
+    counts either way, on the lane-group, TMA and lazy long-vector kernels,
+    including a bad candidate's error and the clean call after it."""
+    from paper_2105_01196_b200 import Evaluator
+
+    monkeypatch.setenv("EBIC_ZC_READ_MAX", zc_read_max)  # read at context creation
+    rng = np.random.default_rng(R)
+    m = rng.standard_normal((R, 250)).astype(np.float32)
+    m[: R // 4] = np.sort(m[: R // 4], axis=1)
+    pop = Population.from_sequences(rng.choice(250, size=int(rng.integers(1, 7)), replace=False) for _ in range(392))
+    with Evaluator(0) as ev:
+        ev.upload(m)
+        keep = []
+        t, buf = _pinned_u32(np.concatenate([pop.offsets, pop.cols]))
+        keep.append(t)
+        ppop = Population(buf[pop.offsets.size:], buf[: pop.offsets.size])
+        t2, out = _pinned_u32(np.full(len(pop), 0xDEADBEEF, np.uint32))
+        keep.append(t2)
+        for approx, neg in ((0.03, False), (0.0, True)):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            for _ in range(2):  # (the lazy index: built on the first call, read on the second)
+                got = ev.evaluate_population(ppop, TrendParams(approx=approx, negative_trends=neg), out=out)
+                np.testing.assert_array_equal(got, want)
+        bad = ppop.cols.copy()
+        bad[2] = 250
+        t3, bc = _pinned_u32(bad)
+        keep.append(t3)
+        with pytest.raises(EbicError):
+            ev.evaluate_population(Population(bc, ppop.offsets), TrendParams(), out=out)
+        want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, False)
+        np.testing.assert_array_equal(ev.evaluate_population(ppop, TrendParams(), out=out), want)
+
+
 @pytest.mark.parametrize("R", [1, 31, 32, 33, 127, 1000, 1037, 4099, 4129, 10000, 20000, 32768, 32800])
 @pytest.mark.parametrize("n_cols", [2, 37, 300])
 def test_pair_trend_index_vs_oracle(evaluator, R, n_cols):
