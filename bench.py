@@ -408,6 +408,14 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     ev.set_path({"auto": 0, "value": 1, "plane": 2, "table": 4}[args.path])
     if args.index_budget_gb is not None:
         ev.set_table_budget(int(args.index_budget_gb * (1 << 30)))
+    # process start-up (lazy CUDA module loading, the page-locked staging
+    # buffers) is paid once per process, not per matrix: a 34-MB warm-up
+    # upload (staged like the real one) and evaluation take it out of the
+    # per-matrix one-time costs below (`cold_start` reports the cold figures)
+    wm = np.random.default_rng(0).standard_normal((16800, 500)).astype(np.float32)
+    ev.upload(wm)
+    ev.evaluate_population(Population.from_sequences([[0, 1, 2], [3, 4]]), tp)
+    del wm
     t0 = time.perf_counter()
     ev.upload(np.ascontiguousarray(m[b:e]), row_base=b)
     upload_ms = (time.perf_counter() - t0) * 1e3
@@ -647,7 +655,9 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         "one_time_ms": {"total": one_time_ms, "upload": upload_ms, "prepare": prepare_ms,
                         "index_alloc": build["alloc_ms"], "plane": build["plane_ms"], "index": build["index_ms"],
                         "lazy_build": lazy_build_ms,
-                        "note": "upload = H2D + finiteness/exactness check + transpose (host clock); prepare = "
+                        "note": "per-(matrix, approx) costs after a warm-up upload of another matrix (process "
+                                "start-up -- lazy module loading, page-locked staging -- is in cold_start); "
+                                "upload = H2D + finiteness/exactness check + transpose (host clock); prepare = "
                                 "index allocation (host clock) + rank plane + pair-trend index (CUDA events); "
                                 "lazy_build = first visits of the cycled populations with the lazy index minus "
                                 "as many steady-state kernel times (CUDA events); max over ranks"},
