@@ -321,7 +321,23 @@ def index_kernel_name(wp, n_cand, n_sms=148, lazy=False):
         return "table_count_tma_kernel"
     if lazy:
         return "table_count_warp_multi_kernel"
-    return "table_count_warp_multi_kernel" if n_cand >= n_sms * 32 else "table_count_kernel"
+    return "table_count_warp_multi_kernel" if n_cand >= n_sms * 6 else "table_count_kernel"
+
+
+def distinct_pairs(pop, n_cols: int, neg: bool) -> int:
+    """Distinct pair vectors a batch reads (consecutive (a, b) pairs; (b, a)
+    too with negatives): the DRAM bytes it must move at least once when the
+    index does not stay in L2 (repeats within a launch may hit L2)."""
+    cols = pop.cols.astype(np.int64)
+    if cols.size < 2:
+        return 0
+    starts = np.zeros(cols.size, dtype=bool)
+    starts[pop.offsets[:-1][pop.offsets[:-1] < cols.size].astype(np.int64)] = True
+    k = np.nonzero(~starts[1:])[0] + 1  # positions k with a pair (k-1 -> k) in the same candidate
+    keys = cols[k - 1] * n_cols + cols[k]
+    if neg:
+        keys = np.concatenate([keys, cols[k] * n_cols + cols[k - 1]])
+    return int(np.unique(keys).size)
 
 
 def table_wp(rows: int) -> int:
@@ -568,8 +584,9 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
 
     # roofline of the count kernel on this rank
     n_pairs = [int(dp[3]) - int(dp[2]) for dp in d_pops]
-    if index_used:  # the pair vectors the kernel must stream
-        phys = [4.0 * wp * npair * neg_factor for npair in n_pairs]
+    reads = [4.0 * wp * npair * neg_factor for npair in n_pairs]  # every pair read (L2 hits included)
+    if index_used:  # the distinct pair vectors the kernel must stream from HBM
+        phys = [4.0 * wp * distinct_pairs(pp, Ccols, cfg["negative"]) for pp in pops_local]
     else:  # the slab kernels stage the rank plane (the value kernel: the store) once per launch
         phys = [4.0 * (e - b) * Ccols for _ in n_pairs]
     alg = [4.0 * (e - b) * int(dp[3]) for dp in d_pops]
@@ -699,10 +716,13 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
                      "traffic": ncu_traffic(args.config, world),
                      "kernel": kernel, "kernel_avg_ms": statistics.mean(kern_ms),
                      "bytes_per_launch": statistics.mean(phys),
-                     "bytes": ("physical: pair-vector bytes the kernel must stream from HBM, 4 B x %d words x "
-                               "(L-1) pairs per candidate%s; achieved = sum(bytes) / sum(kernel time) over the "
-                               "kernel pass (CUDA events around each launch on its stream)"
-                               % (wp, " x 2 (negatives)" if neg_factor == 2 else ""))
+                     "reads_gbs": (sum(reads[i % n_pops] for i in range(args.steps)) / ksum_s / 1e9
+                                   if index_used else None),
+                     "bytes": ("physical: the distinct pair vectors a launch must stream from HBM, 4 B x %d "
+                               "words each (consecutive pairs%s, repeats within a launch counted once: they may "
+                               "hit L2; reads_gbs counts every read); achieved = sum(bytes) / sum(kernel time) "
+                               "over the kernel pass (CUDA events around each launch on its stream)"
+                               % (wp, " in both directions (negatives)" if neg_factor == 2 else ""))
                      if index_used else
                      "physical: the rank plane (4 B x R x C) the slab kernel stages into shared memory once per "
                      "launch; the kernel is bound by its shared-memory pipe, not HBM (DESIGN 4.3), so this "
@@ -897,18 +917,24 @@ def bench_sweep(args):
                 ev.sync()
                 ev.set_stream(None)
                 ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-                phys = 4.0 * wp * P * (L - 1)
+                reads = 4.0 * wp * P * (L - 1)
                 alg = 4.0 * L * R * P
                 # L2 roofline while the whole index is at most 2x the L2 (the
                 # main bench's stream/flush rule): a 132-MB index (256k rows)
-                # is mostly served from L2 and measures above the HBM peak
+                # is mostly served from L2 and measures above the HBM peak.
+                # Against L2 every read counts; against HBM the distinct
+                # vectors a launch must bring in (64 columns: 4096 pairs in all,
+                # so big populations repeat them and the repeats hit L2)
                 regime = "l2" if (l2 is not None and index_bytes <= 2 * L2_BYTES) else "hbm"
+                phys = reads if regime == "l2" else 4.0 * wp * statistics.mean(
+                    distinct_pairs(pp, SWEEP_COLS, False) for pp in pops)
                 peak = l2 if regime == "l2" else hbm
                 line = {"sweep": "c5", "sizing": args.sweep_sizing, "rows": R, "cols": SWEEP_COLS, "L": L,
                         "approx": approx, "population": P,
                         "kernel": index_kernel_name(wp, P), "kernel_ms": ms, "evals_per_s": P / (ms / 1e3),
                         "row_checks_per_s": P * R / (ms / 1e3), "index_bytes": index_bytes, "wp": int(wp),
                         "physical_bytes": phys, "physical_gbs": phys / (ms / 1e3) / 1e9, "regime": regime,
+                        "reads_gbs": reads / (ms / 1e3) / 1e9,
                         "peak_gbs": peak, "peak_source": l2_src if regime == "l2" else hbm_src,
                         "frac": phys / (ms / 1e3) / 1e9 / peak,
                         "effective_algorithmic_gbs": alg / (ms / 1e3) / 1e9}

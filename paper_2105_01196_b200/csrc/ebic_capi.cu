@@ -762,7 +762,10 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
                  int neg, uint32_t* out, int* err_out, uint32_t* d_mask, cudaStream_t s, const IndexPlan& plan) {
   const uint32_t nv = (uint32_t)(table_wp(ctx) / 4);
   const bool lazy = plan.mode == kIndexLazy;
-  const bool many = n_cand >= (uint64_t)ctx->n_sms * 32;  // enough warps to fill every SM
+  // enough warps per SM for the (pipelined) multi-pass kernel (measured
+  // better than a CTA per candidate down to ~1000 candidates: C5's 1024 of
+  // 1M rows 0.29 -> 0.21 ms); below that a CTA per candidate streams better
+  const bool many = n_cand >= (uint64_t)ctx->n_sms * 6;
   if (!lazy && nv <= 32 && (ctx->table_kernel == 0 || ctx->table_kernel == 4) && !MASK) {
     // tiny vectors (R <= 4096 rows): a group of next_pow2(nv) lanes per
     // candidate, register loads (table_count_group_kernel)
@@ -845,8 +848,9 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
   if (!lazy && nv > 256 && (ctx->table_kernel == 1 || (ctx->table_kernel == 0 && many))) {
     // long vectors, many candidates: a warp per candidate sweeping its vectors
     // in passes of 256 slices (no block barriers; measured 0.44 vs 0.67 ms for
-    // the CTA kernel at 200k x 2000, P = 32768).  Few candidates (C5: 1024)
-    // keep the CTA kernel, which puts a whole CTA on each.
+    // the CTA kernel at 200k x 2000, P = 32768, before the pipelining that
+    // took it to 0.41).  Very few candidates keep the CTA kernel, which puts
+    // a whole CTA on each.
     auto go = [&](auto kern) {
       // a warp per candidate for the whole population (the block scheduler
       // balances the tail better than a grid-stride loop over fewer warps)
