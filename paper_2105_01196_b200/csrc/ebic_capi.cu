@@ -1442,7 +1442,13 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
   if (store < EBIC_STORE_AUTO || store > EBIC_STORE_F64)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "bad store mode %d", store);
   EBIC_TRY(set_device(ctx));
+  const bool trace = std::getenv("EBIC_UPLOAD_TRACE") != nullptr;
+  const double tu0 = host_ms();
+  auto mark = [&](const char* what) {
+    if (trace) std::fprintf(stderr, "upload: %-22s at %.1f ms\n", what, host_ms() - tu0);
+  };
   drop_matrix(ctx, /*keep_index_alloc=*/true);
+  mark("previous matrix freed");
   cudaStream_t s = ctx->stream;
   const uint64_t n = n_rows * n_cols;
 
@@ -1499,6 +1505,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
     release_in();
     return fail(EBIC_ERR_INVALID_ARGUMENT, "ExpressionMatrix: non-finite value");
   }
+  mark("checked");
   const bool exact = !(flags & 2);
   int chosen = store;
   if (chosen == EBIC_STORE_AUTO) chosen = exact ? EBIC_STORE_F32 : EBIC_STORE_F64;
@@ -1528,6 +1535,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
     cudaFree(d_mat);
     return fail(EBIC_ERR_CUDA, "matrix transpose: %s", cudaGetErrorString(ce));
   }
+  mark("transposed");
   ctx->d_mat = d_mat;
   ctx->store = chosen;
   ctx->n_rows = n_rows;
@@ -1558,6 +1566,7 @@ int upload_impl(ebic_ctx* ctx, const TI* host, uint64_t n_rows, uint64_t n_cols,
       ctx->d_lmap = nullptr;  // retried (and reported) on first use
     }
   }
+  mark("done");
   if (store_out) *store_out = chosen;
   return EBIC_OK;
 }
