@@ -443,11 +443,26 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     ev.set_stream(stream.cuda_stream)
+    exchange_note = None
     if p2p:
+        # peer-memory exchange windows; if any rank cannot map its peers (no
+        # P2P between the GPUs), every rank falls back to the NCCL all_reduce
+        # and the line says so
         h = ev.xchg_create(world, rank, P)
         handles = [None] * world
         dist.all_gather_object(handles, h)
-        ev.xchg_open(handles)
+        err = ""
+        try:
+            ev.xchg_open(handles)
+        except Exception as ex:  # noqa: BLE001 -- reported in the line
+            err = str(ex)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if any(errs):
+            p2p = False
+            exchange_note = "p2p unavailable (%s): NCCL all_reduce" % next(e for e in errs if e)
+            log("exchange:", exchange_note)
+            ev.xchg_destroy()
 
     d_pops = [(torch.from_numpy(pp.cols.view(np.int32)).to(dev), torch.from_numpy(pp.offsets.view(np.int32)).to(dev),
                len(pp), int(pp.cols.size)) for pp in pops_local]
@@ -702,7 +717,8 @@ def bench_ours(args, cfg, rank, world, local_rank, dist):
         "row_checks_per_s": value * R,
         "config": {"workload": cfg["label"], "rows": R, "cols": Ccols, "population": P,
                    "population_per_step_total": p_total, "parallelism": parallelism, "shard": shard,
-                   "path": args.path, "exchange": ("p2p" if p2p else "nccl") if shard == "rows" and world > 1 else None,
+                   "path": args.path,
+                   "exchange": (exchange_note or ("p2p" if p2p else "nccl")) if shard == "rows" and world > 1 else None,
                    "l2": ("stream: no flush; the per-rank pair-trend index (%.0f MB) exceeds 2x the 126 MB L2 and "
                           "populations are cycled from a pool of %d whose pair vectors cover >= %.0f MB, "
                           "steps issued back to back" % (per_rank_index / 1e6, n_pops, want / 1e6))
