@@ -25,7 +25,7 @@ out = torch.zeros(cfg["pop"], dtype=torch.int32, device="cuda")
 s = torch.cuda.Stream()
 sp = s.cuda_stream if use_torch_stream else None
 for phase in ("warm", "timed", "timed2"):
-    n = 8 if phase == "warm" else 20
+    n = 8 if phase == "warm" else int(sys.argv[2]) if len(sys.argv) > 2 else 20
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
     host = []
     torch.cuda.synchronize()
