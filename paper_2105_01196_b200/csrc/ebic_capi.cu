@@ -770,28 +770,31 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     // tiny vectors (R <= 4096 rows): a group of next_pow2(nv) lanes per
     // candidate, register loads (table_count_group_kernel)
     // lanes per candidate GL <= 8 (at least 4 candidates per warp), J = nv / GL
-    // slices per lane: nv 1, 2, 4 -> GL = nv; 8 -> 8 x 1; 16 -> 8 x 2; 32 -> 8 x 4
+    // slices per lane: nv 1, 2, 4 -> GL = nv; up to 8 -> 8 x 1; beyond: 8 x
+    // ceil(nv / 8) (20 slices: 8 x 3, not 8 x 4)
     const int GL = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : 8;
-    const int J = nv <= 8 ? 1 : nv <= 16 ? 2 : 4;
+    const int J = (int)((nv + 7) / 8);
     const uint64_t per_cta = 8ull * (32 / GL);
     const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + per_cta - 1) / per_cta, (uint64_t)ctx->n_sms * 8);
-    auto go = [&](auto kern) {
-      kern<<<grid, 256, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
-                                d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err);
+    auto go = [&](auto kern) -> cudaError_t {
+      // programmatic dependent launch, as the TMA kernel: back-to-back batches
+      // overlap one kernel's tail with the next one's start
+      return launch_pdl(kern, dim3(grid), dim3(256), 0, s, ctx->pdl, (const uint32_t*)ctx->d_table,
+                        (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows, d_cols, d_offs,
+                        (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err);
     };
-    auto pick = [&](auto negc) {
+    auto pick = [&](auto negc) -> cudaError_t {
       constexpr bool N = decltype(negc)::value;
-      if (GL == 1) go(ebic::table_count_group_kernel<1, 1, 4, N>);
-      else if (GL == 2) go(ebic::table_count_group_kernel<2, 1, 4, N>);
-      else if (GL == 4) go(ebic::table_count_group_kernel<4, 1, 4, N>);
-      else if (J == 1) go(ebic::table_count_group_kernel<8, 1, 4, N>);
-      else if (J == 2) go(ebic::table_count_group_kernel<8, 2, 4, N>);
-      else go(ebic::table_count_group_kernel<8, 4, 2, N>);
+      if (GL == 1) return go(ebic::table_count_group_kernel<1, 1, 4, N>);
+      if (GL == 2) return go(ebic::table_count_group_kernel<2, 1, 4, N>);
+      if (GL == 4) return go(ebic::table_count_group_kernel<4, 1, 4, N>);
+      if (J == 1) return go(ebic::table_count_group_kernel<8, 1, 4, N>);
+      if (J == 2) return go(ebic::table_count_group_kernel<8, 2, 4, N>);
+      if (J == 3) return go(ebic::table_count_group_kernel<8, 3, 2, N>);
+      return go(ebic::table_count_group_kernel<8, 4, 2, N>);
     };
-    if (neg) pick(std::true_type{});
-    else pick(std::false_type{});
+    EBIC_CUDA(neg ? pick(std::true_type{}) : pick(std::false_type{}));
     ctx->launches++;
-    EBIC_CUDA(cudaGetLastError());
     return EBIC_OK;
   }
   if (lazy && nv > 256) {

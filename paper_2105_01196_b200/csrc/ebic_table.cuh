@@ -612,6 +612,18 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
   }
 }
 
+// Programmatic dependent launch (PDL).  The count kernels let the next kernel
+// of their stream launch as soon as they start (their CTAs are persistent, so
+// the next grid's CTAs only fill SM slots as this grid's CTAs retire: the
+// tail of batch k overlaps the start of batch k+1), and wait for the previous
+// grid before their first global store (a back-to-back batch may write the
+// same output buffer).  The count kernels read nothing an earlier count
+// kernel writes; kernels whose output they do read (the index builders, the
+// lazy pair builder) never trigger early, so the count kernel starts after
+// them as usual.  Both instructions are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Tiny vectors (nv <= 32 uint4 slices: R <= 4096 rows): a GROUP of GL lanes
 // per candidate (32 / GL candidates per warp), lane s of the group owning
 // slices s, s + GL, ... (J of them) of every pair vector.  A 128-B vector
@@ -642,6 +654,8 @@ table_count_group_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, ui
   };
   uint32_t b, e;
   load_offs(i0 + lane / GL, b, e);
+  pdl_trigger();
+  bool dep_done = false;  // griddepcontrol.wait issued (before this warp's first store)
   for (; i0 < n_cand; i0 += stride) {
     const uint64_t i = i0 + lane / GL;
     const bool live = i < n_cand;
@@ -703,6 +717,10 @@ table_count_group_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, ui
     }
 #pragma unroll
     for (int w = GL / 2; w >= 1; w >>= 1) n += __shfl_xor_sync(kFull, n, w);
+    if (!dep_done) {
+      pdl_wait();
+      dep_done = true;
+    }
     if (live && s == 0) {
       if (bad_offs || badc) {  // (every lane of a group loads the same columns: same flags)
         out[i] = 0;
@@ -749,17 +767,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                : "memory");
 }
 
-// Programmatic dependent launch (PDL).  The count kernels let the next kernel
-// of their stream launch as soon as they start (their CTAs are persistent, so
-// the next grid's CTAs only fill SM slots as this grid's CTAs retire: the
-// tail of batch k overlaps the start of batch k+1), and wait for the previous
-// grid before their first global store (a back-to-back batch may write the
-// same output buffer).  The count kernels read nothing an earlier count
-// kernel writes; kernels whose output they do read (the index builders, the
-// lazy pair builder) never trigger early, so the count kernel starts after
-// them as usual.  Both instructions are no-ops without the launch attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // LAZY: the vectors come from the lazy index (ebic_lazy.cuh) -- the pair's
 // slot is looked up in la.map (for a candidate's first 31 pairs, one lookup
