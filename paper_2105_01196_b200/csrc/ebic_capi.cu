@@ -824,16 +824,18 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
           (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(ebic::lazy_build_kernel<float>), 256, smem));
       ebic::lazy_build_kernel<float><<<fgrid, 256, smem, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
     }
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern) -> cudaError_t {
       // a warp per candidate for the whole population (the block scheduler
-      // balances the tail better than a grid-stride loop over fewer warps)
+      // balances the tail better than a grid-stride loop over fewer warps);
+      // a plain launch: it reads the pool the build kernel just wrote, so it
+      // must not overlap it (no PDL attribute: the kernel's pdl_* are no-ops)
       const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
-      kern<<<grid, 256, 0, s>>>(nullptr, (uint32_t)ctx->n_cols, wp, (uint32_t)ctx->n_rows, d_cols, d_offs,
-                                (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,
-                                ctx->ld / 32, la);
+      return launch_pdl(kern, dim3(grid), dim3(256), 0, s, false, (const uint32_t*)nullptr, (uint32_t)ctx->n_cols,
+                        wp, (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out,
+                        err_out ? err_out : ctx->d_err, d_mask, (uint64_t)(ctx->ld / 32), la);
     };
-    if (neg) go(ebic::table_count_warp_multi_kernel<8, true, MASK, true, true>);
-    else go(ebic::table_count_warp_multi_kernel<8, false, MASK, true, true>);
+    EBIC_CUDA(neg ? go(ebic::table_count_warp_multi_kernel<8, true, MASK, true, true>)
+                  : go(ebic::table_count_warp_multi_kernel<8, false, MASK, true, true>));
     // candidates with a pair not in the pool (rare): computed from the store
     const unsigned dgrid = (unsigned)ctx->n_sms * 2;
     auto god = [&](auto kern) {
@@ -854,18 +856,19 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     // the CTA kernel at 200k x 2000, P = 32768, before the pipelining that
     // took it to 0.41).  Very few candidates keep the CTA kernel, which puts
     // a whole CTA on each.
-    auto go = [&](auto kern) {
+    auto go = [&](auto kern) -> cudaError_t {
       // a warp per candidate for the whole population (the block scheduler
-      // balances the tail better than a grid-stride loop over fewer warps)
+      // balances the tail better than a grid-stride loop over fewer warps);
+      // programmatic dependent launch like the short-vector kernels
       const unsigned grid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, 1u << 30);
-      kern<<<grid, 256, 0, s>>>(ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows,
-                                d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err,
-                                d_mask, ctx->ld / 32, ebic::LazyArgs{});
+      return launch_pdl(kern, dim3(grid), dim3(256), 0, s, ctx->pdl, (const uint32_t*)ctx->d_table,
+                        (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx), (uint32_t)ctx->n_rows, d_cols, d_offs,
+                        (uint32_t)n_cand, (uint32_t)n_idx, out, err_out ? err_out : ctx->d_err, d_mask,
+                        (uint64_t)(ctx->ld / 32), ebic::LazyArgs{});
     };
-    if (neg) go(ebic::table_count_warp_multi_kernel<8, true, MASK>);
-    else go(ebic::table_count_warp_multi_kernel<8, false, MASK>);
+    EBIC_CUDA(neg ? go(ebic::table_count_warp_multi_kernel<8, true, MASK>)
+                  : go(ebic::table_count_warp_multi_kernel<8, false, MASK>));
     ctx->launches++;
-    EBIC_CUDA(cudaGetLastError());
     return EBIC_OK;
   }
   if (lazy || tma_table_kernel(ctx)) {

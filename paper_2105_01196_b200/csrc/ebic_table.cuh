@@ -405,6 +405,18 @@ table_count_warp_kernel(const uint32_t* __restrict__ table, uint32_t n_cols, uin
   }
 }
 
+// Programmatic dependent launch (PDL).  The count kernels let the next kernel
+// of their stream launch as soon as they start (their CTAs are persistent, so
+// the next grid's CTAs only fill SM slots as this grid's CTAs retire: the
+// tail of batch k overlaps the start of batch k+1), and wait for the previous
+// grid before their first global store (a back-to-back batch may write the
+// same output buffer).  The count kernels read nothing an earlier count
+// kernel writes; kernels whose output they do read (the index builders, the
+// lazy pair builder) never trigger early, so the count kernel starts after
+// them as usual.  Both instructions are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Long vectors (> 256 slices) with many candidates: the same warp-per-
 // candidate scheme sweeping the vectors in passes of 32 J slices (every slice
 // index clamped, loads still unconditional).  A separate kernel so that the
@@ -430,6 +442,16 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
   const uint32_t warps = gridDim.x * (blockDim.x >> 5);
   const uint32_t nv = wp / 4;  // uint4 per pair vector (== 32 J unless MULTI or J == 1)
   const uint4* t4 = reinterpret_cast<const uint4*>(LAZY ? la.pool : table);
+  // programmatic dependent launch (pdl_trigger): wait for the previous grid
+  // only before this warp's first global store
+  pdl_trigger();
+  bool dep_done = false;
+  auto before_store = [&]() {
+    if (!dep_done) {
+      pdl_wait();
+      dep_done = true;
+    }
+  };
   for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_cand; i += warps) {
     const uint32_t b = __ldg(offs + i), e = __ldg(offs + i + 1);
     const bool bad_offs = e <= b || e > n_idx;
@@ -437,6 +459,7 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
     bool badc = false;
     for (uint32_t k = b + lane; k < b + L; k += 32) badc |= __ldg(cols + k) >= n_cols;
     if (__any_sync(kFull, bad_offs || badc)) {
+      before_store();
       if (lane == 0) {
         out[i] = 0;
         *err_out = bad_offs ? 2 : 1;
@@ -444,6 +467,7 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
       continue;
     }
     if (L == 1) {  // no pair: every row supports (the trend.cpp:19 loop never runs)
+      before_store();
       if (lane == 0) out[i] = n_rows;
       if (MASK)
         for (uint32_t w = lane; w < mask_wpc; w += 32)
@@ -471,6 +495,7 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
       }
       if (!NEG) ready = ready && L <= 32;  // (the pipelined loop takes every slot from a lane register)
       if (!__all_sync(kFull, ready)) {
+        before_store();
         if (lane == 0) la.defer[1 + atomicAdd(la.defer, 1u)] = i;
         continue;
       }
@@ -511,6 +536,7 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
             xa[u] = xb[u];
           }
         }
+        before_store();
 #pragma unroll
         for (int u = 0; u < J; ++u) {
           f[u].x &= xa[u].x; f[u].y &= xa[u].y; f[u].z &= xa[u].z; f[u].w &= xa[u].w;
@@ -591,6 +617,7 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
         }
         cp = cc;
       }
+      before_store();
 #pragma unroll
       for (int u = 0; u < J; ++u) {
         const uint32_t v = v0 + u * 32 + lane;
@@ -612,17 +639,6 @@ table_count_warp_multi_kernel(const uint32_t* __restrict__ table, uint32_t n_col
   }
 }
 
-// Programmatic dependent launch (PDL).  The count kernels let the next kernel
-// of their stream launch as soon as they start (their CTAs are persistent, so
-// the next grid's CTAs only fill SM slots as this grid's CTAs retire: the
-// tail of batch k overlaps the start of batch k+1), and wait for the previous
-// grid before their first global store (a back-to-back batch may write the
-// same output buffer).  The count kernels read nothing an earlier count
-// kernel writes; kernels whose output they do read (the index builders, the
-// lazy pair builder) never trigger early, so the count kernel starts after
-// them as usual.  Both instructions are no-ops without the launch attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Tiny vectors (nv <= 32 uint4 slices: R <= 4096 rows): a GROUP of GL lanes
 // per candidate (32 / GL candidates per warp), lane s of the group owning
