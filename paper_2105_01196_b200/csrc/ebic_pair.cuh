@@ -187,7 +187,27 @@ __device__ __forceinline__ void pair_sweep_class(const SlabArgs& a, uint32_t sa_
     } else {
       uint32_t cc[kRecCols];
       rec_cols(rec, cc);
-      if constexpr (L < 8) {
+      if constexpr (L < 8 && P == 1 && SUB == 2 && !NEG) {
+        // The first column contributes only NT words (odd banks of its line)
+        // and the last only Rg words (even banks).  Half-warp 0 fetches its
+        // first column while half-warp 1 fetches its last, then the other way
+        // round: each LDS.32 puts 16 odd-bank and 16 even-bank words in one
+        // wavefront (two ordinary 4-byte loads of the same kind would collide
+        // pairwise across the half-warps and take two).  The middle columns
+        // are LDS.64s of one aligned 128-byte line per half-warp, as before.
+        const uint32_t a_first = lane_base + (cc[0] << COLSHIFT) + 4, a_last = lane_base + (cc[L - 1] << COLSHIFT);
+        const uint32_t x0 = lds<uint32_t>(sub ? a_last : a_first);
+        const uint32_t x1 = lds<uint32_t>(sub ? a_first : a_last);
+        V w[L];
+#pragma unroll
+        for (int q = 1; q < L - 1; ++q) w[q] = lds<V>(lane_base + (cc[q] << COLSHIFT));
+        w[0].y = sub ? x1 : x0;      // NT of the first column
+        w[L - 1].x = sub ? x0 : x1;  // Rg of the last column
+        M f = vmask;
+#pragma unroll
+        for (int q = 1; q < L; ++q) and_pair<P>(f, w[q], w[q - 1]);
+        ok = f;
+      } else if constexpr (L < 8) {
         V w[L];
 #pragma unroll
         for (int q = 0; q < L; ++q) w[q] = lds<V>(lane_base + (cc[q] << COLSHIFT));
