@@ -253,6 +253,19 @@ int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_p
  * max(8 GiB, 10%); use it to opt in to very large indexes (a 200k x 2000
  * matrix needs 100 GB).  AUTO uses the index only if it fits the budget. */
 int ebic_ctx_set_table_budget(ebic_ctx* ctx, uint64_t bytes);
+
+/* How the lazy index builds a batch's missing pair vectors (short vectors,
+ * float32 store; env EBIC_LAZY_BUILD).  0 auto: a cold batch -- nothing
+ * observed in the pool yet, or >= 1024 slots claimed between the two latest
+ * fill samples, and >= 256 candidates -- runs claim, a slab build pass
+ * (lazy_slab_build_kernel: 32-row slices of every column staged once per CTA)
+ * and publish ahead of the count kernel; any other batch builds inside the
+ * count kernel.  1: always inside the count kernel.  2: always the build pass
+ * first (when the slices fit in shared memory).  Bit-exact either way. */
+#define EBIC_LAZY_BUILD_AUTO 0
+#define EBIC_LAZY_BUILD_INLINE 1
+#define EBIC_LAZY_BUILD_FIRST 2
+int ebic_ctx_set_lazy_build(ebic_ctx* ctx, int mode);
 /* Bytes the pair-trend index of the resident matrix needs (0 if the matrix is
  * too wide for the rank plane) and whether it is built. */
 int ebic_matrix_index_info(ebic_ctx* ctx, uint64_t* bytes_needed, int* in_use);

@@ -57,6 +57,7 @@ SIGNATURES = {
     "ebic_matrix_index_stats": (C.c_int, [_vp, C.POINTER(C.c_int)] + [C.POINTER(C.c_uint64)] * 6),
     "ebic_ctx_set_pair_layout": (C.c_int, [_vp, C.c_int, C.c_int]),
     "ebic_ctx_set_table_budget": (C.c_int, [_vp, C.c_uint64]),
+    "ebic_ctx_set_lazy_build": (C.c_int, [_vp, C.c_int]),
     "ebic_matrix_index_info": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
     "ebic_tsv_read": (C.c_int, [C.c_char_p, C.c_int, _vp, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "ebic_matrix_load_tsv": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int),

@@ -251,6 +251,12 @@ struct ebic_ctx {
   uint64_t lazy_built = 0;          // slots filled over all epochs of this (matrix, approx) (ski-rental rent)
   uint64_t lazy_epoch_seen = 0;     // slots of the current epoch already added to lazy_built
   uint64_t lazy_resets = 0;
+  // fill samples (h_lmirror) -> is the pool still filling fast (ebic::LazyArgs::cold)?
+  uint32_t lazy_sample_count = 0, lazy_sample_seq = 0;
+  uint64_t lazy_recent_growth = 0;
+  int lazy_build = EBIC_LAZY_BUILD_AUTO;  // EBIC_LAZY_BUILD / ebic_ctx_set_lazy_build
+  bool lazy_shared_dirty = false;
+  bool lazy_trace = false;  // EBIC_LAZY_TRACE: one line per lazy batch on stderr  // lazy state initialised on one stream, not yet synchronised
   int index_mode = 0;               // index used by the last counting launch (IndexMode)
   double plane_approx = 0.0;
   int path = EBIC_PATH_AUTO;
@@ -545,6 +551,9 @@ constexpr uint64_t kLazyMaxCols = 8192;              // map of C^2 slots <= 256 
 constexpr uint64_t kSmallFullIndex = 1ull << 30;     // a full index this small is built outright (ms)
 constexpr double kLazyRentFrac = 0.5;                // ski rental: buy the full index once this share of
                                                      // the C^2 pairs has been built lazily
+constexpr uint64_t kLazyColdGrowth = 1024;           // slots claimed between two fill samples that keep
+                                                     // batches on the build-first (cold) route
+constexpr uint64_t kLazyColdMinCand = 256;           // smaller batches always build inside the count kernel
 
 // The lazy index runs in the TMA kernel (vectors of <= 256 uint4 slices, i.e.
 // <= 32K rows per shard).
@@ -571,8 +580,11 @@ void lazy_release(ebic_ctx* ctx, cudaStream_t s) {
 int lazy_new_epoch(ebic_ctx* ctx, cudaStream_t s) {
   EBIC_CUDA(cudaMemsetAsync(ctx->d_lmap, 0xFF, lazy_map_bytes(ctx), s));
   EBIC_CUDA(cudaMemsetAsync(ctx->d_lcount, 0, sizeof(uint32_t), s));
+  ctx->lazy_shared_dirty = true;
   ctx->lazy_epoch_seq = ctx->lazy_seq + 1;
   ctx->lazy_epoch_seen = 0;
+  ctx->lazy_sample_count = ctx->lazy_sample_seq = 0;
+  ctx->lazy_recent_growth = 0;
   return EBIC_OK;
 }
 
@@ -596,6 +608,7 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
     ctx->h_lmirror_dev = static_cast<uint32_t*>(dev_alias(ctx->h_lmirror.p));
   }
   if (!ctx->lazy_valid || std::memcmp(&ctx->lazy_approx, &approx, sizeof(double)) != 0) {
+    if (ctx->lazy_valid) EBIC_CUDA(cudaDeviceSynchronize());  // (another approx's batches may be in flight)
     EBIC_TRY(lazy_new_epoch(ctx, s));
     ctx->lazy_valid = true;
     ctx->lazy_approx = approx;
@@ -605,13 +618,26 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
   const uint32_t m_count = *(volatile uint32_t*)&ctx->h_lmirror.p[0];
   const uint32_t m_seq = *(volatile uint32_t*)&ctx->h_lmirror.p[1];
   uint64_t used = 0;
-  if (m_seq >= ctx->lazy_epoch_seq && m_seq <= ctx->lazy_seq) {
+  const bool observed = m_seq >= ctx->lazy_epoch_seq && m_seq <= ctx->lazy_seq;
+  if (observed) {
     used = std::min<uint64_t>(m_count, ctx->lcap);
     if (used > ctx->lazy_epoch_seen) {
       ctx->lazy_built += used - ctx->lazy_epoch_seen;
       ctx->lazy_epoch_seen = used;
     }
+    // growth between the two latest distinct samples (a sample is taken at
+    // the start of a lazy kernel and after a cold batch's claims)
+    if (m_seq != ctx->lazy_sample_seq || m_count != ctx->lazy_sample_count) {
+      ctx->lazy_recent_growth = m_count > ctx->lazy_sample_count ? m_count - ctx->lazy_sample_count : 0;
+      ctx->lazy_sample_count = m_count;
+      ctx->lazy_sample_seq = m_seq;
+    }
   }
+  // cold: nothing observed yet in this epoch, or the pool grew by many slots
+  // recently -- the batch probably brings many new pairs (first calls, a new
+  // population), which a separate build pass makes ~5x cheaper
+  la->cold = ctx->lazy_build == EBIC_LAZY_BUILD_FIRST ||
+             (ctx->lazy_build == EBIC_LAZY_BUILD_AUTO && (!observed || ctx->lazy_recent_growth >= kLazyColdGrowth));
   // Room for this batch at its worst case.  Batches issued since the
   // mirror's sample are not counted at theirs: a GA's populations (and a
   // cycled benchmark pool) reuse most pairs, so a sum of worst cases grows
@@ -637,7 +663,11 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
         cudaGetLastError();  // cannot grow: stay at this capacity (warps build private copies)
       } else {
         if (ctx->d_lpool) {
+          // batches on other streams may still be writing the old pool (their
+          // builds): let them finish before it is copied (growth is rare)
+          EBIC_CUDA(cudaDeviceSynchronize());
           EBIC_CUDA(cudaMemcpyAsync(np, ctx->d_lpool, ctx->lcap * vec_bytes, cudaMemcpyDeviceToDevice, s));
+          ctx->lazy_shared_dirty = true;
           EBIC_CUDA(cudaFree(ctx->d_lpool));
         }
         ctx->d_lpool = np;
@@ -647,11 +677,15 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
       // the pool cannot grow and this batch may not fit: start over (a pool
       // of all C^2 pairs never fills)
       ++ctx->lazy_resets;
+      // (slots are handed out again from 0: batches on other streams must not
+      // be building the old epoch's slots any more)
+      EBIC_CUDA(cudaDeviceSynchronize());
       EBIC_TRY(lazy_new_epoch(ctx, s));
     }
   }
-  if (table_wp(ctx) / 4 > 256 && ctx->lkcap < ctx->lcap) {
-    // long vectors: per-slot claim bookkeeping (only read within one batch: no copy)
+  if (ctx->lkcap < ctx->lcap) {
+    // per-slot claim bookkeeping of the claim / build kernels (long vectors,
+    // cold batches of short ones; only read within one batch: no copy)
     uint32_t *nk = nullptr, *nl = nullptr;
     if (cudaMalloc(reinterpret_cast<void**>(&nk), ctx->lcap * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(reinterpret_cast<void**>(&nl), ctx->lcap * sizeof(uint32_t)) != cudaSuccess) {
@@ -661,14 +695,28 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
                   (unsigned long long)ctx->lcap);
     }
     EBIC_CUDA(cudaMemsetAsync(nk, 0xFF, ctx->lcap * sizeof(uint32_t), s));  // kSlotEmpty: nothing claimed
+    ctx->lazy_shared_dirty = true;
     if (ctx->d_lkeys) cudaFree(ctx->d_lkeys);
     if (ctx->d_lleft) cudaFree(ctx->d_lleft);
     ctx->d_lkeys = nk;
     ctx->d_lleft = nl;
     ctx->lkcap = ctx->lcap;
   }
-  if (!ctx->d_lstart) EBIC_CUDA(cudaMalloc(&ctx->d_lstart, ebic::kLazyStartRing * sizeof(uint32_t)));
+  if (!ctx->d_lstart) EBIC_CUDA(cudaMalloc(&ctx->d_lstart, 2 * ebic::kLazyStartRing * sizeof(uint32_t)));
+  if (ctx->lazy_shared_dirty) {
+    // the map / count / keys were (re)initialised or the pool copied on this
+    // stream: batches the caller issues next on OTHER streams must not see
+    // them half done (fresh cudaMalloc memory can hold a previous map's slot
+    // numbers).  First use, growth and resets only.
+    EBIC_CUDA(cudaStreamSynchronize(s));
+    ctx->lazy_shared_dirty = false;
+  }
   const uint32_t seq = ++ctx->lazy_seq;
+  if (ctx->lazy_trace)
+    std::fprintf(stderr, "lazy: seq %u stream %p cold %d used %llu (sample %u/%u growth %llu) cap %llu worst %llu\n", seq,
+                 (void*)s, la->cold, (unsigned long long)used, m_count, m_seq,
+                 (unsigned long long)ctx->lazy_recent_growth, (unsigned long long)ctx->lcap,
+                 (unsigned long long)worst);
   la->map = ctx->d_lmap;
   la->pool = ctx->d_lpool;
   la->count = ctx->d_lcount;
@@ -814,6 +862,8 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     const unsigned cgrid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, (uint64_t)ctx->n_sms * 16);
     ebic::lazy_claim_kernel<<<cgrid, 256, 0, s>>>(la, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx,
                                                   (uint32_t)ctx->n_cols, (wp + 31) / 32, neg);
+    EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + ebic::kLazyStartRing + la.seq % ebic::kLazyStartRing, ctx->d_lcount,
+                              sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));  // the window end (lazy_window_end)
     const unsigned bgrid = (unsigned)ctx->n_sms * 8;
     if (ctx->store == EBIC_STORE_F64)
       ebic::lazy_build_kernel<double><<<bgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
@@ -879,6 +929,34 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     const uint32_t J = (nv + 31) / 32;
     const int S = lazy ? 2 : ctx->tma_slots;
     const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
+    bool pdl = ctx->pdl;
+    const size_t slab_smem = ebic::slab_build_smem((uint32_t)ctx->n_cols);
+    if (lazy && plan.la.cold && ctx->store == EBIC_STORE_F32 &&
+        (n_cand >= kLazyColdMinCand || ctx->lazy_build == EBIC_LAZY_BUILD_FIRST) &&
+        slab_smem <= ctx->smem_optin) {
+      // a cold batch (the pool still filling fast): claim its missing pairs,
+      // build them from 32-row slices of the whole matrix staged once per CTA
+      // (lazy_slab_build_kernel), publish, then count -- nothing left to build
+      // inside the count kernel (which runs without PDL: it reads what the
+      // publish kernel wrote)
+      const uint32_t wp = (uint32_t)table_wp(ctx);
+      ebic::LazyArgs la = plan.la;
+      la.defer = nullptr;
+      la.pslot = nullptr;
+      EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + la.seq % ebic::kLazyStartRing, ctx->d_lcount, sizeof(uint32_t),
+                                cudaMemcpyDeviceToDevice, s));
+      const unsigned cgrid = (unsigned)std::min<uint64_t>((n_cand + 7) / 8, (uint64_t)ctx->n_sms * 16);
+      ebic::lazy_claim_kernel<<<cgrid, 256, 0, s>>>(la, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx,
+                                                    (uint32_t)ctx->n_cols, 1, neg);
+      EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + ebic::kLazyStartRing + la.seq % ebic::kLazyStartRing, ctx->d_lcount,
+                                sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));  // the window end
+      EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel), ctx));
+      ebic::lazy_slab_build_kernel<<<(unsigned)ctx->n_sms * 2, ebic::kSlabBuildThreads, slab_smem, s>>>(
+          la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+      ebic::lazy_publish_kernel<<<(unsigned)ctx->n_sms * 2, 256, 0, s>>>(la);
+      ctx->launches += 3;
+      pdl = false;
+    }
     auto go = [&](auto kern) -> int {
       EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(kern), ctx));
       // persistent warps: as many CTAs as are resident at once (the kernel
@@ -888,7 +966,7 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
                                                          std::max<uint64_t>(1, per_sm) * ctx->n_sms);
       // programmatic dependent launch (ebic_table.cuh pdl_trigger / pdl_wait):
       // back-to-back batches overlap one kernel's tail with the next one's start
-      EBIC_CUDA(launch_pdl(kern, dim3(grid), dim3(ebic::kTmaWarps * 32), smem, s, ctx->pdl,
+      EBIC_CUDA(launch_pdl(kern, dim3(grid), dim3(ebic::kTmaWarps * 32), smem, s, pdl,
                            (const uint32_t*)ctx->d_table, (uint32_t)ctx->n_cols, (uint32_t)table_wp(ctx),
                            (uint32_t)ctx->n_rows, d_cols, d_offs, (uint32_t)n_cand, (uint32_t)n_idx, out,
                            err_out ? err_out : ctx->d_err, d_mask, (uint64_t)(ctx->ld / 32), plan.la));
@@ -1680,6 +1758,9 @@ int ebic_ctx_create(int device, ebic_ctx** ctx_out) {
     if (ts) ctx->tma_slots = std::max(2, std::min(4, std::atoi(ts)));
     const char* tk = std::getenv("EBIC_TABLE_KERNEL");
     if (tk) ctx->table_kernel = std::atoi(tk);
+    ctx->lazy_trace = std::getenv("EBIC_LAZY_TRACE") != nullptr;
+    const char* lb = std::getenv("EBIC_LAZY_BUILD");
+    if (lb) ctx->lazy_build = std::max(0, std::min(2, std::atoi(lb)));
     const char* pd = std::getenv("EBIC_PDL");
     if (pd) ctx->pdl = std::atoi(pd) != 0;
     const char* xt = std::getenv("EBIC_XCHG_TIMEOUT_MS");
@@ -2226,6 +2307,14 @@ int ebic_ctx_set_pair_layout(ebic_ctx* ctx, int rows_per_lane_pairs, int cands_p
   if (!ok_p || !ok_s)
     return fail(EBIC_ERR_INVALID_ARGUMENT, "bad packed-pair layout (%d, %d)", rows_per_lane_pairs, cands_per_warp);
   ctx->simd_force = rows_per_lane_pairs * 16 + cands_per_warp;
+  return EBIC_OK;
+}
+
+int ebic_ctx_set_lazy_build(ebic_ctx* ctx, int mode) {
+  if (!ctx) return fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+  if (mode < EBIC_LAZY_BUILD_AUTO || mode > EBIC_LAZY_BUILD_FIRST)
+    return fail(EBIC_ERR_INVALID_ARGUMENT, "lazy build mode %d (0 auto, 1 inline, 2 build first)", mode);
+  ctx->lazy_build = mode;
   return EBIC_OK;
 }
 

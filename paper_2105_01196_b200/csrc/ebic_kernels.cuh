@@ -88,11 +88,19 @@ __device__ bool row_exact(const T* __restrict__ mat, uint64_t ld, uint64_t row,
   return true;
 }
 
+// Half-width of the float32 bracket of thr64(x) around t = x - a_f |x|
+// (|x| = ax).  x = +-0 has the exact threshold +-0 (thr64: x - a * 0), which
+// t reproduces, so its bracket is empty: no row with x = 0 (common: zeros in
+// expression data) takes the double test.
+__device__ __forceinline__ float bracket_halfwidth(float ax, float kscale) {
+  return ax > 0.f ? __fmaf_rn(kscale, ax, 0x1p-146f) : 0.f;
+}
+
 // Per-element bracket of the threshold, float32 filter mode.
 __device__ __forceinline__ void bracket(float x, const TrendArgs& ta, float& lo, float& hi) {
   const float ax = fabsf(x);
   const float t = __fmaf_rn(-ta.a_f, ax, x);
-  const float d = __fmaf_rn(ta.kscale, ax, 0x1p-146f);
+  const float d = bracket_halfwidth(ax, ta.kscale);
   lo = __fsub_rn(t, d);
   hi = __fadd_rn(t, d);
 }

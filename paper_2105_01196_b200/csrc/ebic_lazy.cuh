@@ -59,6 +59,8 @@ struct LazyArgs {
   int f64;              // store is double
   double approx;
   float a_f, kscale;    // float32 bracket of the threshold (ebic_kernels.cuh bracket / make_args)
+  int cold;             // host: the pool is still filling fast -- build the batch's pairs first
+                        // (lazy_slab_build_kernel) instead of inside the count kernel
 };
 
 // The per-row test's parameters: the reference threshold in double, and a
@@ -84,7 +86,7 @@ __device__ __forceinline__ bool pair_bit(double x, double y, const PairThr& th) 
 __device__ __forceinline__ bool pair_bit(float x, float y, const PairThr& th) {
   const float ax = fabsf(x);
   const float t = __fmaf_rn(-th.a_f, ax, x);
-  const float d = __fmaf_rn(th.kscale, ax, 0x1p-146f);
+  const float d = bracket_halfwidth(ax, th.kscale);
   if (y > __fadd_rn(t, d)) return true;
   if (y <= __fsub_rn(t, d)) return false;
   return (double)y > thr64((double)x, th.approx);
@@ -180,7 +182,7 @@ __device__ __forceinline__ uint32_t pair_word_staged(const float* __restrict__ c
     const float x = sx[lane * 33 + j], y = sy[lane * 33 + j];
     const float ax = fabsf(x);
     const float t = __fmaf_rn(-th.a_f, ax, x);
-    const float d = __fmaf_rn(th.kscale, ax, 0x1p-146f);
+    const float d = bracket_halfwidth(ax, th.kscale);
     const uint32_t bit = 1u << index_row_bit((uint32_t)j);
     word |= y > __fadd_rn(t, d) ? bit : 0u;
     unc |= (y > __fsub_rn(t, d) && !(y > __fadd_rn(t, d))) ? (1u << j) : 0u;
@@ -296,6 +298,14 @@ __device__ __forceinline__ uint32_t lazy_lookup(const LazyArgs& la, uint64_t p) 
 // a key is set only between its batch's claim and build.
 constexpr uint32_t kLazyKeyBits = 26;
 constexpr uint32_t kLazyStartRing = 64;
+// start[kLazyStartRing + seq % kLazyStartRing]: the count right after the
+// batch's claim kernel (copied on the stream).  Every CTA of the build and
+// publish kernels uses this one window end: other streams keep claiming while
+// they run, and CTAs that each read the live count would partition the window
+// differently (units never built, slots never published).
+__device__ __forceinline__ uint32_t lazy_window_end(const LazyArgs& la) {
+  return min(la.start[kLazyStartRing + la.seq % kLazyStartRing], la.cap);
+}
 __host__ __device__ __forceinline__ uint32_t lazy_tag(uint32_t seq) { return seq % 63u; }
 
 // Did this batch claim slot s for pair p?  (A claim's key is written right
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(256)
 lazy_claim_kernel(const LazyArgs la, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ offs,
                   uint32_t n_cand, uint32_t n_idx, uint32_t n_cols, uint32_t n_chunks, int neg) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    la.defer[0] = 0;  // (read by this batch's count kernel, which runs after this one)
+    if (la.defer) la.defer[0] = 0;  // (read by this batch's count kernel, which runs after this one)
     if (la.count_out) {  // the host's lagged view of the pool's fill
       la.count_out[0] = *(volatile uint32_t*)la.count;
       __threadfence_system();
@@ -355,7 +365,7 @@ lazy_claim_kernel(const LazyArgs la, const uint32_t* __restrict__ cols, const ui
       const uint32_t sf = lazy_claim_pair(la, (uint64_t)x * n_cols + y, n_chunks);
       const uint32_t sr = neg ? lazy_claim_pair(la, (uint64_t)y * n_cols + x, n_chunks) : kSlotEmpty;
       const uint32_t q = k - b - 1;  // pair index
-      if (q < 31) {
+      if (la.pslot && q < 31) {  // (no pslot: lazy_slab_build_kernel's batches count with the TMA kernel)
         la.pslot[(uint64_t)i * 64 + q] = sf;
         if (neg) la.pslot[(uint64_t)i * 64 + 32 + q] = sr;
       }
@@ -367,7 +377,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 lazy_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t wp) {
   const uint32_t start = la.start[la.seq % kLazyStartRing];
-  const uint32_t end = min(*(volatile uint32_t*)la.count, la.cap);
+  const uint32_t end = lazy_window_end(la);
   const uint32_t tag = lazy_tag(la.seq);
   if (end <= start) return;
   const uint32_t n_jobs = end - start, n_chunks = (wp + 31) / 32;
@@ -399,6 +409,165 @@ lazy_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t 
       la.keys[t] = kSlotEmpty;
       atomicExch(la.map + key, t);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cold batches of short vectors (float32 store): claim (lazy_claim_kernel),
+// build every claimed slot here, publish (lazy_publish_kernel), then count
+// with nothing left to build.  A pair vector built inside the count kernel
+// reads both of its columns (2 x 80 KB at 20k rows) for 2.5 KB of output -- a
+// C3 population's 48K first-visit vectors re-read the matrix ~100 times (11 GB
+// of L2 traffic, 2.2 ms).  Here a CTA stages one 16-row slice of EVERY column
+// (64 bytes per column) and builds that half-word of every slot in its part
+// of the window from shared memory: a half-warp per slot -- lane i on row
+// index_bit_row(i), so one ballot is two slots' half-words in index layout --
+// the float32 bracket of the threshold, the double test only for the rare
+// rows inside it.  Two CTAs per SM: one stages while the other builds.
+//
+// Units are (half-word h of the vectors, part of the slot window); the part
+// count is chosen on the device so the units balance over the grid.
+constexpr uint32_t kSlabBuildThreads = 512;
+
+__host__ __device__ constexpr uint32_t slab_build_smem(uint32_t n_cols) {
+  return n_cols * 16 * 4 + (kSlabBuildThreads / 32) * 32 * 8;
+}
+
+__global__ void __launch_bounds__(kSlabBuildThreads, 2)
+lazy_slab_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t wp) {
+  const uint32_t start = la.start[la.seq % kLazyStartRing];
+  const uint32_t end = lazy_window_end(la);
+  if (end <= start) return;
+  const uint32_t tag = lazy_tag(la.seq);
+  constexpr int kWarps = kSlabBuildThreads / 32;
+  const uint32_t n_halves = 2 * wp;
+  // parts: >= 8 units per CTA, >= 2 slots per lane per part
+  const uint32_t n_jobs = end - start;
+  const uint32_t n_parts = max(1u, min((8u * gridDim.x + n_halves - 1) / n_halves, n_jobs / (2u * kSlabBuildThreads)));
+  const uint32_t per_part = (n_jobs + n_parts - 1) / n_parts;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* mat = static_cast<const float*>(la.mat);
+  const PairThr th = pair_thr(la);
+  extern __shared__ float4 smem4[];
+  float* sv = reinterpret_cast<float*>(smem4);                                   // [n_cols][16] values
+  uint2* soff = reinterpret_cast<uint2*>(sv + (size_t)n_cols * 16) + warp * 32;  // the group's 32 (a, b) * 16
+  const uint32_t row_off = 4u * index_bit_row((uint32_t)(lane & 15));  // this lane's row (0..15), bytes
+  const uint32_t half_sel = (uint32_t)(lane & 16);                      // 0: slot j, 16: slot j + 16
+  const unsigned char* sv_b = reinterpret_cast<const unsigned char*>(sv);
+  auto lds_f32 = [&](uint32_t byte_off) { return *reinterpret_cast<const float*>(sv_b + byte_off); };
+  uint16_t* pool16 = reinterpret_cast<uint16_t*>(la.pool);
+  const uint64_t n_units = (uint64_t)n_halves * n_parts;
+  for (uint64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const uint32_t hv = (uint32_t)(u / n_parts), part = (uint32_t)(u % n_parts);
+    const uint32_t w = hv >> 1, hw = hv & 1;
+    const uint32_t t_begin = start + part * per_part, t_end = min(end, t_begin + per_part);
+    const uint32_t r0 = 32u * w + 16u * hw;  // (r0 + 16 <= ld: ld is a multiple of 256)
+    __syncthreads();  // the previous slice is no longer read
+    {
+      constexpr int UNR = 4;  // loads in flight per thread
+      const uint32_t total = n_cols * 4;
+      for (uint32_t i0 = threadIdx.x; i0 < total; i0 += UNR * kSlabBuildThreads) {
+        float4 x[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const uint32_t i = i0 + k * kSlabBuildThreads;
+          if (i < total) x[k] = __ldg(reinterpret_cast<const float4*>(mat + (uint64_t)(i >> 2) * la.ld + r0) + (i & 3));
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+          const uint32_t i = i0 + k * kSlabBuildThreads;
+          if (i < total) reinterpret_cast<float4*>(sv)[i] = x[k];
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t valid = (index_valid_bits(n_rows, w) >> (16 * hw)) & 0xFFFFu;
+    uint32_t tk_next = t_begin + 32u * warp + lane < t_end ? __ldcg(la.keys + t_begin + 32u * warp + lane) : kSlotEmpty;
+    for (uint32_t t0 = t_begin + 32u * warp; t0 < t_end; t0 += 32u * kWarps) {
+      const uint32_t t = t0 + lane;
+      const uint32_t tk = tk_next;  // (loaded one group ahead)
+      tk_next = t + 32u * kWarps < t_end ? __ldcg(la.keys + t + 32u * kWarps) : kSlotEmpty;
+      const bool own = tk != kSlotEmpty && (tk >> kLazyKeyBits) == tag;
+      const uint32_t key = tk & ((1u << kLazyKeyBits) - 1u);
+      const uint32_t ka = own ? key / n_cols : 0u;
+      // byte offsets of the slot's two column slices
+      soff[lane] = make_uint2(ka * 64u, own ? (key - ka * n_cols) * 64u : 0u);
+      const uint32_t own_m = __ballot_sync(kFull, own);
+      __syncwarp();
+      if (own_m) {
+        bool unc = false;  // a row of this lane inside a bracket (rare): the double test below
+        uint32_t hv = 0;   // ballot (lane & 15): this lane's slot's half-word in its low / high half
+        // lanes 0..15: slot j, lanes 16..31: slot j + 16.  Software-pipelined:
+        // the next two slots' offsets (one 16-byte load) and slot j + 1's
+        // values are in flight while slot j is tested.
+        const uint4* soff4 = reinterpret_cast<const uint4*>(soff + half_sel);
+        uint4 o2 = soff4[0];
+        float x_next = lds_f32(o2.x + row_off);
+        float y_next = lds_f32(o2.y + row_off);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float x = x_next, y = y_next;
+          if (j + 1 < 16) {
+            if (j & 1) {
+              o2 = soff4[(j + 1) >> 1];
+              x_next = lds_f32(o2.x + row_off);
+              y_next = lds_f32(o2.y + row_off);
+            } else {
+              x_next = lds_f32(o2.z + row_off);
+              y_next = lds_f32(o2.w + row_off);
+            }
+          }
+          const float ax = fabsf(x);
+          const float tt = __fmaf_rn(-th.a_f, ax, x);
+          const float d = bracket_halfwidth(ax, th.kscale);
+          const bool above = y > __fadd_rn(tt, d);
+          unc |= !above && y > __fsub_rn(tt, d);
+          const uint32_t bal = __ballot_sync(kFull, above);
+          hv = (lane & 15) == j ? bal : hv;
+        }
+        if (__any_sync(kFull, unc)) {
+          // some row sits inside its bracket: redo the warp's ballots with the
+          // reference's double test for those rows
+          __syncwarp();
+#pragma unroll 1
+          for (int j = 0; j < 16; ++j) {
+            const uint2 oj = soff[half_sel + j];
+            const float x = lds_f32(oj.x + row_off), y = lds_f32(oj.y + row_off);
+            const float ax = fabsf(x);
+            const float tt = __fmaf_rn(-th.a_f, ax, x);
+            const float d = bracket_halfwidth(ax, th.kscale);
+            bool bit = y > __fadd_rn(tt, d);
+            if (!bit && y > __fsub_rn(tt, d)) bit = (double)y > thr64((double)x, th.approx);
+            const uint32_t bal = __ballot_sync(kFull, bit);
+            hv = (lane & 15) == j ? bal : hv;
+          }
+        }
+        // lane l: the half-word of slot t0 + l (ballot l & 15, low or high half)
+        const uint32_t h = (hv >> half_sel) & 0xFFFFu;
+        if (own) pool16[((uint64_t)t * wp + w) * 2 + hw] = (uint16_t)(h & valid);
+      }
+      __syncwarp();  // soff is refilled by the next group
+    }
+  }
+}
+
+// Publish the slots lazy_slab_build_kernel built for this batch (map[p] = t)
+// and release their keys.  Runs after the build kernel on the same stream.
+__global__ void __launch_bounds__(256) lazy_publish_kernel(const LazyArgs la) {
+  const uint32_t start = la.start[la.seq % kLazyStartRing];
+  const uint32_t end = lazy_window_end(la);
+  const uint32_t tag = lazy_tag(la.seq);
+  if (la.count_out && blockIdx.x == 0 && threadIdx.x == 0) {  // the fill after this batch's claims
+    la.count_out[0] = *(volatile uint32_t*)la.count;
+    __threadfence_system();
+    la.count_out[1] = la.seq;
+  }
+  for (uint32_t t = start + blockIdx.x * blockDim.x + threadIdx.x; t < end; t += gridDim.x * blockDim.x) {
+    const uint32_t tk = __ldcg(la.keys + t);
+    if (tk == kSlotEmpty || (tk >> kLazyKeyBits) != tag) continue;
+    la.keys[t] = kSlotEmpty;
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // (the count kernel reads the pool by TMA)
+    atomicExch(la.map + (tk & ((1u << kLazyKeyBits) - 1u)), t);
   }
 }
 

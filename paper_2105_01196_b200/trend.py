@@ -166,6 +166,10 @@ class Evaluator:
         """Memory cap of the pair-trend index (AUTO path uses it only below the cap)."""
         check(self._L.ebic_ctx_set_table_budget(self._h, int(nbytes)))
 
+    def set_lazy_build(self, mode: int = 0) -> None:
+        """Lazy index build route: 0 auto (cold batches build first), 1 inside the count kernel, 2 build pass first."""
+        check(self._L.ebic_ctx_set_lazy_build(self._h, int(mode)))
+
     def index_info(self) -> tuple[int, bool]:
         """(bytes the pair-trend index of the resident matrix needs, whether it is built)."""
         nb, used = C.c_uint64(0), C.c_int(0)

@@ -42,12 +42,16 @@ def _pop(C, n, seed, dup_pairs=False):
 # multi-pass count kernel instead of builds inside the TMA kernel
 @pytest.mark.parametrize("R", [1, 33, 1000, 4099, 20000, 32768, 32769, 70001])
 @pytest.mark.parametrize("f64", [False, True])
-def test_lazy_index_vs_oracle(evaluator, R, f64):
+@pytest.mark.parametrize("build", [0, 1, 2], ids=["auto", "inline", "first"])
+def test_lazy_index_vs_oracle(evaluator, R, f64, build):
+    """Every build route of the lazy index (auto; inside the count kernel;
+    the slab build pass ahead of it) against the oracle."""
     C = 150
     m = _matrix(R, C, R + 7 * f64, f64)
     store = evaluator.upload(m)
     assert (store == EBIC_STORE_F64) == f64
     evaluator.set_path(EBIC_PATH_LAZY)
+    evaluator.set_lazy_build(build)
     try:
         for batch in range(3):  # first use, then reuse (and new pairs) across batches
             pop = _pop(C, 700, seed=batch, dup_pairs=batch == 1)
@@ -64,10 +68,12 @@ def test_lazy_index_vs_oracle(evaluator, R, f64):
         assert st["lazy_slots_cap"] > 0 and st["lazy_bytes"] > 0
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
+        evaluator.set_lazy_build(0)
 
 
 @pytest.mark.parametrize("R", [9000, 40000])
-def test_lazy_pool_too_small_resets_and_private_builds(evaluator, R):
+@pytest.mark.parametrize("build", [0, 2], ids=["auto", "first"])
+def test_lazy_pool_too_small_resets_and_private_builds(evaluator, R, build):
     """A budget that holds only a few dozen pair vectors: most new pairs find
     no slot (private builds; for long vectors, slices computed by the count
     kernel), the pool starts over; counts stay exact."""
@@ -77,6 +83,7 @@ def test_lazy_pool_too_small_resets_and_private_builds(evaluator, R):
     wp = ((R + 31) // 32 + 127) // 128 * 128 if (R + 31) // 32 > 128 else ((R + 31) // 32 + 3) // 4 * 4
     evaluator.set_table_budget(C * C * 4 + 40 * wp * 4)
     evaluator.set_path(EBIC_PATH_LAZY)
+    evaluator.set_lazy_build(build)
     try:
         for batch in range(6):
             pop = _pop(C, 500, seed=100 + batch, dup_pairs=True)
@@ -89,19 +96,23 @@ def test_lazy_pool_too_small_resets_and_private_builds(evaluator, R):
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
         evaluator.set_table_budget(0)
+        evaluator.set_lazy_build(0)
 
 
-@pytest.mark.parametrize("R,n_streams", [(12000, 1), (40000, 1), (40000, 2)])
-def test_lazy_device_api_back_to_back(evaluator, R, n_streams):
+@pytest.mark.parametrize("R,n_streams,build", [(12000, 1, 0), (40000, 1, 0), (40000, 2, 0), (12000, 2, 0),
+                                                (12000, 2, 1), (12000, 2, 2), (12000, 1, 2)])
+def test_lazy_device_api_back_to_back(evaluator, R, n_streams, build):
     """Device-pointer batches issued back to back (no host sync, programmatic
     dependent launch, the host's view of the pool lagging): exact.  With two
-    streams, long-vector batches claim and build concurrently (the batch tags
-    keep each build kernel to its own slots)."""
+    streams, batches claim and build concurrently (the batch tags keep each
+    build kernel to its own slots; a pair another stream is building is built
+    privately by the count kernel)."""
     torch = pytest.importorskip("torch")
     C = 400
     m = _matrix(R, C, 11)
     evaluator.upload(m)
     evaluator.set_path(EBIC_PATH_LAZY)
+    evaluator.set_lazy_build(build)
     try:
         pops = [synth.random_population(5000, C, 2, 8, seed=300 + k) for k in range(6)]
         want = [oracle.evaluate_population(m, p.cols, p.offsets, 0.03, True) for p in pops]
@@ -121,6 +132,7 @@ def test_lazy_device_api_back_to_back(evaluator, R, n_streams):
             np.testing.assert_array_equal(outs[i].cpu().numpy().view(np.uint32), want[i % 6], err_msg=f"launch {i}")
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
+        evaluator.set_lazy_build(0)
 
 
 def test_auto_policy_lazy_then_full(evaluator):
