@@ -865,7 +865,20 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + ebic::kLazyStartRing + la.seq % ebic::kLazyStartRing, ctx->d_lcount,
                               sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));  // the window end (lazy_window_end)
     const unsigned bgrid = (unsigned)ctx->n_sms * 8;
-    if (ctx->store == EBIC_STORE_F64)
+    const size_t slab_smem = ebic::slab_build_smem((uint32_t)ctx->n_cols);
+    if (ctx->store == EBIC_STORE_F32 && ctx->lazy_build != EBIC_LAZY_BUILD_INLINE && slab_smem <= ctx->smem_optin) {
+      // 16-row slices of every column staged once per unit (the cold-batch
+      // builder of the short path), then publish: the claimed slots are then
+      // all ready for the count kernel
+      EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel), ctx));
+      const unsigned sgrid = (unsigned)ctx->n_sms *
+          (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel),
+                                              ebic::kSlabBuildThreads, slab_smem));
+      ebic::lazy_slab_build_kernel<<<sgrid, ebic::kSlabBuildThreads, slab_smem, s>>>(la, (uint32_t)ctx->n_rows,
+                                                                                      (uint32_t)ctx->n_cols, wp);
+      ebic::lazy_publish_kernel<<<(unsigned)ctx->n_sms * 2, 256, 0, s>>>(la);
+      ctx->launches++;
+    } else if (ctx->store == EBIC_STORE_F64)
       ebic::lazy_build_kernel<double><<<bgrid, 256, 0, s>>>(la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
     else {
       const size_t smem = 8 * ebic::kStageFloats * sizeof(float);
@@ -951,7 +964,10 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
       EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + ebic::kLazyStartRing + la.seq % ebic::kLazyStartRing, ctx->d_lcount,
                                 sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));  // the window end
       EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel), ctx));
-      ebic::lazy_slab_build_kernel<<<(unsigned)ctx->n_sms * 2, ebic::kSlabBuildThreads, slab_smem, s>>>(
+      const unsigned sgrid = (unsigned)ctx->n_sms *
+          (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel),
+                                              ebic::kSlabBuildThreads, slab_smem));
+      ebic::lazy_slab_build_kernel<<<sgrid, ebic::kSlabBuildThreads, slab_smem, s>>>(
           la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
       ebic::lazy_publish_kernel<<<(unsigned)ctx->n_sms * 2, 256, 0, s>>>(la);
       ctx->launches += 3;
