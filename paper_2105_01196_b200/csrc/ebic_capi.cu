@@ -803,6 +803,27 @@ uint64_t worst_pairs(uint64_t n_cand, uint64_t n_idx, int neg) {
   return pairs * (neg ? 2 : 1);
 }
 
+// lazy_slab_build_kernel: 512 threads x 2 CTAs per SM while two slices fit
+// in shared memory, else 1024 threads x 1 (C up to ~3400 at 227 KB).
+bool slab_build_fits(const ebic_ctx* ctx) {
+  return ctx->store == EBIC_STORE_F32 && ebic::slab_build_smem((uint32_t)ctx->n_cols, 1024) <= ctx->smem_optin;
+}
+int launch_slab_build(ebic_ctx* ctx, const ebic::LazyArgs& la, uint32_t wp, cudaStream_t s) {
+  const uint32_t C = (uint32_t)ctx->n_cols;
+  auto go = [&](auto kern, uint32_t threads) -> int {
+    const size_t smem = ebic::slab_build_smem(C, threads);
+    EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(kern), ctx));
+    const unsigned grid = (unsigned)ctx->n_sms *
+        (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(kern), (int)threads, smem));
+    kern<<<grid, threads, smem, s>>>(la, (uint32_t)ctx->n_rows, C, wp);
+    EBIC_CUDA(cudaGetLastError());
+    return EBIC_OK;
+  };
+  if (2 * (ebic::slab_build_smem(C, 512) + 1024) <= ctx->smem_optin + 1024)
+    return go(ebic::lazy_slab_build_kernel<512>, 512);
+  return go(ebic::lazy_slab_build_kernel<1024>, 1024);
+}
+
 // Counts WRITTEN to out (any device-accessible pointer), optional row masks.
 // n_idx bounds the offsets (checked on device).
 template <bool MASK>
@@ -865,17 +886,11 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + ebic::kLazyStartRing + la.seq % ebic::kLazyStartRing, ctx->d_lcount,
                               sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));  // the window end (lazy_window_end)
     const unsigned bgrid = (unsigned)ctx->n_sms * 8;
-    const size_t slab_smem = ebic::slab_build_smem((uint32_t)ctx->n_cols);
-    if (ctx->store == EBIC_STORE_F32 && ctx->lazy_build != EBIC_LAZY_BUILD_INLINE && slab_smem <= ctx->smem_optin) {
+    if (slab_build_fits(ctx) && ctx->lazy_build != EBIC_LAZY_BUILD_INLINE) {
       // 16-row slices of every column staged once per unit (the cold-batch
       // builder of the short path), then publish: the claimed slots are then
       // all ready for the count kernel
-      EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel), ctx));
-      const unsigned sgrid = (unsigned)ctx->n_sms *
-          (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel),
-                                              ebic::kSlabBuildThreads, slab_smem));
-      ebic::lazy_slab_build_kernel<<<sgrid, ebic::kSlabBuildThreads, slab_smem, s>>>(la, (uint32_t)ctx->n_rows,
-                                                                                      (uint32_t)ctx->n_cols, wp);
+      EBIC_TRY(launch_slab_build(ctx, la, wp, s));
       ebic::lazy_publish_kernel<<<(unsigned)ctx->n_sms * 2, 256, 0, s>>>(la);
       ctx->launches++;
     } else if (ctx->store == EBIC_STORE_F64)
@@ -943,10 +958,8 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     const int S = lazy ? 2 : ctx->tma_slots;
     const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
     bool pdl = ctx->pdl;
-    const size_t slab_smem = ebic::slab_build_smem((uint32_t)ctx->n_cols);
-    if (lazy && plan.la.cold && ctx->store == EBIC_STORE_F32 &&
-        (n_cand >= kLazyColdMinCand || ctx->lazy_build == EBIC_LAZY_BUILD_FIRST) &&
-        slab_smem <= ctx->smem_optin) {
+    if (lazy && plan.la.cold && slab_build_fits(ctx) &&
+        (n_cand >= kLazyColdMinCand || ctx->lazy_build == EBIC_LAZY_BUILD_FIRST)) {
       // a cold batch (the pool still filling fast): claim its missing pairs,
       // build them from 32-row slices of the whole matrix staged once per CTA
       // (lazy_slab_build_kernel), publish, then count -- nothing left to build
@@ -963,12 +976,7 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
                                                     (uint32_t)ctx->n_cols, 1, neg);
       EBIC_CUDA(cudaMemcpyAsync(ctx->d_lstart + ebic::kLazyStartRing + la.seq % ebic::kLazyStartRing, ctx->d_lcount,
                                 sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));  // the window end
-      EBIC_TRY(allow_max_smem(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel), ctx));
-      const unsigned sgrid = (unsigned)ctx->n_sms *
-          (unsigned)std::max(1, resident_ctas(reinterpret_cast<const void*>(ebic::lazy_slab_build_kernel),
-                                              ebic::kSlabBuildThreads, slab_smem));
-      ebic::lazy_slab_build_kernel<<<sgrid, ebic::kSlabBuildThreads, slab_smem, s>>>(
-          la, (uint32_t)ctx->n_rows, (uint32_t)ctx->n_cols, wp);
+      EBIC_TRY(launch_slab_build(ctx, la, wp, s));
       ebic::lazy_publish_kernel<<<(unsigned)ctx->n_sms * 2, 256, 0, s>>>(la);
       ctx->launches += 3;
       pdl = false;

@@ -427,14 +427,18 @@ lazy_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t 
 //
 // Units are (half-word h of the vectors, part of the slot window); the part
 // count is chosen on the device so the units balance over the grid.
-constexpr uint32_t kSlabBuildThreads = 512;
 
-__host__ __device__ constexpr uint32_t slab_build_smem(uint32_t n_cols) {
-  return n_cols * 16 * 4 + (kSlabBuildThreads / 32) * 32 * 8;
+
+// THREADS = 512 (two CTAs per SM: one stages while the other builds) while
+// two slices fit in shared memory (C <= ~1700), else 1024 (one CTA per SM).
+__host__ __device__ constexpr uint32_t slab_build_smem(uint32_t n_cols, uint32_t threads) {
+  return n_cols * 16 * 4 + (threads / 32) * 32 * 8;
 }
 
-__global__ void __launch_bounds__(kSlabBuildThreads, 2)
+template <uint32_t THREADS>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS)
 lazy_slab_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint32_t wp) {
+  constexpr uint32_t kSlabBuildThreads = THREADS;
   const uint32_t start = la.start[la.seq % kLazyStartRing];
   const uint32_t end = lazy_window_end(la);
   if (end <= start) return;
@@ -461,9 +465,13 @@ lazy_slab_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint
     const uint32_t hv = (uint32_t)(u / n_parts), part = (uint32_t)(u % n_parts);
     const uint32_t w = hv >> 1, hw = hv & 1;
     const uint32_t t_begin = start + part * per_part, t_end = min(end, t_begin + per_part);
-    const uint32_t r0 = 32u * w + 16u * hw;  // (r0 + 16 <= ld: ld is a multiple of 256)
+    const uint32_t r0 = 32u * w + 16u * hw;
+    // a half past the last row (the vector's padding words, wp rounded up) is
+    // all zeros and is not staged: the store holds ld rows per column, and a
+    // half with any valid row ends by 32 ceil(R / 32) <= ld
+    const bool dead = r0 >= n_rows;
     __syncthreads();  // the previous slice is no longer read
-    {
+    if (!dead) {
       constexpr int UNR = 4;  // loads in flight per thread
       const uint32_t total = n_cols * 4;
       for (uint32_t i0 = threadIdx.x; i0 < total; i0 += UNR * kSlabBuildThreads) {
@@ -494,7 +502,9 @@ lazy_slab_build_kernel(const LazyArgs la, uint32_t n_rows, uint32_t n_cols, uint
       soff[lane] = make_uint2(ka * 64u, own ? (key - ka * n_cols) * 64u : 0u);
       const uint32_t own_m = __ballot_sync(kFull, own);
       __syncwarp();
-      if (own_m) {
+      if (own_m && dead) {
+        if (own) pool16[((uint64_t)t * wp + w) * 2 + hw] = 0;
+      } else if (own_m) {
         bool unc = false;  // a row of this lane inside a bracket (rare): the double test below
         uint32_t hv = 0;   // ballot (lane & 15): this lane's slot's half-word in its low / high half
         // lanes 0..15: slot j, lanes 16..31: slot j + 16.  Software-pipelined:

@@ -9,7 +9,8 @@ Round 2: the lazy index (short vectors built inside the TMA kernel; long
 vectors through the claim / build / count / deferred kernels, with a pool too
 small for the batch), the lane-group kernel, the software-pipelined
 multi-pass kernel (full and lazy), small batches read in place, and the
-staged upload of a pageable matrix."""
+staged upload of a pageable matrix; the lazy index's build-first route
+(claim, slab-staged build at 512 and 1024 threads, publish)."""
 import sys
 from pathlib import Path
 
@@ -86,6 +87,22 @@ for R, Cn, P in ((5000, 60, 300), (40000, 40, 5000)):
         rows = ev.supporting_rows(pop.sequence(1), TrendParams(0.03, True))
         ok &= np.array_equal(rows, oracle.supporting_rows(m, pop.sequence(1), 0.03, True))
         ev.set_table_budget(0)
+        ev.set_path(EBIC_PATH_AUTO)
+# the build-first route of the lazy index (claim, slab-staged build with 512
+# and 1024 threads, publish) for short and long vectors, and the inline route
+for R, Cn, P in ((3000, 80, 400), (40000, 40, 600), (2000, 1800, 400)):
+    m = rng.standard_normal((R, Cn)).astype(np.float32)
+    m[: R // 3] = np.sort(m[: R // 3], axis=1)
+    m[rng.random(m.shape) < 0.05] = 0.0
+    pop = synth.random_population(P, Cn, 2, 6, seed=5)
+    for build in (2, 1):
+        ev.upload(m)
+        ev.set_path(EBIC_PATH_LAZY)
+        ev.set_lazy_build(build)
+        for neg in (False, True):
+            ok &= np.array_equal(ev.evaluate_population(pop, TrendParams(0.03, neg)),
+                                 oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, neg))
+        ev.set_lazy_build(0)
         ev.set_path(EBIC_PATH_AUTO)
 # small page-locked batch read in place; the lane-group kernel (R <= 4096)
 m = rng.standard_normal((3000, 200)).astype(np.float32)
