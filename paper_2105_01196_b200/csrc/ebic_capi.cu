@@ -596,6 +596,7 @@ int lazy_new_epoch(ebic_ctx* ctx, cudaStream_t s) {
 // privately (short vectors) or computed by the count kernel (long ones).
 int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, ebic::LazyArgs* la) {
   NvtxRange nvtx_("ebic:lazy_reserve");
+  const double t_enter = ctx->lazy_trace ? host_ms() : 0.0;
   const uint64_t vec_bytes = table_wp(ctx) * sizeof(uint32_t);
   if (!ctx->d_lmap) {
     EBIC_CUDA(cudaMalloc(&ctx->d_lmap, lazy_map_bytes(ctx)));
@@ -713,10 +714,12 @@ int lazy_reserve(ebic_ctx* ctx, double approx, uint64_t worst, cudaStream_t s, e
   }
   const uint32_t seq = ++ctx->lazy_seq;
   if (ctx->lazy_trace)
-    std::fprintf(stderr, "lazy: seq %u stream %p cold %d used %llu (sample %u/%u growth %llu) cap %llu worst %llu\n", seq,
-                 (void*)s, la->cold, (unsigned long long)used, m_count, m_seq,
+    std::fprintf(stderr,
+                 "lazy: seq %u stream %p cold %d used %llu (sample %u/%u growth %llu) cap %llu worst %llu "
+                 "reserve %.3f ms\n",
+                 seq, (void*)s, la->cold, (unsigned long long)used, m_count, m_seq,
                  (unsigned long long)ctx->lazy_recent_growth, (unsigned long long)ctx->lcap,
-                 (unsigned long long)worst);
+                 (unsigned long long)worst, host_ms() - t_enter);
   la->map = ctx->d_lmap;
   la->pool = ctx->d_lpool;
   la->count = ctx->d_lcount;
