@@ -266,7 +266,7 @@ struct ebic_ctx {
   int plane_builder = 0;  // EBIC_PLANE_BUILDER: 0 auto, 1 per-row block builder, 2 row-tile builder
   uint64_t table_cap = 0;   // bytes allocated at d_table (kept across uploads for reuse)
   int table_build_a = 2;    // EBIC_TABLE_BUILD_A: a-columns per builder warp (1 or 2)
-  int tma_slots = 2;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4)
+  int tma_slots = 0;       // EBIC_TMA_SLOTS: pair vectors in flight per warp in the TMA index kernel (2..4; 0 auto)
   int table_kernel = 0;    // EBIC_TABLE_KERNEL: 0 auto (lane groups up to 32 slices, TMA warps up to 256; beyond: warps if many candidates, else CTAs), 1 register-load warps, 2 CTAs, 3 TMA, 4 lane groups (A/B)
   int simd_force = 0;     // forced packed-pair layout P*16+SUB (ebic_ctx_set_pair_layout / EBIC_PAIR_LAYOUT="P,SUB"); 0 = auto
   bool pdl = true;         // programmatic dependent launch of the count kernels (EBIC_PDL=0 disables)
@@ -958,8 +958,14 @@ int launch_table(ebic_ctx* ctx, const uint32_t* d_cols, const uint32_t* d_offs, 
     // completion (27.5 vs 31 us for the register-load warp kernel at C3, ncu).
     // The lazy index always runs here (S = 2).
     const uint32_t J = (nv + 31) / 32;
-    const int S = lazy ? 2 : ctx->tma_slots;
-    const size_t smem = (size_t)ebic::kTmaWarps * S * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512;
+    // slots per warp: 2 (more CTAs per SM) when warps loop over several
+    // candidates; 4 -- every pair of a candidate of up to 5 columns in one
+    // round of copies -- when there is about one candidate per warp and the
+    // launch is one latency-bound chain (measured: P = 392 +23%, C2 +6%)
+    auto slots_smem = [&](int k) { return (size_t)ebic::kTmaWarps * k * (neg ? 2 : 1) * table_wp(ctx) * 4 + 512; };
+    int S = lazy ? 2 : ctx->tma_slots ? ctx->tma_slots : n_cand <= (uint64_t)ctx->n_sms * 32 ? 4 : 2;
+    while (S > 2 && slots_smem(S) > ctx->smem_optin) --S;
+    const size_t smem = slots_smem(S);
     bool pdl = ctx->pdl;
     if (lazy && plan.la.cold && slab_build_fits(ctx) &&
         (n_cand >= kLazyColdMinCand || ctx->lazy_build == EBIC_LAZY_BUILD_FIRST)) {
