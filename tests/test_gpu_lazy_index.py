@@ -185,3 +185,38 @@ def test_auto_long_vectors_over_budget_use_lazy(evaluator):
         assert evaluator.index_stats()["lazy_bytes"] <= 256 << 20
     finally:
         evaluator.set_table_budget(0)
+
+
+def test_lazy_build_mode_is_validated(evaluator):
+    """ebic_ctx_set_lazy_build takes 0 (auto), 1 (inline) or 2 (build first);
+    anything else is an argument error that leaves the mode unchanged."""
+    from paper_2105_01196_b200 import EbicError
+
+    for bad in (-1, 3, 99):
+        with pytest.raises(EbicError):
+            evaluator.set_lazy_build(bad)
+    for ok in (2, 1, 0):
+        evaluator.set_lazy_build(ok)
+
+
+def test_cold_route_first_batch_then_steady(evaluator):
+    """AUTO: the first batch of a fresh lazy index takes the build-first route,
+    later batches of the same population find every pair in the pool; a new
+    population again brings new pairs.  Exact throughout, f32 and with zeros
+    (empty brackets) in the matrix."""
+    R, C = 9000, 300
+    m = _matrix(R, C, 23)
+    m[::5, ::7] = 0.0
+    evaluator.upload(m)
+    evaluator.set_path(EBIC_PATH_LAZY)
+    try:
+        pops = [_pop(C, 2000, seed=40 + k) for k in range(2)]
+        for k in (0, 0, 1, 0, 1):
+            pop = pops[k]
+            for neg in (False, True):
+                want = oracle.evaluate_population(m, pop.cols, pop.offsets, 0.03, neg)
+                got = evaluator.evaluate_population(pop, TrendParams(0.03, neg))
+                np.testing.assert_array_equal(got, want, err_msg=f"pop {k} neg {neg}")
+        assert evaluator.index_stats()["lazy_slots_used"] > 0
+    finally:
+        evaluator.set_path(EBIC_PATH_AUTO)
