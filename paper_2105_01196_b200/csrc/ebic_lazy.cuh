@@ -15,8 +15,10 @@
 //                    failed allocation still counts, so the host sees a full
 //                    pool and grows or resets it before the next batch)
 //
-// The count kernels resolve and build inside the evaluation (no extra kernel
-// per batch): a warp looks up its candidate's pairs in the map; ready vectors
+// Warm batches resolve and build inside the count kernel (no extra kernel per
+// batch); cold batches -- the pool still filling fast -- and long vectors run
+// claim / build / publish kernels first (lazy_slab_build_kernel, below).
+// Inside the count kernel a warp looks up its candidate's pairs in the map; ready vectors
 // are read from the pool exactly like full-index vectors; a missing vector is
 // built by the warp from the value store (the reference's own test,
 // trend.cpp:22: v_r(b) > v_r(a) - approx*|v_r(a)| in double with two rounded
@@ -40,10 +42,11 @@ constexpr uint32_t kSlotBusy = 0x80000000u;  // high bit: claimed, vector not ye
 
 struct LazyArgs {
   uint32_t* map;        // C x C slots
-  // long vectors only (lazy_claim_kernel / lazy_build_kernel): per pool slot,
-  // the pair it was claimed for and the claiming batch's tag (kSlotEmpty:
-  // not waiting to be built), the 32-word chunks still to build, and a ring
-  // of batch start counts (entry seq % kLazyStartRing)
+  // claim / build / publish kernels (long vectors, cold batches): per pool
+  // slot, the pair it was claimed for and the claiming batch's tag
+  // (kSlotEmpty: not waiting to be built), the 32-word chunks still to build
+  // (lazy_build_kernel), and a ring of batch windows: start[seq % ring] = the
+  // count before the batch's claims, start[ring + seq % ring] = after them
   uint32_t* keys;
   uint32_t* left;
   const uint32_t* start;
