@@ -220,3 +220,27 @@ def test_cold_route_first_batch_then_steady(evaluator):
         assert evaluator.index_stats()["lazy_slots_used"] > 0
     finally:
         evaluator.set_path(EBIC_PATH_AUTO)
+
+
+@pytest.mark.parametrize("R", [4000, 33000])
+def test_build_first_wide_matrix(evaluator, R):
+    """The build-first route on a matrix too wide for two slab-builder CTAs per
+    SM (1800 columns: the 1024-thread variant), short and long vectors,
+    forward and reversed pairs, counts and row masks."""
+    C = 1800
+    m = _matrix(R, C, 29)
+    evaluator.upload(m)
+    evaluator.set_path(EBIC_PATH_LAZY)
+    evaluator.set_lazy_build(2)
+    try:
+        pop = _pop(C, 600, seed=7)
+        for approx, neg in ((0.03, False), (0.0, True)):
+            want = oracle.evaluate_population(m, pop.cols, pop.offsets, approx, neg)
+            got = evaluator.evaluate_population(pop, TrendParams(approx, neg))
+            np.testing.assert_array_equal(got, want, err_msg=f"R={R} approx={approx} neg={neg}")
+        for j in (0, 3):
+            rows = evaluator.supporting_rows(pop.sequence(j), TrendParams(0.03, True))
+            np.testing.assert_array_equal(rows, oracle.supporting_rows(m, pop.sequence(j), 0.03, True))
+    finally:
+        evaluator.set_lazy_build(0)
+        evaluator.set_path(EBIC_PATH_AUTO)
