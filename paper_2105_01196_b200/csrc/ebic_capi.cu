@@ -464,9 +464,6 @@ uint64_t index_budget(const ebic_ctx* ctx, uint64_t avail) {
 
 constexpr int kTableNoMemory = -1;  // internal status: the index does not fit (fall back)
 
-// Words per pair vector: a multiple of 4 (uint4 slices); vectors of more than
-// 32 slices are padded to a multiple of 32 slices, so the warp kernel's lanes
-// own exactly J = nv / 32 slices each (unpredicated loads).
 // Words per pair vector: whole uint4 slices, and whole 32-slice groups (128
 // words, 512 B) above 128 words -- the register-load kernels read those with
 // unpredicated loads, and the TMA kernel measured faster on 512-B-aligned
